@@ -1,0 +1,205 @@
+/*
+ * saturn.h -- C ABI of the B200-native SPASE plan evaluator and searcher.
+ *
+ * SPASE (§4.1) asks, for every training job, for a parallelism (UPP), a
+ * GPU count, a node and a start time that together minimise the makespan, given the
+ * profiled runtime table (Table 1).  This library evaluates and searches
+ * candidate plans in bulk on one B200 per process:
+ *
+ *   a plan = a GENOME: cfg[t] in [0, S_t) picks job t's configuration (one config per job,
+ *   Eq. 3) and perm[0..T) is a priority permutation of the job ids.  A genome
+ *   is turned into a schedule by the list-scheduling DECODER (reading A6): in
+ *   priority order each job with config (g, R) starts at the g-th smallest free time of the
+ *   node where that start is earliest (ties -> lowest node id), takes the g GPUs of that
+ *   node free by then with the latest free times (ties -> lower GPU id), and holds them for
+ *   [s, s+R).  The makespan is max_t (s_t + R_t) (Eq. 2).  Every decoded plan
+ *   satisfies Eqs. 3-11: one node, exactly g GPUs, one gang start, no overlap on a GPU.
+ *
+ * Conventions
+ *   - Every function is extern "C", returns saturn_status, never throws, never aborts.
+ *     On failure saturn_last_error(p) describes the cause (owned by the handle, valid until
+ *     the next call on it).
+ *   - Host pointers are caller-owned; the library copies what it needs during the call.
+ *     Pointers documented "device" are caller-owned CUDA device memory on the handle's
+ *     device (e.g. torch tensor storage); the library never frees them.
+ *   - Streams are caller-owned cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Device-output calls are stream-ordered and asynchronous; calls with host outputs
+ *     synchronise the stream before returning.
+ *   - Integers: runtimes are int32 seconds (reading A4/A5: integer time loses nothing).
+ *   - A handle is not thread safe; distinct handles are independent.
+ *   - Limits: 1 <= n_nodes, sum_n GPU_n <= 32; 1 <= T <= 255 jobs (u8 genes); R < 2^24 s;
+ *     sum_t max_s R < 2^26 s (packed (makespan, index) keys); <= 255 configs per job;
+ *     the packed table (4 B per (job, config) + 2 B per job) <= 48 KB.
+ */
+#ifndef SATURN_H
+#define SATURN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct saturn_plan saturn_plan; /* opaque; owns the device table and workspaces */
+
+typedef enum {
+  SATURN_OK = 0,
+  SATURN_EINVAL = 1,          /* bad argument or table value (message names it)            */
+  SATURN_EUNSCHEDULABLE = 2,  /* a job has no feasible config fitting any node */
+  SATURN_ELIMIT = 3,          /* a size limit (enumeration space, shared memory) exceeded   */
+  SATURN_ECUDA = 4,           /* CUDA runtime error (message = cudaGetErrorString)          */
+  SATURN_ENCCL = 5,           /* NCCL error or NCCL library not loadable                    */
+  SATURN_ESTATE = 6           /* call out of order (e.g. evaluate before a table is loaded) */
+} saturn_status;
+
+/* saturn_result.flags */
+enum { SATURN_PROVEN_OPTIMAL = 1, SATURN_INCUMBENT = 2 };
+
+/* saturn_set_decoder kinds (row a5: two device designs, chosen by measurement) */
+enum { SATURN_DECODER_AUTO = 0, SATURN_DECODER_THREAD = 1, SATURN_DECODER_WARP = 2 };
+
+/* One job of a decoded plan = the paper's per-task outputs (Table 1 B, O, P,
+ * I): node n (O), UPP index and GPU count of the chosen config, the config index s into the
+ * job's compacted list (B), the gang start I and end I + R, and bit g of gpu_mask set iff
+ * the job holds GPU g of its node (P).  32 bytes. */
+typedef struct {
+  int32_t node;
+  int32_t upp;
+  int32_t gpus;
+  int32_t cfg;
+  int32_t start_s;
+  int32_t end_s;
+  uint64_t gpu_mask;
+} saturn_placement;
+
+typedef struct {
+  int64_t makespan;       /* best makespan found (seconds)                              */
+  uint64_t genome_index;  /* enumerate: index of the best genome (smallest on ties)     */
+  uint64_t evaluated;     /* full decodes performed by this call, all ranks             */
+  double seconds;         /* wall time of the call                                      */
+  int32_t flags;          /* SATURN_PROVEN_OPTIMAL (enumerate) | SATURN_INCUMBENT (search) */
+  int32_t generations;    /* search: generations run                                    */
+} saturn_result;
+
+/* Genetic search parameters (row a7).  Probabilities are q32
+ * thresholds: an event fires iff a Philox u32 < threshold. */
+typedef struct {
+  uint64_t seed;
+  int64_t population;            /* genomes per GPU, >= 64 and >= 2 * elites            */
+  int64_t max_generations;       /* generations after the initial population (>= 0)     */
+  double time_budget_s;          /* stop at the first epoch boundary past this; 0 = none */
+  int32_t elites;                /* 1..32 genomes carried unchanged to the next generation */
+  int32_t generations_per_epoch; /* island migration period (multi-GPU), >= 1           */
+  uint32_t p_xover_q32;          /* crossover probability                               */
+  uint32_t p_cfg_mut_q32;        /* per-job config mutation probability                  */
+  uint32_t p_perm_mut_q32;       /* per-child permutation mutation probability           */
+  const uint8_t *seed_cfg;       /* host [n_seed][T] genomes placed first, or NULL        */
+  const uint8_t *seed_perm;      /* host [n_seed][T]                                      */
+  int64_t n_seed;
+} saturn_search_params;
+
+/* Create a handle for a cluster of n_nodes nodes with node_gpus[n] GPUs each (Table 1: N,
+ * GPU_n) on CUDA device `cuda_device`.
+ * EINVAL: n_nodes < 1, any GPU_n < 1, sum GPU_n > 32.  ECUDA: device not usable. */
+saturn_status saturn_plan_create(const int32_t *node_gpus, int32_t n_nodes, int32_t cuda_device,
+                                 saturn_plan **out);
+
+/* Load the profiled runtime table (row a1; Table 1 G_t, R_t; the Trial Runner grid over
+ * "all supported parallelisms and GPU apportionment levels").
+ * runtime_s: host int32 [n_jobs][n_upps][max_gpus], entry [t][u][g-1] = runtime of job t
+ * under UPP u on g GPUs; <= 0 marks an infeasible (null) profile.
+ * The table is compacted (row a2): job t's configs are its feasible entries with
+ * g <= max_n GPU_n (single-node jobs) in UPP-major, ascending-g order
+ * (SPEC.md:52); config index s in genomes and placements refers to this order.
+ * EINVAL: n_jobs not in [1,255], n_upps < 1, max_gpus < 1, R >= 2^24, sum_t max_s R >= 2^26,
+ * > 255 configs for a job; EUNSCHEDULABLE: a job with no feasible config (message names it);
+ * ELIMIT: packed table > 48 KB.  Replaces any previous table and search state. */
+saturn_status saturn_load_runtime_table(saturn_plan *p, const int32_t *runtime_s, int32_t n_jobs,
+                                        int32_t n_upps, int32_t max_gpus);
+
+/* Shape of the compacted table: n_jobs and S_t (configs per job, host int32 [n_jobs], may
+ * be NULL).  ESTATE before a table is loaded. */
+saturn_status saturn_num_configs(const saturn_plan *p, int32_t *n_jobs, int32_t *configs_per_job);
+
+/* Compacted config s of job t: UPP index, GPU count and runtime.  EINVAL if out of range. */
+saturn_status saturn_config(const saturn_plan *p, int32_t job, int32_t cfg, int32_t *upp, int32_t *gpus,
+                            int32_t *runtime_s);
+
+/* Select the device decoder design for evaluate (AUTO = thread design when compiled for the
+ * cluster shape, else warp).  EINVAL for an unknown kind. */
+saturn_status saturn_set_decoder(saturn_plan *p, int32_t kind);
+
+/* Decode n genomes (row a5).  d_cfg, d_perm: device uint8 [n][T] (genome-major rows);
+ * d_makespan: device int32 [n].  An invalid genome (perm not a permutation of 0..T-1, or
+ * cfg[t] >= S_t) yields makespan -1.  Asynchronous on `stream`.  ESTATE without a table. */
+saturn_status saturn_evaluate(saturn_plan *p, const uint8_t *d_cfg, const uint8_t *d_perm, int64_t n,
+                              int32_t *d_makespan, void *stream);
+
+/* Same with HOST buffers: copies genomes host->device and makespans device->host inside the
+ * call (staged through the handle's device workspace); synchronous. */
+saturn_status saturn_evaluate_host(saturn_plan *p, const uint8_t *h_cfg, const uint8_t *h_perm, int64_t n,
+                                   int32_t *h_makespan, void *stream);
+
+/* Trace-decode n genomes (row a8) into device placements [n][T] (saturn_placement, job-id
+ * order) and device makespans [n].  Invalid genomes: makespan -1, placements unwritten. */
+saturn_status saturn_trace(saturn_plan *p, const uint8_t *d_cfg, const uint8_t *d_perm, int64_t n,
+                           saturn_placement *d_placements, int32_t *d_makespan, void *stream);
+
+/* Size of the genome space, T! * prod_t S_t, if it is < 2^64 (else ELIMIT). */
+saturn_status saturn_space_size(const saturn_plan *p, uint64_t *size);
+
+/* Exhaustive enumeration (row a4-ii + a5 + a6): the minimum makespan over every genome and
+ * the smallest genome index attaining it (reading A7).  Genome index G -> genome:
+ * r_cfg = G mod prod S, r_perm = G div prod S, cfg[t] = (r_cfg div prod_{t'<t} S_t') mod S_t,
+ * perm = lexicographic unrank of r_perm.  With an attached communicator the space is split
+ * into `world` contiguous slices and the (makespan << 38 | index) keys are min-all-reduced
+ * over NCCL; the result is identical for every world size.  ELIMIT if the space exceeds
+ * max_genomes or 2^38, or T > 20.  flags = SATURN_PROVEN_OPTIMAL.  Synchronous. */
+saturn_status saturn_enumerate(saturn_plan *p, uint64_t max_genomes, void *stream, saturn_result *out);
+
+/* Enumerate only genome indices [begin, end) on this device (no collective). */
+saturn_status saturn_enumerate_range(saturn_plan *p, uint64_t begin, uint64_t end, void *stream,
+                                     saturn_result *out);
+
+/* Genetic search (rows a4-iii, a5, a6, a7): an initial
+ * population, then max_generations generations of Philox tournament selection, uniform /
+ * OX1 crossover and mutation, every child decoded on the device, the elites carried over.
+ * With an attached communicator each GPU runs an island and every generations_per_epoch
+ * generations the elites of all islands are all-gathered and every island continues from the
+ * global best E.  Deterministic for fixed (params, world size).  flags = SATURN_INCUMBENT.
+ * Synchronous.  EINVAL for bad params; ESTATE without a table. */
+saturn_status saturn_search(saturn_plan *p, const saturn_search_params *sp, void *stream, saturn_result *out);
+
+/* Best-so-far curve of the last search: up to n_max (seconds since the call, makespan)
+ * pairs, one per epoch; *n_out = number written. */
+saturn_status saturn_search_history(const saturn_plan *p, int64_t n_max, double *t_s, int64_t *makespan,
+                                    int64_t *n_out);
+
+/* Final population of the last search on this device: host uint8 cfg [P][T], perm [P][T],
+ * int32 makespan [P].  (Used for operator-replay parity.)  ESTATE before a search. */
+saturn_status saturn_search_population(const saturn_plan *p, uint8_t *h_cfg, uint8_t *h_perm,
+                                       int32_t *h_makespan);
+
+/* The best plan of the last enumerate/search (row a8): placements host [T] (job-id order),
+ * genome_out host [2T] (cfg then perm) or NULL, makespan.  ESTATE before any search. */
+saturn_status saturn_best_plan(saturn_plan *p, saturn_placement *out, uint8_t *genome_out, int64_t *makespan);
+
+/* Multi-GPU (row e): rank 0 creates an NCCL unique id (128 bytes), the caller broadcasts it
+ * (e.g. torch.distributed), then every rank attaches.  ENCCL if NCCL cannot be loaded. */
+saturn_status saturn_get_unique_id(uint8_t *id128);
+saturn_status saturn_plan_attach_comm(saturn_plan *p, const uint8_t *id128, int32_t rank, int32_t world);
+
+/* Contiguous slice [begin, end) of [0, total) owned by `rank` of `world` (pure host). */
+saturn_status saturn_partition(uint64_t total, int32_t rank, int32_t world, uint64_t *begin, uint64_t *end);
+
+/* Integer-ALU throughput probe on the handle's device: independent IMNMX/IADD3/ISETP/SEL
+ * chains; *int_ops_per_s = measured integer operations per second (roofline check). */
+saturn_status saturn_probe_int_peak(saturn_plan *p, double *int_ops_per_s);
+
+const char *saturn_last_error(const saturn_plan *p);
+void saturn_plan_destroy(saturn_plan *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SATURN_H */

@@ -1,0 +1,783 @@
+// libsaturn host runtime: the C ABI of include/saturn.h (row b), table validation and
+// compaction (rows a1/a2), workspace management, the search epoch loop and the NCCL
+// island exchange (row e).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/saturn.h"
+#include "kernels.h"
+
+using sat::Problem;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed)
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (tried) return n;
+  tried = true;
+  // Prefer the NCCL already loaded in the process (torch's), else the system one.
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    n.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return n;
+  }
+#define SAT_SYM(field, name) n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name));
+  SAT_SYM(getUniqueId, "ncclGetUniqueId")
+  SAT_SYM(commInitRank, "ncclCommInitRank")
+  SAT_SYM(allReduce, "ncclAllReduce")
+  SAT_SYM(allGather, "ncclAllGather")
+  SAT_SYM(commDestroy, "ncclCommDestroy")
+  SAT_SYM(getErrorString, "ncclGetErrorString")
+#undef SAT_SYM
+  n.ok = n.getUniqueId && n.commInitRank && n.allReduce && n.allGather && n.commDestroy && n.getErrorString;
+  if (!n.ok) n.why = "libnccl is missing required symbols";
+  return n;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+struct saturn_plan {
+  int device = 0;
+  int sms = 148;
+  std::vector<int> gpu_n;
+  int sumG = 0, maxG = 0;
+  // compacted table
+  bool loaded = false;
+  int T = 0, stride = 0;
+  std::vector<int> S, cfg_g, cfg_r, cfg_u;   // [T], [T*stride] x3
+  int NN = 0, GP = 0;
+  bool sorted_ok = false;
+  int decoder = SATURN_DECODER_AUTO;
+  DevBuf<uint8_t> blob;
+  int blob_bytes = 0;
+  Problem pb{};
+  // workspaces
+  DevBuf<uint8_t> ws_cfg, ws_perm;
+  DevBuf<int32_t> ws_ms;
+  DevBuf<unsigned long long> ws_key;
+  DevBuf<saturn_placement> ws_place;
+  DevBuf<uint8_t> pop[2];
+  DevBuf<int32_t> pms[2];
+  DevBuf<unsigned long long> cand;
+  DevBuf<int32_t> rec_ms, all_ms;
+  DevBuf<uint8_t> rec_gen, all_gen, seeds;
+  DevBuf<int> sink;
+  // results
+  bool have_best = false;
+  std::vector<uint8_t> best_cfg, best_perm;
+  int64_t best_ms = -1;
+  bool have_pop = false;
+  int last_pop = 0;
+  int64_t pop_P = 0;
+  int pop_GS = 0;
+  std::vector<double> hist_t;
+  std::vector<int64_t> hist_ms;
+  // communicator
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  std::string err;
+};
+
+namespace {
+
+saturn_status fail(saturn_plan* p, saturn_status s, const char* fmt, ...) {
+  if (p) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    p->err = buf;
+  }
+  return s;
+}
+
+#define CU(p, call)                                                                                   \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess) return fail(p, SATURN_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));     \
+  } while (0)
+
+#define NC(p, call)                                                                                   \
+  do {                                                                                                \
+    ncclResult_t r_ = (call);                                                                         \
+    if (r_ != ncclSuccess) return fail(p, SATURN_ENCCL, "%s: %s", #call, nccl().getErrorString(r_)); \
+  } while (0)
+
+int pow2_at_least(int x) {
+  int v = 1;
+  while (v < x) v <<= 1;
+  return v;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int gs_of(int T) { return ((2 * T) + 15) & ~15; }
+
+saturn_status use_decoder_kind(saturn_plan* p, int* kind) {
+  int k = p->decoder;
+  if (k == SATURN_DECODER_AUTO) k = p->sorted_ok ? SATURN_DECODER_THREAD : SATURN_DECODER_WARP;
+  if (k == SATURN_DECODER_THREAD && !p->sorted_ok)
+    return fail(p, SATURN_EINVAL, "thread decoder not compiled for %d nodes x %d GPUs (padded)", p->NN, p->GP);
+  *kind = k;
+  return SATURN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+saturn_status saturn_plan_create(const int32_t* node_gpus, int32_t n_nodes, int32_t cuda_device, saturn_plan** out) {
+  if (!out) return SATURN_EINVAL;
+  *out = nullptr;
+  if (!node_gpus || n_nodes < 1 || n_nodes > sat::MAX_NODES) return SATURN_EINVAL;
+  int sum = 0, mx = 0;
+  for (int n = 0; n < n_nodes; ++n) {
+    if (node_gpus[n] < 1) return SATURN_EINVAL;
+    sum += node_gpus[n];
+    mx = std::max(mx, (int)node_gpus[n]);
+  }
+  if (sum > sat::MAX_GPUS) return SATURN_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
+    cudaGetLastError();
+    return SATURN_ECUDA;
+  }
+  saturn_plan* p = new saturn_plan();
+  p->device = cuda_device;
+  p->gpu_n.assign(node_gpus, node_gpus + n_nodes);
+  p->sumG = sum;
+  p->maxG = mx;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) {
+    delete p;
+    return SATURN_ECUDA;
+  }
+  p->sms = prop.multiProcessorCount;
+  *out = p;
+  return SATURN_OK;
+}
+
+saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s, int32_t n_jobs, int32_t n_upps,
+                                        int32_t max_gpus) {
+  if (!p) return SATURN_EINVAL;
+  if (!runtime_s) return fail(p, SATURN_EINVAL, "runtime_s is NULL");
+  if (n_jobs < 1 || n_jobs > sat::MAX_JOBS) return fail(p, SATURN_EINVAL, "n_jobs=%d not in [1,255]", n_jobs);
+  if (n_upps < 1) return fail(p, SATURN_EINVAL, "n_upps=%d < 1", n_upps);
+  if (max_gpus < 1) return fail(p, SATURN_EINVAL, "max_gpus=%d < 1", max_gpus);
+  DeviceGuard dg(p->device);
+  p->loaded = false;
+  p->have_best = false;
+  p->have_pop = false;
+  const int T = n_jobs;
+  std::vector<std::vector<int>> gs(T), rs(T), us(T);
+  int64_t sum_max = 0;
+  for (int t = 0; t < T; ++t) {
+    int rmax = 0;
+    for (int u = 0; u < n_upps; ++u)
+      for (int g = 1; g <= max_gpus; ++g) {
+        const int32_t r = runtime_s[((int64_t)t * n_upps + u) * max_gpus + (g - 1)];
+        if (r <= 0 || g > p->maxG) continue;
+        if (r >= (1 << 24))
+          return fail(p, SATURN_EINVAL, "runtime[%d][%d][%d]=%d >= 2^24 s", t, u, g - 1, r);
+        gs[t].push_back(g);
+        rs[t].push_back(r);
+        us[t].push_back(u);
+        rmax = std::max(rmax, (int)r);
+      }
+    if (gs[t].empty())
+      return fail(p, SATURN_EUNSCHEDULABLE, "job %d has no feasible configuration fitting a node", t);
+    if (gs[t].size() > 255) return fail(p, SATURN_EINVAL, "job %d has %zu > 255 configurations", t, gs[t].size());
+    sum_max += rmax;
+  }
+  if (sum_max >= (int64_t(1) << 26))
+    return fail(p, SATURN_EINVAL, "sum of per-job max runtimes %lld >= 2^26 s", (long long)sum_max);
+  int stride = 0;
+  for (int t = 0; t < T; ++t) stride = std::max(stride, (int)gs[t].size());
+  const int raw = 4 * T * stride + T + T * stride;
+  const int bytes = (raw + 15) & ~15;
+  if (bytes > 48 * 1024) return fail(p, SATURN_ELIMIT, "packed table %d B > 48 KB", bytes);
+
+  std::vector<uint8_t> blob(bytes, 0);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(blob.data());
+  uint8_t* Sb = blob.data() + 4 * T * stride;
+  uint8_t* upp = Sb + T;
+  p->S.assign(T, 0);
+  p->cfg_g.assign(T * stride, 0);
+  p->cfg_r.assign(T * stride, 0);
+  p->cfg_u.assign(T * stride, -1);
+  for (int t = 0; t < T; ++t) {
+    p->S[t] = (int)gs[t].size();
+    Sb[t] = (uint8_t)gs[t].size();
+    for (size_t s = 0; s < gs[t].size(); ++s) {
+      tab[t * stride + s] = ((uint32_t)gs[t][s] << 24) | (uint32_t)rs[t][s];
+      upp[t * stride + s] = (uint8_t)us[t][s];
+      p->cfg_g[t * stride + s] = gs[t][s];
+      p->cfg_r[t * stride + s] = rs[t][s];
+      p->cfg_u[t * stride + s] = us[t][s];
+    }
+  }
+  CU(p, p->blob.ensure(bytes));
+  CU(p, cudaMemcpy(p->blob.p, blob.data(), bytes, cudaMemcpyHostToDevice));
+  p->T = T;
+  p->stride = stride;
+  p->blob_bytes = bytes;
+  Problem pb{};
+  pb.blob = p->blob.p;
+  pb.blob_bytes = bytes;
+  pb.T = T;
+  pb.stride = stride;
+  pb.N = (int)p->gpu_n.size();
+  pb.sumG = p->sumG;
+  for (int n = 0; n < pb.N; ++n) pb.gpu_n[n] = (int8_t)p->gpu_n[n];
+  p->pb = pb;
+  p->GP = std::max(2, pow2_at_least(p->maxG));
+  p->NN = pow2_at_least((int)p->gpu_n.size());
+  p->sorted_ok = sat::have_sorted_shape(p->NN, p->GP);
+  if (sat::eval_smem_bytes(pb) > 227 * 1024) return fail(p, SATURN_ELIMIT, "evaluate tile exceeds shared memory");
+  p->loaded = true;
+  return SATURN_OK;
+}
+
+saturn_status saturn_num_configs(const saturn_plan* p, int32_t* n_jobs, int32_t* configs_per_job) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return SATURN_ESTATE;
+  if (n_jobs) *n_jobs = p->T;
+  if (configs_per_job)
+    for (int t = 0; t < p->T; ++t) configs_per_job[t] = p->S[t];
+  return SATURN_OK;
+}
+
+saturn_status saturn_config(const saturn_plan* p, int32_t job, int32_t cfg, int32_t* upp, int32_t* gpus,
+                            int32_t* runtime_s) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return SATURN_ESTATE;
+  if (job < 0 || job >= p->T || cfg < 0 || cfg >= p->S[job]) return SATURN_EINVAL;
+  const int k = job * p->stride + cfg;
+  if (upp) *upp = p->cfg_u[k];
+  if (gpus) *gpus = p->cfg_g[k];
+  if (runtime_s) *runtime_s = p->cfg_r[k];
+  return SATURN_OK;
+}
+
+saturn_status saturn_set_decoder(saturn_plan* p, int32_t kind) {
+  if (!p) return SATURN_EINVAL;
+  if (kind < SATURN_DECODER_AUTO || kind > SATURN_DECODER_WARP) return fail(p, SATURN_EINVAL, "decoder %d", kind);
+  p->decoder = kind;
+  return SATURN_OK;
+}
+
+saturn_status saturn_evaluate(saturn_plan* p, const uint8_t* d_cfg, const uint8_t* d_perm, int64_t n,
+                              int32_t* d_makespan, void* stream) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "evaluate before load_runtime_table");
+  if (n < 0) return fail(p, SATURN_EINVAL, "n < 0");
+  if (n == 0) return SATURN_OK;
+  if (!d_cfg || !d_perm || !d_makespan) return fail(p, SATURN_EINVAL, "NULL buffer");
+  int kind;
+  saturn_status s = use_decoder_kind(p, &kind);
+  if (s != SATURN_OK) return s;
+  DeviceGuard dg(p->device);
+  CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, kind, d_cfg, d_perm, n, d_makespan, p->sms,
+                             static_cast<cudaStream_t>(stream)));
+  return SATURN_OK;
+}
+
+saturn_status saturn_evaluate_host(saturn_plan* p, const uint8_t* h_cfg, const uint8_t* h_perm, int64_t n,
+                                   int32_t* h_makespan, void* stream) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "evaluate before load_runtime_table");
+  if (n < 0) return fail(p, SATURN_EINVAL, "n < 0");
+  if (n == 0) return SATURN_OK;
+  if (!h_cfg || !h_perm || !h_makespan) return fail(p, SATURN_EINVAL, "NULL buffer");
+  int kind;
+  saturn_status s = use_decoder_kind(p, &kind);
+  if (s != SATURN_OK) return s;
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 24);
+  CU(p, p->ws_cfg.ensure(chunk * p->T));
+  CU(p, p->ws_perm.ensure(chunk * p->T));
+  CU(p, p->ws_ms.ensure(chunk));
+  for (int64_t off = 0; off < n; off += chunk) {
+    const int64_t m = std::min(chunk, n - off);
+    CU(p, cudaMemcpyAsync(p->ws_cfg.p, h_cfg + off * p->T, m * p->T, cudaMemcpyHostToDevice, st));
+    CU(p, cudaMemcpyAsync(p->ws_perm.p, h_perm + off * p->T, m * p->T, cudaMemcpyHostToDevice, st));
+    CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, kind, p->ws_cfg.p, p->ws_perm.p, m, p->ws_ms.p, p->sms, st));
+    CU(p, cudaMemcpyAsync(h_makespan + off, p->ws_ms.p, m * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  CU(p, cudaStreamSynchronize(st));
+  return SATURN_OK;
+}
+
+saturn_status saturn_trace(saturn_plan* p, const uint8_t* d_cfg, const uint8_t* d_perm, int64_t n,
+                           saturn_placement* d_placements, int32_t* d_makespan, void* stream) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "trace before load_runtime_table");
+  if (n < 0) return fail(p, SATURN_EINVAL, "n < 0");
+  if (n == 0) return SATURN_OK;
+  if (!d_cfg || !d_perm || !d_placements || !d_makespan) return fail(p, SATURN_EINVAL, "NULL buffer");
+  DeviceGuard dg(p->device);
+  CU(p, sat::launch_trace(p->pb, d_cfg, d_perm, n, d_placements, d_makespan, p->sms,
+                          static_cast<cudaStream_t>(stream)));
+  return SATURN_OK;
+}
+
+saturn_status saturn_space_size(const saturn_plan* p, uint64_t* size) {
+  if (!p || !size) return SATURN_EINVAL;
+  if (!p->loaded) return SATURN_ESTATE;
+  unsigned __int128 v = 1;
+  for (int k = 2; k <= p->T; ++k) {
+    v *= (unsigned)k;
+    if (v >> 64) return SATURN_ELIMIT;
+  }
+  for (int t = 0; t < p->T; ++t) {
+    v *= (unsigned)p->S[t];
+    if (v >> 64) return SATURN_ELIMIT;
+  }
+  *size = (uint64_t)v;
+  return SATURN_OK;
+}
+
+namespace {
+
+// Host unrank of a genome index (same definition as the device kernel; used only to
+// materialise the winner for best_plan).
+void unrank_host(const saturn_plan* p, uint64_t G, std::vector<uint8_t>& cfg, std::vector<uint8_t>& perm) {
+  const int T = p->T;
+  uint64_t cs = 1;
+  for (int t = 0; t < T; ++t) cs *= (uint64_t)p->S[t];
+  uint64_t rc = G % cs, rp = G / cs;
+  cfg.assign(T, 0);
+  perm.assign(T, 0);
+  for (int t = 0; t < T; ++t) {
+    cfg[t] = (uint8_t)(rc % (uint64_t)p->S[t]);
+    rc /= (uint64_t)p->S[t];
+  }
+  std::vector<int> avail(T);
+  for (int t = 0; t < T; ++t) avail[t] = t;
+  for (int i = 0; i < T; ++i) {
+    uint64_t f = 1;
+    for (int k = 2; k <= T - 1 - i; ++k) f *= (uint64_t)k;
+    const uint64_t d = rp / f;
+    rp %= f;
+    perm[i] = (uint8_t)avail[d];
+    avail.erase(avail.begin() + (long)d);
+  }
+}
+
+saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint64_t total, bool collective,
+                             cudaStream_t st, saturn_result* out) {
+  const double t0 = now_s();
+  sat::EnumSpace es{};
+  es.cfg_space = 1;
+  for (int t = 0; t < p->T; ++t) {
+    es.radix[t] = es.cfg_space;
+    es.cfg_space *= (uint64_t)p->S[t];
+  }
+  es.fact[0] = 1;
+  for (int k = 1; k <= p->T; ++k) es.fact[k] = es.fact[k - 1] * (uint64_t)k;
+  int kind;
+  saturn_status s = use_decoder_kind(p, &kind);
+  if (s != SATURN_OK) return s;
+  if (kind != SATURN_DECODER_THREAD)
+    return fail(p, SATURN_EINVAL, "enumerate needs the thread decoder for this cluster shape");
+  CU(p, p->ws_key.ensure(1));
+  CU(p, cudaMemsetAsync(p->ws_key.p, 0xff, sizeof(unsigned long long), st));
+  CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, p->ws_key.p, p->sms, st));
+  if (collective && p->comm) {
+    NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
+  }
+  unsigned long long key = 0;
+  CU(p, cudaMemcpyAsync(&key, p->ws_key.p, sizeof key, cudaMemcpyDeviceToHost, st));
+  CU(p, cudaStreamSynchronize(st));
+  if (out) {
+    memset(out, 0, sizeof *out);
+    out->evaluated = collective ? total : (end - begin);
+    out->seconds = now_s() - t0;
+    out->flags = SATURN_PROVEN_OPTIMAL;
+  }
+  if (key == ~0ull) {  // empty range
+    if (out) out->makespan = -1;
+    return SATURN_OK;
+  }
+  const uint64_t idx = key & ((uint64_t(1) << 38) - 1);
+  const int64_t ms = (int64_t)(key >> 38);
+  unrank_host(p, idx, p->best_cfg, p->best_perm);
+  p->best_ms = ms;
+  p->have_best = true;
+  if (out) {
+    out->makespan = ms;
+    out->genome_index = idx;
+  }
+  return SATURN_OK;
+}
+
+}  // namespace
+
+saturn_status saturn_enumerate(saturn_plan* p, uint64_t max_genomes, void* stream, saturn_result* out) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "enumerate before load_runtime_table");
+  if (p->T > sat::ENUM_MAX_T) return fail(p, SATURN_ELIMIT, "T=%d > %d jobs for enumeration", p->T, sat::ENUM_MAX_T);
+  uint64_t size = 0;
+  if (saturn_space_size(p, &size) != SATURN_OK || size >= (uint64_t(1) << 38))
+    return fail(p, SATURN_ELIMIT, "genome space too large for enumeration (>= 2^38)");
+  if (size > max_genomes)
+    return fail(p, SATURN_ELIMIT, "genome space %llu exceeds max_genomes %llu", (unsigned long long)size,
+                (unsigned long long)max_genomes);
+  DeviceGuard dg(p->device);
+  uint64_t b = 0, e = size;
+  saturn_partition(size, p->rank, p->world, &b, &e);
+  return enumerate_impl(p, b, e, size, true, static_cast<cudaStream_t>(stream), out);
+}
+
+saturn_status saturn_enumerate_range(saturn_plan* p, uint64_t begin, uint64_t end, void* stream, saturn_result* out) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "enumerate before load_runtime_table");
+  if (p->T > sat::ENUM_MAX_T) return fail(p, SATURN_ELIMIT, "T=%d > %d jobs for enumeration", p->T, sat::ENUM_MAX_T);
+  uint64_t size = 0;
+  if (saturn_space_size(p, &size) != SATURN_OK || size >= (uint64_t(1) << 38))
+    return fail(p, SATURN_ELIMIT, "genome space too large for enumeration (>= 2^38)");
+  if (begin > end || end > size) return fail(p, SATURN_EINVAL, "range [%llu,%llu) outside [0,%llu)",
+                                             (unsigned long long)begin, (unsigned long long)end,
+                                             (unsigned long long)size);
+  DeviceGuard dg(p->device);
+  return enumerate_impl(p, begin, end, size, false, static_cast<cudaStream_t>(stream), out);
+}
+
+saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "search before load_runtime_table");
+  if (!sp) return fail(p, SATURN_EINVAL, "params is NULL");
+  const int64_t P = sp->population;
+  const int E = sp->elites;
+  if (E < 1 || E > 32) return fail(p, SATURN_EINVAL, "elites=%d not in [1,32]", E);
+  if (P < 64 || P < 2 * E || P > (int64_t(1) << 31) - 1)
+    return fail(p, SATURN_EINVAL, "population=%lld must be in [max(64, 2*elites), 2^31)", (long long)P);
+  if (sp->max_generations < 0) return fail(p, SATURN_EINVAL, "max_generations < 0");
+  if (sp->generations_per_epoch < 1) return fail(p, SATURN_EINVAL, "generations_per_epoch < 1");
+  if (sp->n_seed < 0 || (sp->n_seed > 0 && (!sp->seed_cfg || !sp->seed_perm)))
+    return fail(p, SATURN_EINVAL, "bad seed genomes");
+  if (!p->sorted_ok) return fail(p, SATURN_EINVAL, "search needs the thread decoder for this cluster shape");
+  const int T = p->T;
+  const int GS = gs_of(T);
+  for (int64_t i = 0; i < sp->n_seed; ++i) {  // seed genomes must be valid
+    std::vector<int> seen(T, 0);
+    for (int k = 0; k < T; ++k) {
+      const int t = sp->seed_perm[i * T + k];
+      if (t >= T || seen[t]++) return fail(p, SATURN_EINVAL, "seed genome %lld: perm is not a permutation", (long long)i);
+      if (sp->seed_cfg[i * T + t] >= p->S[t]) return fail(p, SATURN_EINVAL, "seed genome %lld: cfg out of range", (long long)i);
+    }
+  }
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double t0 = now_s();
+  for (int b = 0; b < 2; ++b) {
+    CU(p, p->pop[b].ensure((size_t)P * GS));
+    CU(p, p->pms[b].ensure((size_t)P));
+  }
+  CU(p, p->cand.ensure((size_t)p->sms * 64 * 4 * 32 + 1024));
+  CU(p, p->rec_ms.ensure(E));
+  CU(p, p->rec_gen.ensure((size_t)E * GS));
+  CU(p, p->all_ms.ensure((size_t)E * p->world));
+  CU(p, p->all_gen.ensure((size_t)E * GS * p->world));
+  const int64_t n_seed = std::min<int64_t>(sp->n_seed, P);
+  if (n_seed > 0) {
+    std::vector<uint8_t> packed((size_t)n_seed * GS, 0);
+    for (int64_t i = 0; i < n_seed; ++i) {
+      memcpy(&packed[i * GS], sp->seed_cfg + i * T, T);
+      memcpy(&packed[i * GS + T], sp->seed_perm + i * T, T);
+    }
+    CU(p, p->seeds.ensure(packed.size()));
+    CU(p, cudaMemcpyAsync(p->seeds.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
+  }
+  sat::GaParams gp{};
+  gp.seed = sp->seed;
+  gp.rank = (uint32_t)p->rank;
+  gp.gen = 0;
+  gp.P = P;
+  gp.E = E;
+  gp.GS = GS;
+  gp.px = sp->p_xover_q32;
+  gp.pc = sp->p_cfg_mut_q32;
+  gp.pm = sp->p_perm_mut_q32;
+  int n_cand = 0;
+  uint64_t evaluated = (uint64_t)P;
+  CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p, p->pms[0].p,
+                            p->cand.p, &n_cand, p->sms, st));
+  if ((size_t)n_cand > p->cand.n) return fail(p, SATURN_ELIMIT, "candidate buffer too small");
+  CU(p, sat::launch_select(p->cand.p, n_cand, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
+
+  auto exchange = [&]() -> saturn_status {
+    if (!p->comm || p->world < 2) return SATURN_OK;
+    NC(p, nccl().allGather(p->rec_ms.p, p->all_ms.p, (size_t)E, ncclInt32, p->comm, st));
+    NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
+    CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, p->world, E, GS, p->rec_ms.p, p->rec_gen.p, st));
+    return SATURN_OK;
+  };
+  p->hist_t.clear();
+  p->hist_ms.clear();
+  auto record = [&]() -> saturn_status {
+    int32_t best = 0;
+    CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
+    CU(p, cudaStreamSynchronize(st));
+    p->hist_t.push_back(now_s() - t0);
+    p->hist_ms.push_back(best);
+    return SATURN_OK;
+  };
+  saturn_status s;
+  if ((s = exchange()) != SATURN_OK) return s;
+  if ((s = record()) != SATURN_OK) return s;
+  int cur = 0;
+  int64_t gen = 1;
+  for (; gen <= sp->max_generations; ++gen) {
+    gp.gen = (uint32_t)gen;
+    const int nxt = cur ^ 1;
+    CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
+                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, &n_cand, p->sms, st));
+    CU(p, sat::launch_select(p->cand.p, n_cand, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st));
+    evaluated += (uint64_t)(P - E);
+    cur = nxt;
+    if (gen % sp->generations_per_epoch == 0) {
+      if ((s = exchange()) != SATURN_OK) return s;
+      if ((s = record()) != SATURN_OK) return s;
+      if (sp->time_budget_s > 0 && now_s() - t0 >= sp->time_budget_s) {
+        ++gen;
+        break;
+      }
+    }
+  }
+  const int64_t gens_run = gen - 1;
+  if ((s = exchange()) != SATURN_OK) return s;
+  if ((s = record()) != SATURN_OK) return s;
+  std::vector<uint8_t> g0(GS);
+  int32_t best = 0;
+  CU(p, cudaMemcpyAsync(g0.data(), p->rec_gen.p, GS, cudaMemcpyDeviceToHost, st));
+  CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
+  CU(p, cudaStreamSynchronize(st));
+  p->best_cfg.assign(g0.begin(), g0.begin() + T);
+  p->best_perm.assign(g0.begin() + T, g0.begin() + 2 * T);
+  p->best_ms = best;
+  p->have_best = true;
+  p->have_pop = true;
+  p->last_pop = cur;
+  p->pop_P = P;
+  p->pop_GS = GS;
+  if (out) {
+    memset(out, 0, sizeof *out);
+    out->makespan = best;
+    out->evaluated = evaluated * (uint64_t)p->world;
+    out->seconds = now_s() - t0;
+    out->flags = SATURN_INCUMBENT;
+    out->generations = (int32_t)gens_run;
+  }
+  return SATURN_OK;
+}
+
+saturn_status saturn_search_history(const saturn_plan* p, int64_t n_max, double* t_s, int64_t* makespan,
+                                    int64_t* n_out) {
+  if (!p || !n_out) return SATURN_EINVAL;
+  const int64_t n = std::min<int64_t>(n_max, (int64_t)p->hist_t.size());
+  for (int64_t i = 0; i < n; ++i) {
+    if (t_s) t_s[i] = p->hist_t[i];
+    if (makespan) makespan[i] = p->hist_ms[i];
+  }
+  *n_out = n;
+  return SATURN_OK;
+}
+
+saturn_status saturn_search_population(const saturn_plan* p, uint8_t* h_cfg, uint8_t* h_perm, int32_t* h_makespan) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->have_pop) return SATURN_ESTATE;
+  DeviceGuard dg(p->device);
+  const int64_t P = p->pop_P;
+  const int GS = p->pop_GS, T = p->T;
+  std::vector<uint8_t> buf((size_t)P * GS);
+  if (cudaMemcpy(buf.data(), p->pop[p->last_pop].p, buf.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return SATURN_ECUDA;
+  if (h_makespan && cudaMemcpy(h_makespan, p->pms[p->last_pop].p, P * sizeof(int32_t), cudaMemcpyDeviceToHost) !=
+                        cudaSuccess)
+    return SATURN_ECUDA;
+  for (int64_t i = 0; i < P; ++i) {
+    if (h_cfg) memcpy(h_cfg + i * T, &buf[i * GS], T);
+    if (h_perm) memcpy(h_perm + i * T, &buf[i * GS + T], T);
+  }
+  return SATURN_OK;
+}
+
+saturn_status saturn_best_plan(saturn_plan* p, saturn_placement* out, uint8_t* genome_out, int64_t* makespan) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->have_best) return fail(p, SATURN_ESTATE, "best_plan before enumerate/search");
+  DeviceGuard dg(p->device);
+  const int T = p->T;
+  if (out) {
+    CU(p, p->ws_cfg.ensure(T));
+    CU(p, p->ws_perm.ensure(T));
+    CU(p, p->ws_ms.ensure(1));
+    CU(p, p->ws_place.ensure(T));
+    CU(p, cudaMemcpy(p->ws_cfg.p, p->best_cfg.data(), T, cudaMemcpyHostToDevice));
+    CU(p, cudaMemcpy(p->ws_perm.p, p->best_perm.data(), T, cudaMemcpyHostToDevice));
+    CU(p, sat::launch_trace(p->pb, p->ws_cfg.p, p->ws_perm.p, 1, p->ws_place.p, p->ws_ms.p, p->sms, 0));
+    CU(p, cudaMemcpy(out, p->ws_place.p, T * sizeof(saturn_placement), cudaMemcpyDeviceToHost));
+    int32_t ms = 0;
+    CU(p, cudaMemcpy(&ms, p->ws_ms.p, sizeof ms, cudaMemcpyDeviceToHost));
+    if (ms != p->best_ms)
+      return fail(p, SATURN_ECUDA, "trace makespan %d != recorded best %lld", ms, (long long)p->best_ms);
+  }
+  if (genome_out) {
+    memcpy(genome_out, p->best_cfg.data(), T);
+    memcpy(genome_out + T, p->best_perm.data(), T);
+  }
+  if (makespan) *makespan = p->best_ms;
+  return SATURN_OK;
+}
+
+saturn_status saturn_get_unique_id(uint8_t* id128) {
+  if (!id128) return SATURN_EINVAL;
+  if (!nccl().ok) return SATURN_ENCCL;
+  ncclUniqueId id;
+  if (nccl().getUniqueId(&id) != ncclSuccess) return SATURN_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id128, &id, 128);
+  return SATURN_OK;
+}
+
+saturn_status saturn_plan_attach_comm(saturn_plan* p, const uint8_t* id128, int32_t rank, int32_t world) {
+  if (!p) return SATURN_EINVAL;
+  if (!id128 || world < 1 || rank < 0 || rank >= world) return fail(p, SATURN_EINVAL, "bad rank/world");
+  if (!nccl().ok) return fail(p, SATURN_ENCCL, "%s", nccl().why.c_str());
+  DeviceGuard dg(p->device);
+  if (p->comm) {
+    nccl().commDestroy(p->comm);
+    p->comm = nullptr;
+  }
+  ncclUniqueId id;
+  memcpy(&id, id128, 128);
+  NC(p, nccl().commInitRank(&p->comm, world, id, rank));
+  p->rank = rank;
+  p->world = world;
+  return SATURN_OK;
+}
+
+saturn_status saturn_partition(uint64_t total, int32_t rank, int32_t world, uint64_t* begin, uint64_t* end) {
+  if (!begin || !end || world < 1 || rank < 0 || rank >= world) return SATURN_EINVAL;
+  const unsigned __int128 tt = total;
+  *begin = (uint64_t)(tt * (unsigned)rank / (unsigned)world);
+  *end = (uint64_t)(tt * (unsigned)(rank + 1) / (unsigned)world);
+  return SATURN_OK;
+}
+
+saturn_status saturn_probe_int_peak(saturn_plan* p, double* int_ops_per_s) {
+  if (!p || !int_ops_per_s) return SATURN_EINVAL;
+  DeviceGuard dg(p->device);
+  CU(p, p->sink.ensure(p->sms * 8));
+  cudaEvent_t a, b;
+  CU(p, cudaEventCreate(&a));
+  CU(p, cudaEventCreate(&b));
+  double ops = 0;
+  for (int w = 0; w < 3; ++w) sat::launch_int_probe(p->sms, p->sink.p, 0);
+  float best_ms = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    CU(p, cudaEventRecord(a, 0));
+    ops = sat::launch_int_probe(p->sms, p->sink.p, 0);
+    CU(p, cudaEventRecord(b, 0));
+    CU(p, cudaEventSynchronize(b));
+    float ms = 0;
+    CU(p, cudaEventElapsedTime(&ms, a, b));
+    best_ms = std::min(best_ms, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  CU(p, cudaGetLastError());
+  *int_ops_per_s = ops / (best_ms * 1e-3);
+  return SATURN_OK;
+}
+
+const char* saturn_last_error(const saturn_plan* p) { return p ? p->err.c_str() : "NULL handle"; }
+
+void saturn_plan_destroy(saturn_plan* p) {
+  if (!p) return;
+  {
+    DeviceGuard dg(p->device);
+    if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
+    p->blob.release();
+    p->ws_cfg.release();
+    p->ws_perm.release();
+    p->ws_ms.release();
+    p->ws_key.release();
+    p->ws_place.release();
+    for (int b = 0; b < 2; ++b) {
+      p->pop[b].release();
+      p->pms[b].release();
+    }
+    p->cand.release();
+    p->rec_ms.release();
+    p->all_ms.release();
+    p->rec_gen.release();
+    p->all_gen.release();
+    p->seeds.release();
+    p->sink.release();
+  }
+  delete p;
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// Device-side building blocks shared by the saturn kernels (sm_100a only).
+//
+// Nothing here is shared with oracle/ (the CPU reference); see DESIGN.md "Boundary".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "saturn kernels are written for sm_100a (B200) only"
+#endif
+
+namespace sat {
+
+constexpr int INF = 0x7fffffff;          // "never free" / padded GPU slot
+constexpr int MAX_JOBS = 255;            // u8 genes
+constexpr int MAX_GPUS = 32;             // sum_n GPU_n (one warp of lanes in the W decoder)
+constexpr int MAX_NODES = 32;
+constexpr uint32_t R_MASK = 0x00ffffffu; // config word = (g << 24) | R, R < 2^24 s
+
+// Problem description passed by value to every kernel.  The packed config table
+// (u32 words, job-major, `stride` words per job) is followed in the same allocation by
+// S[t] (u8, configs per job); `blob_bytes` (multiple of 16) covers both so one bulk copy
+// stages everything into shared memory.
+struct Problem {
+  const uint8_t* blob;     // device: tab[T*stride] u32, then S[T] u8, zero padded
+  int blob_bytes;
+  int T;                   // jobs
+  int stride;              // words per job row = max_t S_t
+  int N;                   // nodes
+  int sumG;                // sum_n GPU_n
+  int8_t gpu_n[MAX_NODES]; // GPU_n
+};
+
+__device__ __forceinline__ const uint32_t* tab_of(const uint8_t* blob) {
+  return reinterpret_cast<const uint32_t*>(blob);
+}
+__device__ __forceinline__ const uint8_t* S_of(const uint8_t* blob, const Problem& pb) {
+  return blob + 4 * pb.T * pb.stride;
+}
+
+// ------------------------------------------------------------------ TMA bulk staging
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D TMA: cp.async.bulk global -> shared, completion counted on an mbarrier (SASS UBLKCP).
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Stage the problem blob into shared memory (one elected thread issues, all wait).
+// Must be called by every thread of the block; `bar` is a fresh shared mbarrier.
+__device__ __forceinline__ void stage_problem(uint8_t* s_blob, const Problem& pb, uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(bar, pb.blob_bytes);
+    bulk_g2s(s_blob, pb.blob, pb.blob_bytes, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+}
+
+// ------------------------------------------------------------------ Philox4x32-10
+// Salmon et al. SC'11; counters (c0, c1, c2, block) and key (k0, k1).
+struct Philox {
+  uint32_t k0, k1, c0, c1, c2, block;
+  uint32_t b0, b1, b2, b3;  // unread words of the current block, consumed front first
+  int left;
+  __device__ __forceinline__ Philox(uint64_t seed, uint32_t a, uint32_t b, uint32_t c)
+      : k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), c0(a), c1(b), c2(c), block(0), left(0) {}
+  __device__ __forceinline__ void refill() {
+    uint32_t x0 = c0, x1 = c1, x2 = c2, x3 = block, a = k0, b = k1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      if (r) { a += 0x9E3779B9u; b += 0xBB67AE85u; }
+      uint32_t hi0 = __umulhi(0xD2511F53u, x0), lo0 = 0xD2511F53u * x0;
+      uint32_t hi1 = __umulhi(0xCD9E8D57u, x2), lo1 = 0xCD9E8D57u * x2;
+      uint32_t y0 = hi1 ^ x1 ^ a, y2 = hi0 ^ x3 ^ b;
+      x0 = y0; x1 = lo1; x2 = y2; x3 = lo0;
+    }
+    b0 = x0; b1 = x1; b2 = x2; b3 = x3;
+    ++block;
+    left = 4;
+  }
+  __device__ __forceinline__ uint32_t u32() {
+    if (left == 0) refill();
+    uint32_t v = b0;
+    b0 = b1; b1 = b2; b2 = b3;
+    --left;
+    return v;
+  }
+  // U(n) = (u32 * n) >> 32
+  __device__ __forceinline__ uint32_t below(uint32_t n) {
+    return (uint32_t)(((uint64_t)u32() * n) >> 32);
+  }
+};
+
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  lo = __shfl_xor_sync(0xffffffffu, lo, m);
+  hi = __shfl_xor_sync(0xffffffffu, hi, m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    uint64_t o = shfl_xor_u64(v, m);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+}  // namespace sat

@@ -1,0 +1,263 @@
+// The SPASE plan decoders (row a5 of SURVEY.md §8): genome -> integer makespan.
+//
+// Semantics (reading A6): jobs are placed in priority order
+// perm[0..T); job t with config (g, R) = table[t][cfg[t]] starts at the g-th smallest free
+// time of the node where that start is earliest (ties -> lowest node id); it takes the g
+// GPUs of that node that are free by then with the LATEST free times (ties -> lower GPU
+// id) and holds them for [s, s + R).  makespan = max_t (s_t + R_t)   (Eq. 2).
+// One config per job and one node per job (Eq. 3), exactly g GPUs (Eqs. 4-5),
+// one start for all of them (gang, Eqs. 8-9), no overlap on a GPU (Eqs. 10-11).
+//
+// Two device designs:
+//   T  decode_sorted<NN, GP>  one thread per genome; each node's free times are kept as a
+//      SORTED multiset in registers (GP slots, +inf padded).  Starts and makespans depend
+//      only on those multisets, and the latest-free-first pick becomes a closed-form update
+//        b = a shifted left by g-1 (so b[0] = a[g-1] = s),  v = s + R,
+//        a'[i] = (b[i+1] <= s) ? a[i] : min(b[i+1], max(a[i], v))
+//      (b[i+1] = a[i+g] <= s  <=>  i < m-g with m = #{a <= s}: the kept prefix; the rest is
+//      the merge of a[m..] with g copies of v).  No GPU ids: used for throughput.
+//   W  decode_warp            lanes = GPUs (node-major inside a pow2 segment, 32/seg genomes
+//      per warp).  Each lane ranks its free time inside its node with warp shuffles, the
+//      start of every node comes from a ballot, the earliest node from a shuffle-xor min,
+//      and the chosen GPUs from a ballot count -- the north-star design.  It yields the GPU
+//      ids, so it also produces the trace (row a8).
+#pragma once
+#include "common.cuh"
+
+namespace sat {
+
+// a[k] for a runtime k in [0, GP): binary mux tree on the bits of k (GP-1 selects).
+template <int GP>
+__device__ __forceinline__ int mux(const int (&a)[GP], int k) {
+  if constexpr (GP == 1) {
+    return a[0];
+  } else {
+    int v[GP / 2];
+#pragma unroll
+    for (int i = 0; i < GP / 2; ++i) v[i] = (k & 1) ? a[2 * i + 1] : a[2 * i];
+    return mux<GP / 2>(v, k >> 1);
+  }
+}
+
+// In-place update of one node's sorted free-time vector after placing (g, R) at its
+// g-th smallest free time.  Returns s + R.
+template <int GP>
+__device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R) {
+  const int k = g - 1;
+  int b[GP];
+#pragma unroll
+  for (int i = 0; i < GP; ++i) b[i] = x[i];
+#pragma unroll
+  for (int sh = 1; sh < GP; sh <<= 1) {
+    const bool on = (k & sh) != 0;
+#pragma unroll
+    for (int i = 0; i < GP; ++i) b[i] = on ? (i + sh < GP ? b[i + sh] : INF) : b[i];
+  }
+  const int s = b[0];
+  const int v = s + R;
+#pragma unroll
+  for (int i = 0; i < GP; ++i) {
+    const int bn = (i + 1 < GP) ? b[i + 1] : INF;
+    const int merged = min(bn, max(x[i], v));
+    x[i] = (bn <= s) ? x[i] : merged;
+  }
+  return v;
+}
+
+// Genome accessors: RowGenome reads a genome stored as two contiguous T-byte rows (the
+// caller's [n][T] layout, staged tile by tile); IlvGenome reads a thread-private genome kept
+// word-interleaved in shared memory (word w of thread i at base[w * 4 * B + 4 * i]), which is
+// bank-conflict free for any per-lane byte index.  Bytes [0, T) = cfg, [T, 2T) = perm.
+struct RowGenome {
+  const uint8_t* c;
+  const uint8_t* p;
+  __device__ __forceinline__ int cfg(int t) const { return c[t]; }
+  __device__ __forceinline__ int perm(int i) const { return p[i]; }
+};
+struct IlvGenome {
+  uint8_t* base;   // &smem[4 * tid]
+  int row;         // 4 * blockDim.x
+  int T;
+  __device__ __forceinline__ uint8_t& at(int k) const { return base[(k >> 2) * row + (k & 3)]; }
+  __device__ __forceinline__ int cfg(int t) const { return at(t); }
+  __device__ __forceinline__ int perm(int i) const { return at(T + i); }
+};
+
+// T design.  `tab` = packed (g << 24 | R) words [T][stride] in shared memory, `S` the
+// configs per job; `gen` is a genome accessor.
+// With CHECK, invalid genomes (perm not a permutation of 0..T-1, cfg[t] >= S_t) return -1;
+// `mask` is this thread's scratch bit set (ceil(T/32) words, `mstride` words apart).
+template <int NN, int GP, bool CHECK, class G>
+__device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
+                                             int stride, const G& gen, int T, const Problem& pb,
+                                             uint32_t* mask = nullptr, int mstride = 0) {
+  int a[NN][GP];
+#pragma unroll
+  for (int n = 0; n < NN; ++n)
+#pragma unroll
+    for (int i = 0; i < GP; ++i) a[n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
+
+  bool bad = false;
+  if constexpr (CHECK) {
+    for (int w = 0; w < (T + 31) / 32; ++w) mask[w * mstride] = 0u;
+  }
+  int ms = 0;
+  for (int p = 0; p < T; ++p) {
+    int t = gen.perm(p);
+    int c;
+    if constexpr (CHECK) {
+      bad |= t >= T;
+      t = min(t, T - 1);
+      uint32_t* mw = mask + (t >> 5) * mstride;
+      const uint32_t bit = 1u << (t & 31);
+      const uint32_t m = *mw;
+      bad |= (m & bit) != 0;
+      *mw = m | bit;
+      c = gen.cfg(t);
+      const int st = S[t];
+      bad |= c >= st;
+      c = min(c, st - 1);
+    } else {
+      c = gen.cfg(t);
+    }
+    const uint32_t w = tab[t * stride + c];
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    int v;
+    if constexpr (NN == 1) {
+      v = place_sorted<GP>(a[0], g, R);
+    } else {
+      // start of every node: its g-th smallest free time (+inf if it has fewer GPUs)
+      int best = mux<GP>(a[0], g - 1);
+      int bn = 0;
+#pragma unroll
+      for (int n = 1; n < NN; ++n) {
+        const int st = mux<GP>(a[n], g - 1);
+        const bool lt = st < best;   // strict: ties keep the lowest node id
+        best = lt ? st : best;
+        bn = lt ? n : bn;
+      }
+      int x[GP];
+#pragma unroll
+      for (int i = 0; i < GP; ++i) {
+        int y = a[0][i];
+#pragma unroll
+        for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
+        x[i] = y;
+      }
+      v = place_sorted<GP>(x, g, R);
+#pragma unroll
+      for (int n = 0; n < NN; ++n)
+#pragma unroll
+        for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
+    }
+    ms = max(ms, v);
+  }
+  if constexpr (CHECK) return bad ? -1 : ms;
+  return ms;
+}
+
+// Per-lane constants of the W design for a cluster with sumG <= 32 GPUs.
+struct WarpLane {
+  int seg;        // segment width (pow2 >= sumG)
+  int q;          // GPU slot within the segment (node-major)
+  int base;       // first lane of the segment
+  int node;       // node of this GPU (-1: padding lane)
+  int first;      // lane (within segment) of GPU 0 of this node
+  int local;      // GPU id within the node
+  int size;       // GPU_n of this node
+  uint32_t nmask; // lanes (absolute) of this node
+  uint32_t smask; // lanes (absolute) of this segment
+  int maxg;       // max_n GPU_n
+};
+
+__device__ __forceinline__ WarpLane warp_lane(const Problem& pb) {
+  WarpLane L;
+  int seg = 1;
+  while (seg < pb.sumG) seg <<= 1;
+  const int lane = threadIdx.x & 31;
+  L.seg = seg;
+  L.q = lane & (seg - 1);
+  L.base = lane & ~(seg - 1);
+  L.node = -1;
+  L.first = 0;
+  L.local = 0;
+  L.size = 0;
+  L.maxg = 0;
+  int acc = 0;
+  for (int n = 0; n < pb.N; ++n) {
+    const int gn = pb.gpu_n[n];
+    if (L.q >= acc && L.q < acc + gn) { L.node = n; L.first = acc; L.local = L.q - acc; L.size = gn; }
+    acc += gn;
+    L.maxg = max(L.maxg, (int)gn);
+  }
+  L.smask = (seg == 32) ? 0xffffffffu : (((1u << seg) - 1u) << L.base);
+  L.nmask = (L.node < 0) ? 0u : ((L.size == 32 ? 0xffffffffu : ((1u << L.size) - 1u)) << (L.base + L.first));
+  return L;
+}
+
+// Per-job record written by the trace decoder; layout == saturn_placement (32 bytes).
+struct Placement {
+  int32_t node, upp, gpus, cfg, start_s, end_s;
+  uint64_t gpu_mask;
+};
+
+// W design.  All 32 lanes must call it (shuffles use the full mask); `live` lanes belong to
+// a real genome.  cfg/perm point at this segment's genome.  If `rec` is non-null, lane q==0
+// of each live segment writes the T placement records (job-id order).  Lanes return the
+// genome's makespan.
+__device__ __forceinline__ int decode_warp(const uint32_t* __restrict__ tab, int stride, const uint8_t* cfg,
+                                           const uint8_t* perm, int T, const WarpLane& L, bool live,
+                                           const int* node_first, const uint8_t* upp, Placement* rec) {
+  const int lane = threadIdx.x & 31;
+  int f = (L.node >= 0) ? 0 : INF;
+  int ms = 0;
+  for (int p = 0; p < T; ++p) {
+    const int t = live ? perm[p] : 0;
+    const int c = live ? cfg[t] : 0;
+    const uint32_t w = tab[t * stride + c];
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    // rank of (f, local id) among the GPUs of my node
+    int less = 0, eq = 0, eqpos = 0;
+    for (int j = 0; j < L.maxg; ++j) {
+      const int src = L.base + L.first + min(j, max(L.size - 1, 0));
+      const int fj = __shfl_sync(0xffffffffu, f, src);
+      const bool ok = j < L.size;
+      less += (ok && fj < f);
+      eq += (ok && fj == f);
+      eqpos += (ok && fj == f && j < L.local);
+    }
+    const int rank = less + eqpos;
+    // start of my node = free time of the lane whose rank is g-1
+    const uint32_t hit = __ballot_sync(0xffffffffu, L.node >= 0 && rank == g - 1) & L.nmask;
+    const int src = hit ? (__ffs(hit) - 1) : lane;
+    const int fs = __shfl_sync(0xffffffffu, f, src);
+    uint32_t key = hit ? (((uint32_t)fs << 5) | (uint32_t)L.node) : 0xffffffffu;
+    for (int m = L.seg >> 1; m >= 1; m >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, m));
+    const int nstar = (int)(key & 31u);
+    const int s = (int)(key >> 5);
+    const int v = s + R;
+    const bool le = (L.node == nstar) && f <= s;
+    const int m = __popc(__ballot_sync(0xffffffffu, le) & L.smask);
+    const int rank2 = m - less - eq + eqpos;   // order: free time descending, then id ascending
+    const bool chosen = le && rank2 < g;
+    const uint32_t cb = __ballot_sync(0xffffffffu, chosen) & L.smask;
+    f = chosen ? v : f;
+    ms = max(ms, v);
+    if (rec && live && L.q == 0) {
+      Placement r;
+      r.node = nstar;
+      r.upp = upp[t * stride + c];
+      r.gpus = g;
+      r.cfg = c;
+      r.start_s = s;
+      r.end_s = v;
+      r.gpu_mask = (uint64_t)(cb >> (L.base + node_first[nstar]));
+      rec[t] = r;
+    }
+  }
+  return ms;
+}
+
+}  // namespace sat

@@ -1,0 +1,618 @@
+// saturn device kernels for sm_100a: evaluate (K1), trace (K6), enumerate (K2),
+// GA init/generation (K3 fused with K1), top-E select and elite merge (K4), and the
+// integer-ALU probe used as the roofline denominator check.
+//
+// Every kernel stages the problem blob (packed config table + S_t + UPP ids, <= 48 KB)
+// into shared memory once per persistent CTA with a 1-D TMA bulk copy (row a3).
+#include <climits>
+#include <cstdio>
+
+#include "decode.cuh"
+#include "kernels.h"
+
+namespace sat {
+
+constexpr int EVAL_B = 128;  // threads (= genomes per tile) of the evaluate kernel
+constexpr int ENUM_B = 128;
+constexpr int GA_B = 128;
+constexpr int WARP_B = 128;
+
+// ------------------------------------------------------------------ shapes
+#define SAT_SHAPES(X) \
+  X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(1, 32) X(2, 2) X(2, 4) X(2, 8) X(2, 16) X(2, 32) X(4, 2) X(4, 4) X(4, 8) \
+  X(4, 16) X(8, 2) X(8, 4) X(8, 8) X(16, 2) X(16, 4)
+
+bool have_sorted_shape(int NN, int GP) {
+#define SAT_HAVE(a, b) if (NN == a && GP == b) return true;
+  SAT_SHAPES(SAT_HAVE)
+#undef SAT_HAVE
+  return false;
+}
+
+
+// ------------------------------------------------------------------ warp-level top-E list
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
+  uint32_t lo = __shfl_up_sync(0xffffffffu, (uint32_t)v, d);
+  uint32_t hi = __shfl_up_sync(0xffffffffu, (uint32_t)(v >> 32), d);
+  return ((uint64_t)hi << 32) | lo;
+}
+// `lst` is a warp-distributed ascending list (lane k = k-th smallest key seen); insert
+// each lane's `key` if it beats the E-th entry.  Keys are unique.
+__device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E) {
+  const int lane = threadIdx.x & 31;
+  uint64_t thr = shfl_u64(lst, E - 1);
+  uint32_t cm = __ballot_sync(0xffffffffu, key < thr);
+  while (cm) {
+    const int src = __ffs(cm) - 1;
+    cm &= cm - 1;
+    const uint64_t k = shfl_u64(key, src);
+    thr = shfl_u64(lst, E - 1);
+    if (k < thr) {
+      const int pos = __popc(__ballot_sync(0xffffffffu, lst < k));
+      const uint64_t up = shfl_up_u64(lst, 1);
+      if (lane > pos) lst = up;
+      else if (lane == pos) lst = k;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K1: evaluate (T design)
+size_t eval_smem_bytes(const Problem& pb) {
+  return (size_t)pb.blob_bytes + 4u * EVAL_B * pb.T + 4u * EVAL_B * ((pb.T + 31) / 32) + 3 * 8;
+}
+
+template <int NN, int GP>
+__global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* __restrict__ gcfg,
+                                                     const uint8_t* __restrict__ gperm, int64_t n,
+                                                     int32_t* __restrict__ out, int use_bulk) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int T = pb.T;
+  const int tileB = EVAL_B * T;  // bytes per array per tile (multiple of 16)
+  uint8_t* s_blob = sm;
+  uint8_t* s_g = sm + pb.blob_bytes;                          // [2 buffers][cfg | perm]
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 4 * tileB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_mask + EVAL_B * ((T + 31) / 32));
+  const int64_t ntiles = (n + EVAL_B - 1) / EVAL_B;
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bars[2], pb.blob_bytes);
+    bulk_g2s(s_blob, pb.blob, pb.blob_bytes, &bars[2]);
+    const int64_t tile = blockIdx.x;
+    if (use_bulk && tile < ntiles && (tile + 1) * EVAL_B <= n) {
+      mbar_expect_tx(&bars[0], 2 * tileB);
+      bulk_g2s(s_g, gcfg + tile * tileB, tileB, &bars[0]);
+      bulk_g2s(s_g + tileB, gperm + tile * tileB, tileB, &bars[0]);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bars[2], 0);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    uint8_t* bc = s_g + buf * 2 * tileB;
+    uint8_t* bp = bc + tileB;
+    const int64_t first = tile * EVAL_B;
+    const bool full = use_bulk && first + EVAL_B <= n;
+    if (full) {
+      mbar_wait(&bars[buf], (it >> 1) & 1);
+    } else {  // ragged last tile (or unaligned caller buffers): plain cooperative loads
+      const int cnt = (int)min((int64_t)EVAL_B, n - first) * T;
+      for (int k = tid; k < cnt; k += EVAL_B) {
+        bc[k] = gcfg[first * T + k];
+        bp[k] = gperm[first * T + k];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {  // prefetch the next tile into the other buffer
+      const int64_t nt = tile + gridDim.x;
+      if (use_bulk && nt < ntiles && (nt + 1) * EVAL_B <= n) {
+        uint8_t* nc = s_g + (buf ^ 1) * 2 * tileB;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[buf ^ 1], 2 * tileB);
+        bulk_g2s(nc, gcfg + nt * tileB, tileB, &bars[buf ^ 1]);
+        bulk_g2s(nc + tileB, gperm + nt * tileB, tileB, &bars[buf ^ 1]);
+      }
+    }
+    if (first + tid < n) {
+      RowGenome gen{bc + tid * T, bp + tid * T};
+      out[first + tid] = decode_sorted<NN, GP, true>(tab, S, pb.stride, gen, T, pb, s_mask + tid, EVAL_B);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ K1-W / K6: warp decoder
+static size_t warp_smem_bytes(const Problem& pb) {
+  return (size_t)pb.blob_bytes + 4 * MAX_NODES + 4 * (WARP_B / 32) * 32 * 8 + 8;
+}
+
+template <bool TRACE>
+__global__ void __launch_bounds__(WARP_B) k_eval_warp(Problem pb, const uint8_t* __restrict__ gcfg,
+                                                      const uint8_t* __restrict__ gperm, int64_t n,
+                                                      int32_t* __restrict__ out, Placement* __restrict__ rec) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint8_t* s_blob = sm;
+  int* s_first = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_first + MAX_NODES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_bits + (WARP_B / 32) * 32 * 8);
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < pb.N; ++k) { s_first[k] = acc; acc += pb.gpu_n[k]; }
+  }
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  const uint8_t* upp = S + pb.T;
+  const int T = pb.T;
+  const WarpLane L = warp_lane(pb);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gpw = 32 / L.seg;
+  const int64_t wg = (int64_t)blockIdx.x * (WARP_B / 32) + warp;
+  const int64_t wtot = (int64_t)gridDim.x * (WARP_B / 32);
+  uint32_t* bits = s_bits + warp * 32 * 8 + (L.base / L.seg) * 8;
+
+  for (int64_t base = wg * gpw; base < n; base += wtot * gpw) {
+    const int64_t gi = base + lane / L.seg;
+    const bool live = gi < n;
+    const uint8_t* c = gcfg + (live ? gi : 0) * T;
+    const uint8_t* p = gperm + (live ? gi : 0) * T;
+    // genome validity, lanes of the segment cooperate
+    for (int w = L.q; w < 8; w += L.seg) bits[w] = 0u;
+    __syncwarp();
+    bool bad = false;
+    if (live) {
+      for (int i = L.q; i < T; i += L.seg) {
+        const int t = p[i];
+        if (t >= T) { bad = true; continue; }
+        const uint32_t bit = 1u << (t & 31);
+        if (atomicOr(&bits[t >> 5], bit) & bit) bad = true;
+        if (c[t] >= S[t]) bad = true;
+      }
+    }
+    const bool segbad = (__ballot_sync(0xffffffffu, bad) & L.smask) != 0u;
+    __syncwarp();
+    const int ms = decode_warp(tab, pb.stride, c, p, T, L, live && !segbad, s_first, upp,
+                               TRACE ? rec + (live ? gi : 0) * T : nullptr);
+    if (live && L.q == 0) out[gi] = segbad ? -1 : ms;
+  }
+}
+
+// ------------------------------------------------------------------ launch helpers
+template <class K>
+static int grid_for(K kernel, int threads, size_t smem, int sms, int64_t work_blocks) {
+  static_assert(sizeof(K) > 0, "");
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+  if (occ < 1) occ = 1;
+  int64_t g = (int64_t)sms * occ;
+  if (work_blocks < g) g = work_blocks;
+  return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const uint8_t* cfg, const uint8_t* perm,
+                            int64_t n, int32_t* out, int sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (kind == 1) {
+    const size_t smem = eval_smem_bytes(pb);
+    const int use_bulk = ((((uintptr_t)cfg) | ((uintptr_t)perm)) & 15u) == 0;
+    const int64_t ntiles = (n + EVAL_B - 1) / EVAL_B;
+#define SAT_EVAL(a, b)                                                                   \
+  if (NN == a && GP == b) {                                                              \
+    const int g = grid_for(k_evaluate<a, b>, EVAL_B, smem, sms, ntiles);                 \
+    k_evaluate<a, b><<<g, EVAL_B, smem, st>>>(pb, cfg, perm, n, out, use_bulk);          \
+    return cudaGetLastError();                                                           \
+  }
+    SAT_SHAPES(SAT_EVAL)
+#undef SAT_EVAL
+    return cudaErrorInvalidConfiguration;
+  }
+  const size_t smem = warp_smem_bytes(pb);
+  int seg = 1;
+  while (seg < pb.sumG) seg <<= 1;
+  const int64_t per_block = (int64_t)(WARP_B / 32) * (32 / seg);
+  const int g = grid_for(k_eval_warp<false>, WARP_B, smem, sms, (n + per_block - 1) / per_block);
+  k_eval_warp<false><<<g, WARP_B, smem, st>>>(pb, cfg, perm, n, out, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* perm, int64_t n, void* placements,
+                         int32_t* out, int sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = warp_smem_bytes(pb);
+  int seg = 1;
+  while (seg < pb.sumG) seg <<= 1;
+  const int64_t per_block = (int64_t)(WARP_B / 32) * (32 / seg);
+  const int g = grid_for(k_eval_warp<true>, WARP_B, smem, sms, (n + per_block - 1) / per_block);
+  k_eval_warp<true><<<g, WARP_B, smem, st>>>(pb, cfg, perm, n, out, static_cast<Placement*>(placements));
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K2: enumerate
+// Genome index G -> (cfg, perm): r_cfg = G mod prod S, r_perm = G div prod S,
+// cfg[t] = (r_cfg div radix[t]) mod S_t, perm = lexicographic unrank of r_perm.
+// Consecutive indices advance cfg like an odometer (job 0 fastest), then perm by
+// next_permutation, so only the first index of a chunk is unranked.
+static size_t enum_smem_bytes(const Problem& pb) {
+  return (size_t)pb.blob_bytes + (size_t)4 * ENUM_B * ((2 * pb.T + 3) / 4) + 32 * 8 + 8;
+}
+
+template <int NN, int GP>
+__global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, uint64_t begin, uint64_t end,
+                                                      uint64_t chunk, unsigned long long* best_key) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint8_t* s_blob = sm;
+  uint8_t* s_gen = sm + pb.blob_bytes;
+  const int T = pb.T;
+  const int words = (2 * T + 3) / 4;
+  uint64_t* s_red = reinterpret_cast<uint64_t*>(s_gen + 4 * ENUM_B * words);
+  uint64_t* bar = s_red + 32;
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  IlvGenome gen{s_gen + 4 * threadIdx.x, 4 * ENUM_B, T};
+
+  uint64_t best = ~0ull;
+  const uint64_t total = end - begin;
+  const uint64_t nchunks = (total + chunk - 1) / chunk;
+  const uint64_t gt = (uint64_t)blockIdx.x * ENUM_B + threadIdx.x;
+  const uint64_t nthr = (uint64_t)gridDim.x * ENUM_B;
+  for (uint64_t ch = gt; ch < nchunks; ch += nthr) {
+    const uint64_t i0 = begin + ch * chunk;
+    const uint64_t i1 = min(i0 + chunk, end);
+    // unrank i0
+    uint64_t r_cfg = i0 % es.cfg_space;
+    uint64_t r_perm = i0 / es.cfg_space;
+    for (int t = 0; t < T; ++t) gen.at(t) = (uint8_t)((r_cfg / es.radix[t]) % (uint64_t)S[t]);
+    uint32_t avail = (T == 32) ? 0xffffffffu : ((1u << T) - 1u);
+    for (int p = 0; p < T; ++p) {
+      const uint64_t f = es.fact[T - 1 - p];
+      int d = (int)(r_perm / f);
+      r_perm %= f;
+      uint32_t m = avail;
+      for (int k = 0; k < d; ++k) m &= m - 1;
+      const int x = __ffs(m) - 1;
+      avail &= ~(1u << x);
+      gen.at(T + p) = (uint8_t)x;
+    }
+    for (uint64_t idx = i0; idx < i1; ++idx) {
+      const int ms = decode_sorted<NN, GP, false>(tab, S, pb.stride, gen, T, pb);
+      const uint64_t key = ((uint64_t)ms << 38) | idx;
+      best = key < best ? key : best;
+      // odometer over cfg (job 0 least significant), carry into perm
+      int t = 0;
+      for (; t < T; ++t) {
+        const int c = gen.at(t) + 1;
+        if (c < S[t]) { gen.at(t) = (uint8_t)c; break; }
+        gen.at(t) = 0;
+      }
+      if (t == T) {  // next lexicographic permutation of perm
+        int k = T - 2;
+        while (k >= 0 && gen.at(T + k) >= gen.at(T + k + 1)) --k;
+        if (k >= 0) {
+          int l = T - 1;
+          while (gen.at(T + l) <= gen.at(T + k)) --l;
+          uint8_t tmp = gen.at(T + k); gen.at(T + k) = gen.at(T + l); gen.at(T + l) = tmp;
+          for (int a = k + 1, b = T - 1; a < b; ++a, --b) {
+            tmp = gen.at(T + a); gen.at(T + a) = gen.at(T + b); gen.at(T + b) = tmp;
+          }
+        }
+      }
+    }
+  }
+  best = warp_min_u64(best);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_red[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t b = s_red[0];
+    for (int w = 1; w < ENUM_B / 32; ++w) b = s_red[w] < b ? s_red[w] : b;
+    if (b != ~0ull) atomicMin(best_key, (unsigned long long)b);
+  }
+}
+
+cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace& es, uint64_t begin, uint64_t end,
+                             unsigned long long* best_key, int sms, cudaStream_t st) {
+  if (end <= begin) return cudaSuccess;
+  const size_t smem = enum_smem_bytes(pb);
+  const uint64_t total = end - begin;
+#define SAT_ENUM(a, b)                                                                           \
+  if (NN == a && GP == b) {                                                                      \
+    const int g0 = grid_for(k_enumerate<a, b>, ENUM_B, smem, sms, 1 << 30);                      \
+    const uint64_t thr = (uint64_t)g0 * ENUM_B;                                                  \
+    uint64_t chunk = (total + thr - 1) / thr;                                                    \
+    if (chunk > 4096) chunk = 4096;                                                              \
+    if (chunk < 1) chunk = 1;                                                                    \
+    const uint64_t nch = (total + chunk - 1) / chunk;                                            \
+    int64_t blocks = (int64_t)((nch + ENUM_B - 1) / ENUM_B);                                     \
+    const int g = (int)(blocks < g0 ? blocks : g0);                                              \
+    k_enumerate<a, b><<<g, ENUM_B, smem, st>>>(pb, es, begin, end, chunk, best_key);             \
+    return cudaGetLastError();                                                                   \
+  }
+  SAT_SHAPES(SAT_ENUM)
+#undef SAT_ENUM
+  return cudaErrorInvalidConfiguration;
+}
+
+// ------------------------------------------------------------------ K3 (+K1): GA
+// Thread-private genomes live word-interleaved in shared memory: child (GS/4 words) then
+// parent B (GS/4 words), then the OX1 slice bit set (8 words), each row GA_B words wide.
+static size_t ga_smem_bytes(const Problem& pb, int GS) {
+  return (size_t)pb.blob_bytes + (size_t)4 * GA_B * (2 * (GS / 4) + 8) + 8;
+}
+
+// Copy a GS-byte global record into an interleaved smem genome (and back).
+__device__ __forceinline__ void load_ilv(uint8_t* base, int row, const uint8_t* __restrict__ g, int GS) {
+  const uint4* src = reinterpret_cast<const uint4*>(g);
+  for (int k = 0; k < GS / 16; ++k) {
+    const uint4 v = src[k];
+    uint32_t* d = reinterpret_cast<uint32_t*>(base + (4 * k) * row);
+    d[0] = v.x;
+    d[row / 4] = v.y;
+    d[2 * (row / 4)] = v.z;
+    d[3 * (row / 4)] = v.w;
+  }
+}
+__device__ __forceinline__ void store_ilv(uint8_t* __restrict__ g, const uint8_t* base, int row, int GS) {
+  uint4* dst = reinterpret_cast<uint4*>(g);
+  for (int k = 0; k < GS / 16; ++k) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(base + (4 * k) * row);
+    dst[k] = make_uint4(s[0], s[row / 4], s[2 * (row / 4)], s[3 * (row / 4)]);
+  }
+}
+
+template <int NN, int GP>
+__global__ void __launch_bounds__(GA_B) k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds,
+                                             int64_t n_seed, const uint8_t* __restrict__ prev_pop,
+                                             const int32_t* __restrict__ prev_ms, const int32_t* __restrict__ rec_ms,
+                                             const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
+                                             int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int T = pb.T;
+  const int GS = gp.GS;
+  const int row = 4 * GA_B;
+  uint8_t* s_blob = sm;
+  uint8_t* s_child = sm + pb.blob_bytes;
+  uint8_t* s_B = s_child + (GS / 4) * row;
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + (GS / 4) * row);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_bits + 8 * GA_B);
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  const int tid = threadIdx.x, lane = tid & 31;
+  IlvGenome ch{s_child + 4 * tid, row, T};
+  IlvGenome gb{s_B + 4 * tid, row, T};
+  uint32_t* inA = s_bits + tid;  // word w at inA[w * GA_B]
+  const uint32_t P = (uint32_t)gp.P;
+
+  uint64_t lst = ~0ull;
+  const int64_t nthr = (int64_t)gridDim.x * GA_B;
+  for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P; base += nthr) {
+    const int64_t slot = base + lane;
+    const bool live = slot < gp.P;
+    int msv = INT_MAX;
+    if (live) {
+      bool decode = true;
+      if (gp.gen == 0) {
+        if (slot < n_seed) {
+          load_ilv(ch.base, row, seeds + slot * GS, GS);
+        } else {  // Philox-initialised genome: cfg[t] = U(S_t), then Fisher-Yates on identity
+          Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
+          for (int t = 0; t < T; ++t) ch.at(t) = (uint8_t)rng.below(S[t]);
+          for (int t = 0; t < T; ++t) ch.at(T + t) = (uint8_t)t;
+          for (int i = T - 1; i > 0; --i) {
+            const int j = (int)rng.below(i + 1);
+            const uint8_t a = ch.at(T + i);
+            ch.at(T + i) = ch.at(T + j);
+            ch.at(T + j) = a;
+          }
+        }
+      } else if (slot < gp.E) {  // elite: copied with its makespan
+        load_ilv(ch.base, row, rec_gen + slot * GS, GS);
+        msv = rec_ms[slot];
+        decode = false;
+      } else {
+        Philox rng(gp.seed, (uint32_t)slot, gp.gen, (gp.rank << 16) | 0u);
+        uint32_t A, B;
+        {
+          const uint32_t i = rng.below(P), j = rng.below(P);
+          const uint64_t ki = ((uint64_t)(uint32_t)prev_ms[i] << 32) | i;
+          const uint64_t kj = ((uint64_t)(uint32_t)prev_ms[j] << 32) | j;
+          A = ki < kj ? i : j;
+        }
+        {
+          const uint32_t i = rng.below(P), j = rng.below(P);
+          const uint64_t ki = ((uint64_t)(uint32_t)prev_ms[i] << 32) | i;
+          const uint64_t kj = ((uint64_t)(uint32_t)prev_ms[j] << 32) | j;
+          B = ki < kj ? i : j;
+        }
+        load_ilv(ch.base, row, prev_pop + (uint64_t)A * GS, GS);
+        if (rng.u32() < gp.px) {
+          load_ilv(gb.base, row, prev_pop + (uint64_t)B * GS, GS);
+          uint32_t word = 0;
+          for (int t = 0; t < T; ++t) {  // uniform crossover of the config genes
+            if ((t & 31) == 0) word = rng.u32();
+            if (!((word >> (t & 31)) & 1u)) ch.at(t) = gb.at(t);
+          }
+          uint32_t a = rng.below(T), b = rng.below(T);  // OX1 on the permutation
+          if (a > b) { const uint32_t x = a; a = b; b = x; }
+          for (int w = 0; w < (T + 31) / 32; ++w) inA[w * GA_B] = 0u;
+          for (uint32_t q = a; q <= b; ++q) {
+            const int x = ch.at(T + q);
+            inA[(x >> 5) * GA_B] |= 1u << (x & 31);
+          }
+          int pos = (b + 1 == (uint32_t)T) ? 0 : (int)b + 1;
+          int rd = pos;
+          const int fill = T - (int)(b - a + 1);
+          for (int k = 0; k < fill; ++k) {
+            int x;
+            while (true) {
+              x = gb.at(T + rd);
+              rd = (rd + 1 == T) ? 0 : rd + 1;
+              if (!((inA[(x >> 5) * GA_B] >> (x & 31)) & 1u)) break;
+            }
+            ch.at(T + pos) = (uint8_t)x;
+            pos = (pos + 1 == T) ? 0 : pos + 1;
+          }
+        }
+        for (int t = 0; t < T; ++t)  // config mutation
+          if (rng.u32() < gp.pc) ch.at(t) = (uint8_t)rng.below(S[t]);
+        if (rng.u32() < gp.pm) {  // permutation mutation: swap or insertion
+          const uint32_t kind = rng.u32() & 1u;
+          const int i = (int)rng.below(T), j = (int)rng.below(T);
+          if (kind == 0) {
+            const uint8_t x = ch.at(T + i);
+            ch.at(T + i) = ch.at(T + j);
+            ch.at(T + j) = x;
+          } else {
+            const uint8_t x = ch.at(T + i);
+            if (i < j) {
+              for (int k = i; k < j; ++k) ch.at(T + k) = ch.at(T + k + 1);
+            } else {
+              for (int k = i; k > j; --k) ch.at(T + k) = ch.at(T + k - 1);
+            }
+            ch.at(T + j) = x;
+          }
+        }
+      }
+      if (decode) msv = decode_sorted<NN, GP, false>(tab, S, pb.stride, ch, T, pb);
+      store_ilv(pop + slot * GS, ch.base, row, GS);
+      ms_out[slot] = msv;
+    }
+    const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
+    topE_insert(lst, key, gp.E);
+  }
+  const int64_t wglob = (int64_t)blockIdx.x * (GA_B / 32) + (tid >> 5);
+  if (lane < gp.E) cand[wglob * gp.E + lane] = lst;
+}
+
+static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
+                             int64_t n_seed, const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
+                             const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand,
+                             int* n_cand, int sms, cudaStream_t st) {
+  const size_t smem = ga_smem_bytes(pb, gp.GS);
+  const int64_t blocks = (gp.P + GA_B - 1) / GA_B;
+#define SAT_GA(a, b)                                                                                        \
+  if (NN == a && GP == b) {                                                                                 \
+    const int g = grid_for(k_ga<a, b>, GA_B, smem, sms, blocks);                                            \
+    *n_cand = g * (GA_B / 32) * gp.E;                                                                       \
+    k_ga<a, b><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,   \
+                                      cand);                                                                \
+    return cudaGetLastError();                                                                              \
+  }
+  SAT_SHAPES(SAT_GA)
+#undef SAT_GA
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
+                           int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* n_cand, int sms,
+                           cudaStream_t st) {
+  return launch_ga(pb, NN, GP, gp, seeds, n_seed, nullptr, nullptr, nullptr, nullptr, pop, ms, cand, n_cand, sms, st);
+}
+cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
+                                 const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen, uint8_t* pop,
+                                 int32_t* ms, unsigned long long* cand, int* n_cand, int sms, cudaStream_t st) {
+  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, n_cand, sms, st);
+}
+
+// ------------------------------------------------------------------ K4: select / merge
+__global__ void __launch_bounds__(1024) k_select(const unsigned long long* __restrict__ cand, int n, int E, int GS,
+                                                 const uint8_t* __restrict__ pop, int32_t* __restrict__ rec_ms,
+                                                 uint8_t* __restrict__ rec_gen) {
+  __shared__ uint64_t s_l[32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t lst = ~0ull;
+  for (int base = warp * 32; base < n; base += 1024) {
+    const uint64_t key = (base + lane < n) ? cand[base + lane] : ~0ull;
+    topE_insert(lst, key, E);
+  }
+  s_l[warp][lane] = lst;
+  __syncthreads();
+  if (warp == 0) {
+    lst = ~0ull;
+    for (int w = 0; w < 32; ++w) topE_insert(lst, s_l[w][lane], E);
+    if (lane < E) {
+      const uint32_t slot = (uint32_t)(lst & 0xffffffffu);
+      rec_ms[lane] = (int32_t)(lst >> 32);
+      const uint4* src = reinterpret_cast<const uint4*>(pop + (uint64_t)slot * GS);
+      uint4* dst = reinterpret_cast<uint4*>(rec_gen + (uint64_t)lane * GS);
+      for (int k = 0; k < GS / 16; ++k) dst[k] = src[k];
+    }
+  }
+}
+
+cudaError_t launch_select(const unsigned long long* cand, int n_cand, int E, int GS, const uint8_t* pop,
+                          int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st) {
+  k_select<<<1, 1024, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);
+  return cudaGetLastError();
+}
+
+__global__ void k_merge(const int32_t* __restrict__ all_ms, const uint8_t* __restrict__ all_gen, int W, int E, int GS,
+                        int32_t* __restrict__ rec_ms, uint8_t* __restrict__ rec_gen) {
+  const int lane = threadIdx.x & 31;
+  uint64_t lst = ~0ull;
+  const int n = W * E;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const uint64_t key = (i < n) ? (((uint64_t)(uint32_t)all_ms[i] << 32) | (uint32_t)i) : ~0ull;
+    topE_insert(lst, key, E);
+  }
+  if (lane < E) {
+    const uint32_t i = (uint32_t)(lst & 0xffffffffu);
+    rec_ms[lane] = (int32_t)(lst >> 32);
+    const uint4* src = reinterpret_cast<const uint4*>(all_gen + (uint64_t)i * GS);
+    uint4* dst = reinterpret_cast<uint4*>(rec_gen + (uint64_t)lane * GS);
+    for (int k = 0; k < GS / 16; ++k) dst[k] = src[k];
+  }
+}
+
+cudaError_t launch_merge_elites(const int32_t* all_ms, const uint8_t* all_gen, int W, int E, int GS, int32_t* rec_ms,
+                                uint8_t* rec_gen, cudaStream_t st) {
+  k_merge<<<1, 32, 0, st>>>(all_ms, all_gen, W, E, GS, rec_ms, rec_gen);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ integer-ALU probe
+// 8 independent chains of IMNMX / IADD3 / ISETP+SEL per thread; 6 int ops per chain step.
+constexpr int PROBE_ITERS = 4096;
+__global__ void __launch_bounds__(256) k_int_probe(int* sink, int seed) {
+  int x[8], y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { x[k] = seed + threadIdx.x + k; y[k] = seed ^ (k * 7919); }
+  for (int i = 0; i < PROBE_ITERS; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int a = max(x[k], y[k]);       // IMNMX
+      const int b = min(a + i, x[k] + 3);  // IADD3, IADD3, IMNMX
+      y[k] = (b < y[k]) ? b : a;           // ISETP + SEL
+      x[k] = b;
+    }
+  }
+  int acc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc ^= x[k] ^ y[k];
+  if (acc == 0x12345678) sink[blockIdx.x] = acc;
+}
+
+double launch_int_probe(int sms, int* sink, cudaStream_t st) {
+  const int blocks = sms * 8;
+  k_int_probe<<<blocks, 256, 0, st>>>(sink, 1);
+  return (double)blocks * 256 * PROBE_ITERS * 8 * 6;
+}
+
+}  // namespace sat

@@ -1,0 +1,66 @@
+// Host-side launchers for the saturn device kernels (internal to libsaturn; not the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace sat {
+
+// Thread-decoder shapes (NN padded nodes x GP padded GPUs per node) compiled into the
+// library.  Anything else runs on the warp decoder.
+bool have_sorted_shape(int NN, int GP);
+
+// Shared-memory bytes of each kernel for a given problem.
+size_t eval_smem_bytes(const Problem& pb);
+
+// saturn_evaluate: one makespan per genome (rows of T bytes).  kind: 1 = thread, 2 = warp.
+cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const uint8_t* cfg,
+                            const uint8_t* perm, int64_t n, int32_t* out, int sms, cudaStream_t st);
+
+// Trace decode (W design): placements[n][T] (32 B records, job-id order) and makespans.
+cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* perm, int64_t n,
+                         void* placements, int32_t* out, int sms, cudaStream_t st);
+
+// Mixed-radix / factoradic constants of the genome index space.
+constexpr int ENUM_MAX_T = 20;
+struct EnumSpace {
+  uint64_t cfg_space;              // prod_t S_t
+  uint64_t radix[ENUM_MAX_T];      // prod_{t' < t} S_t'
+  uint64_t fact[ENUM_MAX_T + 1];   // k!
+};
+// Exhaustive enumeration of genome indices [begin, end): atomicMin of (ms << 38 | index).
+cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace& es, uint64_t begin,
+                             uint64_t end, unsigned long long* best_key, int sms, cudaStream_t st);
+
+struct GaParams {
+  uint64_t seed;
+  uint32_t rank;
+  uint32_t gen;       // generation being produced (0 = initial population)
+  int64_t P;          // population per rank
+  int E;              // elites
+  int GS;             // genome record stride in bytes (multiple of 16)
+  uint32_t px, pc, pm;
+};
+
+// Generation 0: seed genomes then Philox-initialised genomes, all decoded.
+cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
+                           int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* n_cand,
+                           int sms, cudaStream_t st);
+// Generation gen >= 1 from the previous population and the elite records.
+cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
+                                 const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen,
+                                 uint8_t* pop, int32_t* ms, unsigned long long* cand, int* n_cand, int sms,
+                                 cudaStream_t st);
+// Top-E of the candidate keys -> elite records (ms, genome) copied from `pop`.
+cudaError_t launch_select(const unsigned long long* cand, int n_cand, int E, int GS, const uint8_t* pop,
+                          int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st);
+// Island migration: the E best of W ranks' gathered records by (ms, rank, position).
+cudaError_t launch_merge_elites(const int32_t* all_ms, const uint8_t* all_gen, int W, int E, int GS,
+                                int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st);
+
+// Integer-ALU throughput probe (independent IMNMX/ISETP/IADD3/SEL chains).  Returns the
+// number of integer operations one launch performs.
+double launch_int_probe(int sms, int* sink, cudaStream_t st);
+
+}  // namespace sat

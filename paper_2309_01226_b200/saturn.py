@@ -1,0 +1,394 @@
+"""Thin Python binding of include/saturn.h (argument marshalling only).
+
+Every computation runs in libsaturn.so (hand-written sm_100a kernels).  PyTorch is used for
+device memory (tensors), streams and torch.distributed bootstrap only.  There is no CPU
+fallback: importing this module fails loudly if the library is missing.
+
+Function names follow the C ABI without the ``saturn_`` prefix; ``Plan`` wraps a handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsaturn.so")
+
+OK, EINVAL, EUNSCHEDULABLE, ELIMIT, ECUDA, ENCCL, ESTATE = range(7)
+STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EUNSCHEDULABLE", 3: "ELIMIT", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
+PROVEN_OPTIMAL, INCUMBENT = 1, 2
+DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
+
+# Every symbol declared in include/saturn.h.
+EXPORTS = (
+    "saturn_plan_create", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
+    "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
+    "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
+    "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
+    "saturn_partition", "saturn_probe_int_peak", "saturn_last_error", "saturn_plan_destroy",
+)
+
+
+class SaturnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Placement(ctypes.Structure):
+    _fields_ = [("node", ctypes.c_int32), ("upp", ctypes.c_int32), ("gpus", ctypes.c_int32),
+                ("cfg", ctypes.c_int32), ("start_s", ctypes.c_int32), ("end_s", ctypes.c_int32),
+                ("gpu_mask", ctypes.c_uint64)]
+
+
+PLACEMENT_DTYPE = np.dtype([("node", "<i4"), ("upp", "<i4"), ("gpus", "<i4"), ("cfg", "<i4"),
+                            ("start_s", "<i4"), ("end_s", "<i4"), ("gpu_mask", "<u8")])
+
+
+class Result(ctypes.Structure):
+    _fields_ = [("makespan", ctypes.c_int64), ("genome_index", ctypes.c_uint64), ("evaluated", ctypes.c_uint64),
+                ("seconds", ctypes.c_double), ("flags", ctypes.c_int32), ("generations", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class SearchParams(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("population", ctypes.c_int64), ("max_generations", ctypes.c_int64),
+                ("time_budget_s", ctypes.c_double), ("elites", ctypes.c_int32),
+                ("generations_per_epoch", ctypes.c_int32), ("p_xover_q32", ctypes.c_uint32),
+                ("p_cfg_mut_q32", ctypes.c_uint32), ("p_perm_mut_q32", ctypes.c_uint32),
+                ("seed_cfg", ctypes.POINTER(ctypes.c_uint8)), ("seed_perm", ctypes.POINTER(ctypes.c_uint8)),
+                ("n_seed", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsaturn.so; raises (never falls back) if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libsaturn.so not built at {path}: run __graft_entry__.build() "
+                          "(python -m paper_2309_01226_b200.build)")
+    lib = ctypes.CDLL(path)
+    P, i32, i64, u64, u8, vp = ctypes.POINTER, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint8, \
+        ctypes.c_void_p
+    h = vp
+    sigs = {
+        "saturn_plan_create": [P(i32), i32, i32, P(vp)],
+        "saturn_load_runtime_table": [h, P(i32), i32, i32, i32],
+        "saturn_num_configs": [h, P(i32), P(i32)],
+        "saturn_config": [h, i32, i32, P(i32), P(i32), P(i32)],
+        "saturn_set_decoder": [h, i32],
+        "saturn_evaluate": [h, vp, vp, i64, vp, vp],
+        "saturn_evaluate_host": [h, P(u8), P(u8), i64, P(i32), vp],
+        "saturn_trace": [h, vp, vp, i64, vp, vp, vp],
+        "saturn_space_size": [h, P(u64)],
+        "saturn_enumerate": [h, u64, vp, P(Result)],
+        "saturn_enumerate_range": [h, u64, u64, vp, P(Result)],
+        "saturn_search": [h, P(SearchParams), vp, P(Result)],
+        "saturn_search_history": [h, i64, P(ctypes.c_double), P(i64), P(i64)],
+        "saturn_search_population": [h, P(u8), P(u8), P(i32)],
+        "saturn_best_plan": [h, P(Placement), P(u8), P(i64)],
+        "saturn_get_unique_id": [P(u8)],
+        "saturn_plan_attach_comm": [h, P(u8), i32, i32],
+        "saturn_partition": [u64, i32, i32, P(u64), P(u64)],
+        "saturn_probe_int_peak": [h, P(ctypes.c_double)],
+    }
+    for name, args in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.saturn_last_error.argtypes = [h]
+    lib.saturn_last_error.restype = ctypes.c_char_p
+    lib.saturn_plan_destroy.argtypes = [h]
+    lib.saturn_plan_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+def _np_ptr(a, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_ptr(t, dtype_name, shape=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA torch.Tensor")
+    if str(t.dtype) != "torch." + dtype_name:
+        raise TypeError(f"expected dtype {dtype_name}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def partition(total: int, rank: int, world: int):
+    lib = load_library()
+    b, e = ctypes.c_uint64(), ctypes.c_uint64()
+    st = lib.saturn_partition(total, rank, world, ctypes.byref(b), ctypes.byref(e))
+    if st != OK:
+        raise SaturnError(st, "saturn_partition")
+    return int(b.value), int(e.value)
+
+
+def get_unique_id() -> bytes:
+    lib = load_library()
+    buf = (ctypes.c_uint8 * 128)()
+    st = lib.saturn_get_unique_id(buf)
+    if st != OK:
+        raise SaturnError(st, "saturn_get_unique_id (NCCL not loadable)")
+    return bytes(buf)
+
+
+@dataclass
+class SearchConfig:
+    seed: int = 0
+    population: int = 1 << 20
+    max_generations: int = 64
+    time_budget_s: float = 0.0
+    elites: int = 16
+    generations_per_epoch: int = 8
+    p_xover: float = 0.9
+    p_cfg_mut: float | None = None   # default 1/T
+    p_perm_mut: float = 0.5
+
+
+def q32(p: float) -> int:
+    return min(int(p * 4294967296.0), 0xFFFFFFFF)
+
+
+class Plan:
+    """Handle over one cluster on one CUDA device (saturn_plan_create)."""
+
+    def __init__(self, node_gpus, device: int = 0):
+        self._lib = load_library()
+        arr = np.ascontiguousarray(node_gpus, dtype=np.int32)
+        h = ctypes.c_void_p()
+        st = self._lib.saturn_plan_create(_np_ptr(arr, ctypes.c_int32), int(arr.size), int(device), ctypes.byref(h))
+        if st != OK:
+            raise SaturnError(st, f"saturn_plan_create(node_gpus={list(arr)}, device={device})")
+        self._h = h
+        self.node_gpus = list(int(x) for x in arr)
+        self.device = device
+        self.n_jobs = 0
+
+    # -- plumbing
+    def _check(self, st, what):
+        if st != OK:
+            raise SaturnError(st, f"{what}: {self._lib.saturn_last_error(self._h).decode()}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.saturn_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- table
+    def load_runtime_table(self, runtime):
+        r = np.ascontiguousarray(runtime, dtype=np.int32)
+        if r.ndim != 3:
+            raise ValueError("runtime must be [T][U][Gmax]")
+        T, U, G = r.shape
+        self._check(self._lib.saturn_load_runtime_table(self._h, _np_ptr(r, ctypes.c_int32), T, U, G),
+                    "saturn_load_runtime_table")
+        self.n_jobs = T
+        return self
+
+    def num_configs(self) -> np.ndarray:
+        n = ctypes.c_int32()
+        self._check(self._lib.saturn_num_configs(self._h, ctypes.byref(n), None), "saturn_num_configs")
+        out = np.zeros(n.value, np.int32)
+        self._check(self._lib.saturn_num_configs(self._h, ctypes.byref(n), _np_ptr(out, ctypes.c_int32)),
+                    "saturn_num_configs")
+        return out
+
+    def config(self, job: int, cfg: int):
+        u, g, r = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(self._lib.saturn_config(self._h, job, cfg, ctypes.byref(u), ctypes.byref(g), ctypes.byref(r)),
+                    "saturn_config")
+        return u.value, g.value, r.value
+
+    def set_decoder(self, kind: int):
+        self._check(self._lib.saturn_set_decoder(self._h, int(kind)), "saturn_set_decoder")
+
+    def space_size(self) -> int:
+        v = ctypes.c_uint64()
+        self._check(self._lib.saturn_space_size(self._h, ctypes.byref(v)), "saturn_space_size")
+        return int(v.value)
+
+    # -- hot path
+    def evaluate(self, cfg, perm, out=None, stream=None):
+        """cfg, perm: CUDA uint8 tensors [n][T]; returns CUDA int32 makespans [n] (async)."""
+        import torch
+        n = int(cfg.shape[0])
+        if out is None:
+            out = torch.empty(n, dtype=torch.int32, device=cfg.device)
+        self._check(self._lib.saturn_evaluate(self._h, _dev_ptr(cfg, "uint8", (n, self.n_jobs)),
+                                              _dev_ptr(perm, "uint8", (n, self.n_jobs)), n,
+                                              _dev_ptr(out, "int32", (n,)), _stream_ptr(stream)),
+                    "saturn_evaluate")
+        return out
+
+    def evaluate_host(self, cfg: np.ndarray, perm: np.ndarray, stream=None) -> np.ndarray:
+        cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
+        perm = np.ascontiguousarray(perm, dtype=np.uint8)
+        n = cfg.shape[0]
+        out = np.empty(n, np.int32)
+        self._check(self._lib.saturn_evaluate_host(self._h, _np_ptr(cfg, ctypes.c_uint8), _np_ptr(perm, ctypes.c_uint8),
+                                                   n, _np_ptr(out, ctypes.c_int32), _stream_ptr(stream)),
+                    "saturn_evaluate_host")
+        return out
+
+    def trace(self, cfg, perm, stream=None):
+        """-> (placements uint8 tensor [n][T][32] viewable with PLACEMENT_DTYPE, makespans [n])."""
+        import torch
+        n = int(cfg.shape[0])
+        T = self.n_jobs
+        pl = torch.zeros((n, T, 32), dtype=torch.uint8, device=cfg.device)
+        ms = torch.empty(n, dtype=torch.int32, device=cfg.device)
+        self._check(self._lib.saturn_trace(self._h, _dev_ptr(cfg, "uint8", (n, T)), _dev_ptr(perm, "uint8", (n, T)), n,
+                                           _dev_ptr(pl, "uint8"), _dev_ptr(ms, "int32"), _stream_ptr(stream)),
+                    "saturn_trace")
+        return pl, ms
+
+    def enumerate(self, max_genomes: int = 1 << 34, stream=None) -> dict:
+        r = Result()
+        self._check(self._lib.saturn_enumerate(self._h, int(max_genomes), _stream_ptr(stream), ctypes.byref(r)),
+                    "saturn_enumerate")
+        return r.as_dict()
+
+    def enumerate_range(self, begin: int, end: int, stream=None) -> dict:
+        r = Result()
+        self._check(self._lib.saturn_enumerate_range(self._h, int(begin), int(end), _stream_ptr(stream),
+                                                     ctypes.byref(r)), "saturn_enumerate_range")
+        return r.as_dict()
+
+    def search(self, cfg: SearchConfig | None = None, seed_genomes=None, stream=None) -> dict:
+        cfg = cfg or SearchConfig()
+        T = self.n_jobs
+        p_c = cfg.p_cfg_mut if cfg.p_cfg_mut is not None else 1.0 / max(T, 1)
+        sp = SearchParams(seed=cfg.seed, population=cfg.population, max_generations=cfg.max_generations,
+                          time_budget_s=cfg.time_budget_s, elites=cfg.elites,
+                          generations_per_epoch=cfg.generations_per_epoch, p_xover_q32=q32(cfg.p_xover),
+                          p_cfg_mut_q32=q32(p_c), p_perm_mut_q32=q32(cfg.p_perm_mut))
+        keep = None
+        if seed_genomes is not None:
+            sc = np.ascontiguousarray(seed_genomes[0], dtype=np.uint8)
+            sq = np.ascontiguousarray(seed_genomes[1], dtype=np.uint8)
+            keep = (sc, sq)
+            sp.seed_cfg = _np_ptr(sc, ctypes.c_uint8)
+            sp.seed_perm = _np_ptr(sq, ctypes.c_uint8)
+            sp.n_seed = sc.shape[0]
+        r = Result()
+        self._check(self._lib.saturn_search(self._h, ctypes.byref(sp), _stream_ptr(stream), ctypes.byref(r)),
+                    "saturn_search")
+        del keep
+        return r.as_dict()
+
+    def search_history(self, n_max: int = 1 << 16):
+        t = np.zeros(n_max, np.float64)
+        m = np.zeros(n_max, np.int64)
+        n = ctypes.c_int64()
+        self._check(self._lib.saturn_search_history(self._h, n_max, _np_ptr(t, ctypes.c_double),
+                                                    _np_ptr(m, ctypes.c_int64), ctypes.byref(n)),
+                    "saturn_search_history")
+        return t[:n.value], m[:n.value]
+
+    def search_population(self, P: int):
+        T = self.n_jobs
+        c = np.zeros((P, T), np.uint8)
+        q = np.zeros((P, T), np.uint8)
+        m = np.zeros(P, np.int32)
+        self._check(self._lib.saturn_search_population(self._h, _np_ptr(c, ctypes.c_uint8), _np_ptr(q, ctypes.c_uint8),
+                                                       _np_ptr(m, ctypes.c_int32)), "saturn_search_population")
+        return c, q, m
+
+    def best_plan(self):
+        """-> (makespan, placements list of dicts (job-id order), cfg, perm)."""
+        T = self.n_jobs
+        out = (Placement * T)()
+        g = np.zeros(2 * T, np.uint8)
+        ms = ctypes.c_int64()
+        self._check(self._lib.saturn_best_plan(self._h, out, _np_ptr(g, ctypes.c_uint8), ctypes.byref(ms)),
+                    "saturn_best_plan")
+        pl = [dict(node=o.node, upp=o.upp, gpus=o.gpus, cfg=o.cfg, start_s=o.start_s, end_s=o.end_s,
+                   gpu_mask=int(o.gpu_mask)) for o in out]
+        return int(ms.value), pl, g[:T].copy(), g[T:].copy()
+
+    def attach_comm(self, uid: bytes, rank: int, world: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self._lib.saturn_plan_attach_comm(self._h, buf, rank, world), "saturn_plan_attach_comm")
+
+    def probe_int_peak(self) -> float:
+        v = ctypes.c_double()
+        self._check(self._lib.saturn_probe_int_peak(self._h, ctypes.byref(v)), "saturn_probe_int_peak")
+        return float(v.value)
+
+
+# Names of the C ABI, for callers who prefer the flat form.
+def plan_create(node_gpus, device: int = 0) -> Plan:
+    return Plan(node_gpus, device)
+
+
+def load_runtime_table(plan: Plan, runtime):
+    return plan.load_runtime_table(runtime)
+
+
+def evaluate(plan: Plan, cfg, perm, out=None, stream=None):
+    return plan.evaluate(cfg, perm, out, stream)
+
+
+def enumerate(plan: Plan, max_genomes: int = 1 << 34, stream=None):  # noqa: A001
+    return plan.enumerate(max_genomes, stream)
+
+
+def search(plan: Plan, cfg: SearchConfig | None = None, seed_genomes=None, stream=None):
+    return plan.search(cfg, seed_genomes, stream)
+
+
+def best_plan(plan: Plan):
+    return plan.best_plan()
+
+
+def attach_distributed(plan: Plan, group=None):
+    """Create the library's NCCL communicator over a torch.distributed group: rank 0 makes
+    the unique id, torch.distributed broadcasts it, every rank attaches (row e)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = get_unique_id() if rank == 0 else bytes(128)
+    buf = torch.tensor(list(uid), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        buf = buf.cuda()
+    dist.broadcast(buf, src=0, group=group)
+    uid = bytes(buf.cpu().tolist())
+    plan.attach_comm(uid, rank, world)
+    return uid

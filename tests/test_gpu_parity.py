@@ -1,0 +1,286 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, bit for bit.
+
+Integer work (makespans, schedules, enumeration (makespan, index), GA children) must be
+identical; no tolerance anywhere.  Inputs are seeded (synth/); sizes span several tiles
+and a ragged tail.  Run under gpurun: python -m pytest tests -m gpu
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import ga as oga
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = ("TINY", "TXT", "IMG", "MIX", "SWEEP")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    if not t.cuda.is_available():
+        pytest.skip("no GPU")
+    return t
+
+
+@pytest.fixture(scope="module")
+def sat(torch):
+    import paper_2309_01226_b200 as s
+    s.load_library()
+    return s
+
+
+def _plan(sat, inst):
+    return sat.Plan(inst.node_gpus, 0).load_runtime_table(inst.runtime)
+
+
+def _ms(plan, torch, cfg, perm):
+    return plan.evaluate(torch.from_numpy(cfg).cuda(), torch.from_numpy(perm).cuda()).cpu().numpy()
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+@pytest.mark.parametrize("decoder", ["thread", "warp"])
+def test_evaluate_matches_oracle(sat, torch, name, decoder):
+    inst = synth.by_name(name, seed=1)
+    plan = _plan(sat, inst)
+    plan.set_decoder(sat.DECODER_THREAD if decoder == "thread" else sat.DECODER_WARP)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    assert list(plan.num_configs()) == list(c.S)
+    n = 20000 if name != "SWEEP" else 5003
+    cfg, perm = synth.random_genomes(c.S, n, seed=11)
+    got = _ms(plan, torch, cfg, perm)
+    ref = oracle.decode_batch(c, cfg, perm)
+    assert (ref > 0).all()
+    assert np.array_equal(got, ref), np.nonzero(got != ref)[0][:10]
+
+
+@pytest.mark.parametrize("n", [1, 2, 127, 128, 129, 1000, 4097])
+def test_evaluate_ragged_sizes(sat, torch, n):
+    inst = synth.txt(2)
+    plan = _plan(sat, inst)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    cfg, perm = synth.random_genomes(c.S, n, seed=n)
+    assert np.array_equal(_ms(plan, torch, cfg, perm), oracle.decode_batch(c, cfg, perm))
+
+
+def test_evaluate_unaligned_buffers_use_plain_loads(sat, torch):
+    inst = synth.mix(0)
+    plan = _plan(sat, inst)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    n = 3001
+    cfg, perm = synth.random_genomes(c.S, n, seed=5)
+    T = c.n_jobs
+    big_c = torch.zeros(n * T + 1, dtype=torch.uint8, device="cuda")
+    big_p = torch.zeros(n * T + 1, dtype=torch.uint8, device="cuda")
+    big_c[1:] = torch.from_numpy(cfg.reshape(-1)).cuda()
+    big_p[1:] = torch.from_numpy(perm.reshape(-1)).cuda()
+    got = plan.evaluate(big_c[1:].view(n, T), big_p[1:].view(n, T)).cpu().numpy()
+    assert np.array_equal(got, oracle.decode_batch(c, cfg, perm))
+
+
+def test_evaluate_invalid_genomes(sat, torch):
+    inst = synth.txt(0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    for decoder in (sat.DECODER_THREAD, sat.DECODER_WARP):
+        plan = _plan(sat, inst)
+        plan.set_decoder(decoder)
+        cfg, perm = synth.random_genomes(c.S, 300, seed=9)
+        perm[0, 3] = perm[0, 4]          # duplicate job
+        perm[1, 0] = 200                 # job id out of range
+        cfg[2, 5] = c.S[5]               # config out of range
+        got = _ms(plan, torch, cfg, perm)
+        ref = oracle.decode_batch(c, cfg, perm)
+        assert list(got[:3]) == [-1, -1, -1] and list(ref[:3]) == [-1, -1, -1]
+        assert np.array_equal(got, ref)
+
+
+def test_evaluate_host_path(sat, torch):
+    inst = synth.img(3)
+    plan = _plan(sat, inst)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    cfg, perm = synth.random_genomes(c.S, 10000, seed=4)
+    assert np.array_equal(plan.evaluate_host(cfg, perm), oracle.decode_batch(c, cfg, perm))
+
+
+def test_heterogeneous_clusters(sat, torch):
+    """{2,2,4,8} and 8+4 (PAPER.md:1118-style) on both decoders."""
+    for nodes in ([2, 2, 4, 8], [8, 4], [3, 5], [1, 1, 1]):
+        inst = synth.sweep(7, n_jobs=30, nodes=nodes)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        cfg, perm = synth.random_genomes(c.S, 3000, seed=len(nodes))
+        ref = oracle.decode_batch(c, cfg, perm)
+        for decoder in (sat.DECODER_AUTO, sat.DECODER_WARP):
+            plan = _plan(sat, inst)
+            plan.set_decoder(decoder)
+            assert np.array_equal(_ms(plan, torch, cfg, perm), ref), (nodes, decoder)
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_trace_matches_oracle_schedules(sat, torch, name):
+    inst = synth.by_name(name, seed=4)
+    plan = _plan(sat, inst)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    n = 300
+    cfg, perm = synth.random_genomes(c.S, n, seed=3)
+    pl, ms = plan.trace(torch.from_numpy(cfg).cuda(), torch.from_numpy(perm).cuda())
+    rec = pl.cpu().numpy().view(sat.PLACEMENT_DTYPE).reshape(n, c.n_jobs)
+    ms = ms.cpu().numpy()
+    for i in range(n):
+        ref_ms, ref_pl = oracle.decode(c, cfg[i], perm[i])
+        assert ms[i] == ref_ms
+        for t in range(c.n_jobs):
+            r, o = rec[i, t], ref_pl[t]
+            assert (r["node"], r["upp"], r["gpus"], r["cfg"], r["start_s"], r["end_s"], r["gpu_mask"]) == \
+                (o["node"], o["upp"], o["gpus"], o["cfg"], o["start_s"], o["end_s"], o["gpu_mask"]), (i, t)
+
+
+def test_hand_traces_on_device(sat, torch, golden_dir):
+    import json
+    import os
+    from conftest import dense_from_single
+    cases = json.load(open(os.path.join(golden_dir, "hand_traces.json")))["cases"]
+    for case in cases:
+        table = dense_from_single(case["jobs"])
+        plan = sat.Plan(case["nodes"], 0).load_runtime_table(table)
+        T = len(case["jobs"])
+        cfg = np.zeros((1, T), np.uint8)
+        perm = np.array([case["order"]], np.uint8)
+        for decoder in (sat.DECODER_THREAD, sat.DECODER_WARP):
+            plan.set_decoder(decoder)
+            assert _ms(plan, torch, cfg, perm)[0] == case["makespan"], case["id"]
+        if "starts" in case:
+            pl, _ = plan.trace(torch.from_numpy(cfg).cuda(), torch.from_numpy(perm).cuda())
+            rec = pl.cpu().numpy().view(sat.PLACEMENT_DTYPE).reshape(T)
+            assert list(rec["start_s"]) == case["starts"]
+            assert list(rec["gpu_mask"]) == case["masks"]
+
+
+# ------------------------------------------------------------------ enumerate
+def test_enumerate_tiny_matches_brute_force(sat, torch):
+    for seed in range(5):
+        inst = synth.tiny(seed)
+        plan = _plan(sat, inst)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        r = plan.enumerate()
+        assert (r["makespan"], r["genome_index"]) == oracle.brute_force(c)
+        assert r["evaluated"] == 1296 and r["flags"] == sat.PROVEN_OPTIMAL
+        best, pl, bc, bp = plan.best_plan()
+        ms, opl = oracle.decode(c, bc, bp)
+        assert ms == best == r["makespan"]
+        assert oracle.validate(c, pl, best) == []
+
+
+@pytest.mark.parametrize("jobs,nodes", [(4, (4,)), (5, (4,)), (4, (2, 2)), (5, (2, 2)), (6, (2, 2))])
+def test_enumerate_tiny_variants(sat, torch, jobs, nodes):
+    inst = synth.tiny_variant(jobs * 10 + len(nodes), jobs, nodes)
+    plan = _plan(sat, inst)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    N = oracle.space_size(c)
+    assert plan.space_size() == N
+    r = plan.enumerate()
+    if N <= 3_000_000:
+        assert (r["makespan"], r["genome_index"]) == oracle.brute_force(c)
+    else:  # oracle on the winning genome + a sampled slice
+        cfg, perm = oracle.unrank(c, r["genome_index"])
+        assert oracle.decode(c, cfg, perm)[0] == r["makespan"]
+        b = r["genome_index"] - r["genome_index"] % 100000
+        sub = plan.enumerate_range(b, min(b + 100000, N))
+        assert (sub["makespan"], sub["genome_index"]) == oracle.brute_force(c, b, min(b + 100000, N))
+
+
+def test_enumerate_ranges_compose_like_multi_gpu(sat, torch):
+    """The min over any partition of the index space = the whole-space result (the
+    W-invariance of the multi-GPU enumeration, reading A7)."""
+    inst = synth.tiny_variant(45, 5, (2, 2))
+    plan = _plan(sat, inst)
+    N = plan.space_size()
+    whole = plan.enumerate()
+    for W in (2, 3, 8):
+        parts = [plan.enumerate_range(*sat.partition(N, r, W)) for r in range(W)]
+        best = min((p["makespan"], p["genome_index"]) for p in parts)
+        assert best == (whole["makespan"], whole["genome_index"])
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    assert plan.enumerate_range(17, 12345)["makespan"] == oracle.brute_force(c, 17, 12345)[0]
+
+
+def test_enumerate_limits(sat, torch):
+    inst = synth.txt(0)
+    plan = _plan(sat, inst)
+    with pytest.raises(sat.SaturnError) as e:
+        plan.enumerate()
+    assert e.value.status == sat.ELIMIT
+
+
+# ------------------------------------------------------------------ GA search
+def test_ga_operator_replay_bit_exact(sat, torch):
+    """Initial population and several generations reproduced by the oracle's operator
+    definitions (oracle/ga.py) from the same seed: identical genomes and makespans."""
+    inst = synth.txt(0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    P, E, seed = 256, 4, 12345
+    px, pc, pm = oga.q32(0.9), oga.q32(0.25), oga.q32(0.5)
+    cfg, perm = oga.initial_population(c.S, P, seed)
+    ms = oracle.decode_batch(c, cfg, perm)
+    plan = _plan(sat, inst)
+    for G in (0, 1, 3):
+        plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=G, elites=E,
+                                     generations_per_epoch=1, p_xover=0.9, p_cfg_mut=0.25, p_perm_mut=0.5))
+        gc, gq, gm = plan.search_population(P)
+        rc, rq, rm = cfg, perm, ms
+        for gen in range(1, G + 1):
+            rc, rq, _ = oga.next_generation(c.S, rc, rq, rm, gen, seed, 0, E, px, pc, pm)
+            rm = oracle.decode_batch(c, rc, rq)
+        assert np.array_equal(gc, rc) and np.array_equal(gq, rq) and np.array_equal(gm, rm), G
+
+
+def test_ga_replay_with_seed_genomes_and_sweep(sat, torch):
+    inst = synth.sweep(1)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    P, E, seed = 128, 8, 99
+    sc, sq = synth.random_genomes(c.S, 5, seed=2)
+    cfg, perm = oga.initial_population(c.S, P, seed, seed_cfg=sc, seed_perm=sq)
+    ms = oracle.decode_batch(c, cfg, perm)
+    rc, rq, _ = oga.next_generation(c.S, cfg, perm, ms, 1, seed, 0, E, oga.q32(0.9), oga.q32(0.01), oga.q32(0.5))
+    rm = oracle.decode_batch(c, rc, rq)
+    plan = _plan(sat, inst)
+    plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=1, elites=E, generations_per_epoch=1,
+                                 p_xover=0.9, p_cfg_mut=0.01, p_perm_mut=0.5), seed_genomes=(sc, sq))
+    gc, gq, gm = plan.search_population(P)
+    assert np.array_equal(gc, rc) and np.array_equal(gq, rq) and np.array_equal(gm, rm)
+
+
+def test_search_best_is_valid_and_monotone(sat, torch):
+    inst = synth.txt(0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    plan = _plan(sat, inst)
+    r = plan.search(sat.SearchConfig(seed=1, population=1 << 14, max_generations=40, elites=16,
+                                     generations_per_epoch=4))
+    best, pl, bc, bp = plan.best_plan()
+    assert best == r["makespan"]
+    ms, opl = oracle.decode(c, bc, bp)
+    assert ms == best and oracle.validate(c, pl, best) == []
+    assert best >= oracle.lower_bound(c)
+    _, hist = plan.search_history()
+    assert all(a >= b for a, b in zip(hist, hist[1:]))
+    assert r["evaluated"] == (1 << 14) + 40 * ((1 << 14) - 16)
+    # determinism
+    r2 = plan.search(sat.SearchConfig(seed=1, population=1 << 14, max_generations=40, elites=16,
+                                      generations_per_epoch=4))
+    assert r2["makespan"] == r["makespan"] and (plan.best_plan()[2] == bc).all()
+
+
+def test_search_reaches_optimum_on_tiny(sat, torch):
+    for seed in range(3):
+        inst = synth.tiny(seed)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        opt = oracle.brute_force(c)[0]
+        plan = _plan(sat, inst)
+        r = plan.search(sat.SearchConfig(seed=seed, population=256, max_generations=20, elites=4))
+        assert r["makespan"] == opt
+
+
+def test_int_probe_runs(sat, torch):
+    plan = _plan(sat, synth.txt(0))
+    v = plan.probe_int_peak()
+    assert 1e12 < v < 1e14
