@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: SPASE plans evaluated per second (BASELINE.json metric) on 1..N B200s.
+
+One STEP = one pass of the whole hot path over one batch: a ``saturn_search`` call on the
+resident runtime table -- an initial population of P genomes (Philox init + decode), then
+G generations of Philox tournament / crossover / mutation fused with the decode of every
+child, per-generation top-E reduction, epoch exchange of elites (NCCL when N > 1), and the
+best genome returned to the host (rows a3-a7).  The e2e leg repeats the step through the
+host API including the table upload (a1/a2) and the trace-decoded best plan (a8).
+
+``value`` counts full decodes only (SURVEY.md §8d counting rule), summed over all ranks,
+divided by the max-over-ranks device time of K steps (CUDA events on the launching stream).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload TXT] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SPASE plans evaluated/sec at 1/2/4/8 B200; best makespan vs oracle"
+UNIT = "plans/s"
+# Integer-ALU roofline denominator: 148 SMs x 4 SMSPs x 16 INT32
+# lanes of the ALU pipe per clock x 1.965 GHz max SM clock (B200_PROFILING.md / MEASURED_PEAKS.json).
+ALU_PEAK_OPS = 148 * 4 * 16 * 1.965e9
+
+WORKLOADS = {
+    "TINY": "C1 TINY: 3 jobs x {DDP,FSDP} x g{1,2,4} on 1x4 GPUs",
+    "TXT": "C2 TXT: 12 GPT-2/GPT-J jobs x 4 UPPs x g1-8 on 1x8 GPUs",
+    "IMG": "C3 IMG: 12 ViT-G/ResNet jobs x 4 UPPs x g1-8 on 1x8 GPUs",
+    "MIX": "C4 MIX: 24 TXT+IMG jobs on 2x8 GPUs",
+    "SWEEP": "C5 SWEEP: 100 jobs x 4 UPPs on 4x8 GPUs",
+}
+
+
+def algorithmic_ops_per_plan(T: int, node_gpus) -> int:
+    """T * (2 + 2N + 4 * GPU_node) integer ops per decode."""
+    return T * (2 + 2 * len(node_gpus) + 4 * max(node_gpus))
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def _oracle_worker(args):
+    name, seed, n = args
+    import oracle
+    import synth
+    inst = synth.by_name(name, 0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    cfg, perm = synth.random_genomes(c.S, n, seed=seed)
+    t0 = time.perf_counter()
+    ms = oracle.decode_batch(c, cfg, perm)
+    dt = time.perf_counter() - t0
+    assert (ms > 0).all()
+    return n, dt
+
+
+def oracle_rate(name: str, n_per_core: int, cores: int, seed0: int = 0):
+    """Plain C oracle decoder (oracle/saturn_oracle.c, single-threaded per process) on
+    `cores` host processes; returns (decodes/s, wall seconds, total decodes)."""
+    import multiprocessing as mp
+    import oracle
+    oracle.build_library()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_worker, [(name, seed0 + 999, 1000)] * cores)  # warm (imports, lib load)
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_worker, [(name, seed0 + k, n_per_core) for k in range(cores)])
+        wall = time.perf_counter() - t0
+    total = sum(n for n, _ in res)
+    return total / wall, wall, total
+
+
+def cpu_baseline(name: str, target_s: float = 10.0):
+    cores = os.cpu_count() or 1
+    rate1, _, _ = oracle_rate(name, 20000, 1)
+    n = max(1000, int(rate1 * target_s))
+    rate, wall, total = oracle_rate(name, n, cores, seed0=100)
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"O1 decode (oracle/saturn_oracle.c) of {total} seeded random {name} genomes "
+                      f"({n} per process x {cores} processes, {wall:.1f} s wall)"}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    name = args.workload
+    per_core = args.ref_per_core
+    for _ in range(args.warmup):
+        oracle_rate(name, per_core // 4, cores, seed0=7)
+    t_total, n_total = 0.0, 0
+    for k in range(args.steps):
+        rate, wall, total = oracle_rate(name, per_core, cores, seed0=1000 * k)
+        t_total += wall
+        n_total += total
+    value = n_total / t_total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "config": _config(args, None),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"per step: O1 decode of {per_core} seeded random {name} genomes on each of "
+                                       f"{cores} host processes"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML clocks / throttle reasons sampled every 20 ms during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, torch_device: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            uuid = str(torch.cuda.get_device_properties(torch_device).uuid)
+            h = None
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(hi)
+                u = u.decode() if isinstance(u, bytes) else u
+                if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                    h = hi
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(torch_device)
+            self.h, self.nv = h, pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": len(self.samples)}
+        s = sorted(self.samples)
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
+
+
+# ------------------------------------------------------------------ helpers
+def _config(args, extra):
+    cfg = {"workload": WORKLOADS[args.workload], "table_seed": 0, "population_per_gpu": args.population,
+           "generations_per_step": args.generations, "elites": args.elites,
+           "parallelism": f"islands x{args.gpus} (one GA population per GPU, NCCL elite exchange)",
+           "l2": "inputs larger than L2: two population buffers of P genomes x genome stride "
+                 "(>= 2 x 128 MB at the default P) > 126 MB L2"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def _traffic(workload: str):
+    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="saturn", choices=["saturn", "reference"])
+    ap.add_argument("--workload", default="TXT", choices=sorted(WORKLOADS))
+    ap.add_argument("--population", type=int, default=1 << 22)
+    ap.add_argument("--generations", type=int, default=16)
+    ap.add_argument("--elites", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-per-core", type=int, default=100000)
+    ap.add_argument("--kernel-only-n", type=int, default=1 << 24)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import synth
+    import paper_2309_01226_b200 as sat
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    inst = synth.by_name(args.workload, 0)
+    plan = sat.Plan(inst.node_gpus, local).load_runtime_table(inst.runtime)
+    if world > 1:
+        sat.attach_distributed(plan)
+    T = inst.n_jobs
+    P, G, E = args.population, args.generations, args.elites
+    scfg = sat.SearchConfig(seed=2309, population=P, max_generations=G, elites=E,
+                            generations_per_epoch=max(1, G // 2))
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up
+    for _ in range(max(args.warmup, 0)):
+        plan.search(scfg, stream=stream)
+    barrier()
+
+    # ---- timed region: K steps, device time via CUDA events on the launching stream
+    plan.reset_stats()
+    plan.set_profiling(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evaluated = 0
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = plan.search(scfg, stream=stream)
+            evaluated += r["evaluated"]
+        ev1.record(stream)
+        barrier()
+    st = plan.stats()
+    plan.set_profiling(False)
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    best_ms = r["makespan"]
+    value = evaluated / (dev_ms * 1e-3)          # `evaluated` already sums all ranks
+
+    # ---- e2e: host API with host buffers (table upload + search + best plan to host)
+    plan.reset_stats()
+    barrier()
+    t0 = time.perf_counter()
+    ev_e2e = 0
+    for _ in range(args.steps):
+        plan.load_runtime_table(inst.runtime)
+        r2 = plan.search(scfg, stream=stream)
+        ms_host, placements, _, _ = plan.best_plan()
+        ev_e2e += r2["evaluated"]
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    st_e2e = plan.stats()
+    e2e = {"value": ev_e2e / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": st_e2e["h2d_bytes"] // args.steps,
+           "d2h_bytes_per_step": st_e2e["d2h_bytes"] // args.steps}
+
+    # ---- roofline of the dominant kernel (the fused GA generation + decode kernel)
+    ops = algorithmic_ops_per_plan(T, inst.node_gpus)
+    launch_s = st["ga_kernel_ms"] * 1e-3 / max(st["ga_launches"], 1)
+    units = st["ga_decodes"] / max(st["ga_launches"], 1)
+    achieved = ops * units / launch_s
+    traffic = _traffic(args.workload)
+    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": ALU_PEAK_OPS / 1e12, "unit": "TOP/s",
+                "frac": achieved / ALU_PEAK_OPS, "traffic": traffic,
+                "kernel": "k_ga (Philox GA operators fused with the sorted-multiset decode)",
+                "ops_per_plan": ops, "plans_per_launch": units, "launch_ms": launch_s * 1e3,
+                "kernel_share_of_step": (st["ga_kernel_ms"] / dev_ms)
+                if dev_ms > 0 else None}
+
+    # ---- kernel-only evaluate throughput (K1 alone, genomes resident in HBM)
+    kernel_only = None
+    if rank == 0 and args.kernel_only_n > 0:
+        S = plan.num_configs()
+        n = args.kernel_only_n
+        cfg_h, perm_h = synth.random_genomes(S, n, seed=5)
+        cfg_d, perm_d = torch.from_numpy(cfg_h).cuda(), torch.from_numpy(perm_h).cuda()
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        kernel_only = {}
+        for name, kind in (("thread", sat.DECODER_THREAD), ("warp", sat.DECODER_WARP)):
+            plan.set_decoder(kind)
+            for _ in range(3):
+                plan.evaluate(cfg_d, perm_d, out)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 5
+            a.record()
+            for _ in range(reps):
+                plan.evaluate(cfg_d, perm_d, out)
+            b.record()
+            torch.cuda.synchronize()
+            kernel_only[name] = n * reps / (a.elapsed_time(b) * 1e-3)
+        plan.set_decoder(sat.DECODER_AUTO)
+        kernel_only["unit"] = UNIT
+        kernel_only["genomes"] = n
+        kernel_only["int_probe_ops_per_s"] = plan.probe_int_peak()
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    import oracle
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    lb = oracle.lower_bound(c)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.workload, args.cpu_seconds)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded runtime tables shaped like the paper's workloads; random-init GA)",
+            "config": _config(args, {"best_makespan_s": best_ms, "lower_bound_s": lb,
+                                     "best_over_lb": best_ms / lb}),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"],
+            "clocks": clk.summary(), "kernel_only": kernel_only}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

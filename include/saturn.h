@@ -196,6 +196,22 @@ saturn_status saturn_partition(uint64_t total, int32_t rank, int32_t world, uint
  * chains; *int_ops_per_s = measured integer operations per second (roofline check). */
 saturn_status saturn_probe_int_peak(saturn_plan *p, double *int_ops_per_s);
 
+/* Counters since the last reset (measurement support, row d): kernel launches issued by
+ * the library, host<->device bytes it copied, and -- when profiling is on -- the summed
+ * device time of the GA generation kernel (the dominant kernel of a search), measured
+ * with CUDA events on the launching stream. */
+typedef struct {
+  int64_t kernel_launches;
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+  int64_t ga_launches;      /* GA generation kernels timed (profiling on)            */
+  double ga_kernel_ms;      /* their summed device time                             */
+  int64_t ga_decodes;       /* children decoded by those launches                   */
+} saturn_stats;
+saturn_status saturn_set_profiling(saturn_plan *p, int32_t on);
+saturn_status saturn_get_stats(const saturn_plan *p, saturn_stats *out);
+saturn_status saturn_reset_stats(saturn_plan *p);
+
 const char *saturn_last_error(const saturn_plan *p);
 void saturn_plan_destroy(saturn_plan *p);
 

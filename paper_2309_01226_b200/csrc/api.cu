@@ -123,6 +123,10 @@ struct saturn_plan {
   // communicator
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // measurement
+  bool profiling = false;
+  saturn_stats stats{};
+  std::vector<cudaEvent_t> ev_pool;
   std::string err;
 };
 
@@ -278,6 +282,7 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   }
   CU(p, p->blob.ensure(bytes));
   CU(p, cudaMemcpy(p->blob.p, blob.data(), bytes, cudaMemcpyHostToDevice));
+  p->stats.h2d_bytes += bytes;
   p->T = T;
   p->stride = stride;
   p->blob_bytes = bytes;
@@ -339,6 +344,7 @@ saturn_status saturn_evaluate(saturn_plan* p, const uint8_t* d_cfg, const uint8_
   DeviceGuard dg(p->device);
   CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, kind, d_cfg, d_perm, n, d_makespan, p->sms,
                              static_cast<cudaStream_t>(stream)));
+  p->stats.kernel_launches += 1;
   return SATURN_OK;
 }
 
@@ -364,6 +370,9 @@ saturn_status saturn_evaluate_host(saturn_plan* p, const uint8_t* h_cfg, const u
     CU(p, cudaMemcpyAsync(p->ws_perm.p, h_perm + off * p->T, m * p->T, cudaMemcpyHostToDevice, st));
     CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, kind, p->ws_cfg.p, p->ws_perm.p, m, p->ws_ms.p, p->sms, st));
     CU(p, cudaMemcpyAsync(h_makespan + off, p->ws_ms.p, m * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    p->stats.kernel_launches += 1;
+    p->stats.h2d_bytes += 2 * m * p->T;
+    p->stats.d2h_bytes += m * (int64_t)sizeof(int32_t);
   }
   CU(p, cudaStreamSynchronize(st));
   return SATURN_OK;
@@ -379,6 +388,7 @@ saturn_status saturn_trace(saturn_plan* p, const uint8_t* d_cfg, const uint8_t* 
   DeviceGuard dg(p->device);
   CU(p, sat::launch_trace(p->pb, d_cfg, d_perm, n, d_placements, d_makespan, p->sms,
                           static_cast<cudaStream_t>(stream)));
+  p->stats.kernel_launches += 1;
   return SATURN_OK;
 }
 
@@ -444,6 +454,8 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
   CU(p, p->ws_key.ensure(1));
   CU(p, cudaMemsetAsync(p->ws_key.p, 0xff, sizeof(unsigned long long), st));
   CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, p->ws_key.p, p->sms, st));
+  p->stats.kernel_launches += 1;
+  p->stats.d2h_bytes += 8;
   if (collective && p->comm) {
     NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
   }
@@ -549,6 +561,7 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     }
     CU(p, p->seeds.ensure(packed.size()));
     CU(p, cudaMemcpyAsync(p->seeds.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
+    p->stats.h2d_bytes += (int64_t)packed.size();
   }
   sat::GaParams gp{};
   gp.seed = sp->seed;
@@ -566,12 +579,21 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
                             p->cand.p, &n_cand, p->sms, st));
   if ((size_t)n_cand > p->cand.n) return fail(p, SATURN_ELIMIT, "candidate buffer too small");
   CU(p, sat::launch_select(p->cand.p, n_cand, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
+  p->stats.kernel_launches += 2;
+  // profiling: event pairs around the GA generation kernels (first 512 per search)
+  const int64_t n_prof = p->profiling ? std::min<int64_t>(sp->max_generations, 512) : 0;
+  while ((int64_t)p->ev_pool.size() < 2 * n_prof) {
+    cudaEvent_t e;
+    CU(p, cudaEventCreate(&e));
+    p->ev_pool.push_back(e);
+  }
 
   auto exchange = [&]() -> saturn_status {
     if (!p->comm || p->world < 2) return SATURN_OK;
     NC(p, nccl().allGather(p->rec_ms.p, p->all_ms.p, (size_t)E, ncclInt32, p->comm, st));
     NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
     CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, p->world, E, GS, p->rec_ms.p, p->rec_gen.p, st));
+    p->stats.kernel_launches += 1;
     return SATURN_OK;
   };
   p->hist_t.clear();
@@ -580,6 +602,7 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     int32_t best = 0;
     CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
     CU(p, cudaStreamSynchronize(st));
+    p->stats.d2h_bytes += sizeof best;
     p->hist_t.push_back(now_s() - t0);
     p->hist_ms.push_back(best);
     return SATURN_OK;
@@ -592,9 +615,13 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   for (; gen <= sp->max_generations; ++gen) {
     gp.gen = (uint32_t)gen;
     const int nxt = cur ^ 1;
+    const bool timed = gen <= n_prof;
+    if (timed) CU(p, cudaEventRecord(p->ev_pool[2 * (gen - 1)], st));
     CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
                                     p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, &n_cand, p->sms, st));
+    if (timed) CU(p, cudaEventRecord(p->ev_pool[2 * (gen - 1) + 1], st));
     CU(p, sat::launch_select(p->cand.p, n_cand, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st));
+    p->stats.kernel_launches += 2;
     evaluated += (uint64_t)(P - E);
     cur = nxt;
     if (gen % sp->generations_per_epoch == 0) {
@@ -614,6 +641,14 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   CU(p, cudaMemcpyAsync(g0.data(), p->rec_gen.p, GS, cudaMemcpyDeviceToHost, st));
   CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
   CU(p, cudaStreamSynchronize(st));
+  p->stats.d2h_bytes += GS + sizeof best;
+  for (int64_t g = 1; g <= std::min<int64_t>(n_prof, gens_run); ++g) {
+    float ms = 0.f;
+    CU(p, cudaEventElapsedTime(&ms, p->ev_pool[2 * (g - 1)], p->ev_pool[2 * (g - 1) + 1]));
+    p->stats.ga_kernel_ms += ms;
+    p->stats.ga_launches += 1;
+    p->stats.ga_decodes += P - E;
+  }
   p->best_cfg.assign(g0.begin(), g0.begin() + T);
   p->best_perm.assign(g0.begin() + T, g0.begin() + 2 * T);
   p->best_ms = best;
@@ -680,6 +715,9 @@ saturn_status saturn_best_plan(saturn_plan* p, saturn_placement* out, uint8_t* g
     CU(p, cudaMemcpy(out, p->ws_place.p, T * sizeof(saturn_placement), cudaMemcpyDeviceToHost));
     int32_t ms = 0;
     CU(p, cudaMemcpy(&ms, p->ws_ms.p, sizeof ms, cudaMemcpyDeviceToHost));
+    p->stats.kernel_launches += 1;
+    p->stats.h2d_bytes += 2 * T;
+    p->stats.d2h_bytes += T * (int64_t)sizeof(saturn_placement) + (int64_t)sizeof ms;
     if (ms != p->best_ms)
       return fail(p, SATURN_ECUDA, "trace makespan %d != recorded best %lld", ms, (long long)p->best_ms);
   }
@@ -752,6 +790,24 @@ saturn_status saturn_probe_int_peak(saturn_plan* p, double* int_ops_per_s) {
   return SATURN_OK;
 }
 
+saturn_status saturn_set_profiling(saturn_plan* p, int32_t on) {
+  if (!p) return SATURN_EINVAL;
+  p->profiling = on != 0;
+  return SATURN_OK;
+}
+
+saturn_status saturn_get_stats(const saturn_plan* p, saturn_stats* out) {
+  if (!p || !out) return SATURN_EINVAL;
+  *out = p->stats;
+  return SATURN_OK;
+}
+
+saturn_status saturn_reset_stats(saturn_plan* p) {
+  if (!p) return SATURN_EINVAL;
+  p->stats = saturn_stats{};
+  return SATURN_OK;
+}
+
 const char* saturn_last_error(const saturn_plan* p) { return p ? p->err.c_str() : "NULL handle"; }
 
 void saturn_plan_destroy(saturn_plan* p) {
@@ -776,6 +832,7 @@ void saturn_plan_destroy(saturn_plan* p) {
     p->all_gen.release();
     p->seeds.release();
     p->sink.release();
+    for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   }
   delete p;
 }

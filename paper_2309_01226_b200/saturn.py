@@ -28,7 +28,8 @@ EXPORTS = (
     "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
     "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
-    "saturn_partition", "saturn_probe_int_peak", "saturn_last_error", "saturn_plan_destroy",
+    "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
+    "saturn_reset_stats", "saturn_last_error", "saturn_plan_destroy",
 )
 
 
@@ -51,6 +52,14 @@ PLACEMENT_DTYPE = np.dtype([("node", "<i4"), ("upp", "<i4"), ("gpus", "<i4"), ("
 class Result(ctypes.Structure):
     _fields_ = [("makespan", ctypes.c_int64), ("genome_index", ctypes.c_uint64), ("evaluated", ctypes.c_uint64),
                 ("seconds", ctypes.c_double), ("flags", ctypes.c_int32), ("generations", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("ga_launches", ctypes.c_int64), ("ga_kernel_ms", ctypes.c_double), ("ga_decodes", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -100,6 +109,9 @@ def load_library(path: str = LIB_PATH):
         "saturn_plan_attach_comm": [h, P(u8), i32, i32],
         "saturn_partition": [u64, i32, i32, P(u64), P(u64)],
         "saturn_probe_int_peak": [h, P(ctypes.c_double)],
+        "saturn_set_profiling": [h, i32],
+        "saturn_get_stats": [h, P(Stats)],
+        "saturn_reset_stats": [h],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
@@ -347,6 +359,17 @@ class Plan:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         self._check(self._lib.saturn_plan_attach_comm(self._h, buf, rank, world), "saturn_plan_attach_comm")
 
+    def set_profiling(self, on: bool = True):
+        self._check(self._lib.saturn_set_profiling(self._h, int(bool(on))), "saturn_set_profiling")
+
+    def stats(self) -> dict:
+        st = Stats()
+        self._check(self._lib.saturn_get_stats(self._h, ctypes.byref(st)), "saturn_get_stats")
+        return st.as_dict()
+
+    def reset_stats(self):
+        self._check(self._lib.saturn_reset_stats(self._h), "saturn_reset_stats")
+
     def probe_int_peak(self) -> float:
         v = ctypes.c_double()
         self._check(self._lib.saturn_probe_int_peak(self._h, ctypes.byref(v)), "saturn_probe_int_peak")
@@ -378,17 +401,23 @@ def best_plan(plan: Plan):
     return plan.best_plan()
 
 
-def attach_distributed(plan: Plan, group=None):
-    """Create the library's NCCL communicator over a torch.distributed group: rank 0 makes
-    the unique id, torch.distributed broadcasts it, every rank attaches (row e)."""
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 creates the NCCL unique id, torch.distributed broadcasts its 128 bytes
+    (any backend: nccl on GPU boxes, gloo in CPU tests)."""
     import torch
     import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    rank = dist.get_rank(group)
     uid = get_unique_id() if rank == 0 else bytes(128)
     buf = torch.tensor(list(uid), dtype=torch.uint8)
     if dist.get_backend(group) == "nccl":
         buf = buf.cuda()
     dist.broadcast(buf, src=0, group=group)
-    uid = bytes(buf.cpu().tolist())
-    plan.attach_comm(uid, rank, world)
+    return bytes(buf.cpu().tolist())
+
+
+def attach_distributed(plan: Plan, group=None):
+    """Create the library's NCCL communicator over a torch.distributed group (row e)."""
+    import torch.distributed as dist
+    uid = broadcast_unique_id(group)
+    plan.attach_comm(uid, dist.get_rank(group), dist.get_world_size(group))
     return uid
