@@ -1,33 +1,43 @@
 """a7: GA operator replay (reference definitions).  TEST INFRASTRUCTURE ONLY.
 
 The paper has no search heuristic besides its MILP; the genetic search is
-this build's design, so this module *is* its definition, written out
-step by step.  The CUDA search must reproduce it bit for bit from the same inputs.
+this build's design, so this module *is* its
+definition, written out step by step.  The CUDA search must reproduce it bit for bit from
+the same inputs.
 
 Genome: cfg[t] in [0, S_t) per job t, perm = priority permutation of job ids.
 Population of P genomes per rank with makespans ms[i]; order key of slot i is (ms[i], i).
-Philox stream of a slot (oracle.philox.Stream) with key (seed_lo, seed_hi):
-    initial genome: counters (slot, 0, rank << 16 | 1)
-    child of gen g: counters (slot, g, rank << 16 | 0)          (g = the child's generation)
 Thresholds are q32 integers: an event with probability p fires iff u32 < p_q32.
+U(n, w) = (w * n) >> 32.
 
-Generation g -> g+1:
-  slots [0, E): the E elites, i.e. the E smallest (ms, slot) of generation g in order
-                (or the migrated global elites at an epoch boundary, see ``migrate``);
-                copied with their makespan, not re-decoded;
-  slot k >= E : 1. tournament x2: i = U(P), j = U(P); parent A = smaller (ms, slot);
-                   again for parent B;
-                2. crossover gate: u32 < p_x, else the child copies A (steps 3-4 skipped);
-                3. cfg genes: bit t of the (t // 32)-th u32 word; 1 -> A's gene, 0 -> B's;
-                4. OX1: a = U(T), b = U(T), swapped so a <= b; keep A.perm[a..b]; fill
-                   positions b+1, b+2, ... (cyclic) with B's genes read from position b+1
-                   (cyclic), skipping genes already present;
-                5. cfg mutation, t = 0..T-1: if u32 < p_c then cfg[t] = U(S_t);
-                6. perm mutation: if u32 < p_m: kind = u32 & 1, i = U(T), j = U(T);
-                   kind 0 swaps positions i and j, kind 1 removes the gene at i and
-                   reinserts it at position j.
-Initial genome of slot k (>= number of seed genomes): cfg[t] = U(S_t) for t = 0..T-1,
-then a Fisher-Yates shuffle of the identity: for i = T-1 down to 1, j = U(i+1), swap.
+Philox4x32-10 (oracle/philox.py), key (seed_lo, seed_hi).  Word k of a stream with
+counters (c0, c1, c2) is word k % 4 of philox((c0, c1, c2, k // 4)).
+
+Initial genome of slot k (>= number of seed genomes), stream (k, 0, rank << 16 | 1), words
+consumed in order: cfg[t] = U(S_t) for t = 0..T-1, then a Fisher-Yates shuffle of the
+identity: for i = T-1 down to 1, j = U(i+1), swap perm[i], perm[j].
+
+Child of slot k >= E in generation g (GA v3: every word has a FIXED position, so the
+draws never depend on earlier outcomes; 16-bit fields are lo = w & 0xFFFF, hi = w >> 16,
+V(n, h) = (h * n) >> 16 and a 16-bit gate with q32 threshold p fires iff h < p >> 16),
+stream (k, g, rank << 16 | 0):
+   w0, w1   tournament for parent A: i = U(P, w0), j = U(P, w1); A = smaller (ms, slot)
+   w2, w3   tournament for parent B, same rule
+   w4       lo: crossover gate (p_x)          hi: OX1 cut a = V(T, hi)
+   w5       lo: OX1 cut b = V(T, lo)          hi: permutation-mutation gate (p_m)
+   w6       lo: mutation kind = lo & 1        hi: mutation position i = V(T, hi)
+   w7       lo: mutation position j = V(T, lo) hi: config-mutation gate (p_c)
+   w8       lo: mutated job t* = V(T, lo)     hi: its new gene V(S_t*, hi)
+   w9 .. w9+nb-1   crossover bits, nb = ceil(T/32): bit t of word t // 32, 1 -> A's cfg gene
+ Steps, in order:
+   1. tournaments;  2. child = copy of A;
+   3. if crossover: cfg[t] = B.cfg[t] where bit t is 0;
+   4. if crossover: OX1 -- a, b swapped so a <= b; keep A.perm[a..b]; fill positions b+1,
+      b+2, ... (cyclic) with B's genes read from position b+1 (cyclic), skipping genes in
+      A's slice;
+   5. if config mutation: cfg[t*] = new gene;
+   6. if permutation mutation: kind 0 swaps positions i and j; kind 1 removes the gene at i
+      and reinserts it at position j.
 """
 from __future__ import annotations
 
@@ -73,44 +83,46 @@ def elites(ms, E: int):
 def make_child(S, cfg, perm, ms, slot: int, gen: int, seed: int, rank: int,
                p_x: int, p_c: int, p_m: int):
     P, T = cfg.shape
+    nb = (T + 31) // 32
     st = Stream(_key(seed), slot, gen, (rank << 16) | 0)
+    w = [st.u32() for _ in range(9 + nb)]                # every word has a fixed position
+    lo = [x & 0xFFFF for x in w]
+    hi = [x >> 16 for x in w]
 
-    def tournament():
-        i, j = st.below(P), st.below(P)
+    def U(n, x):
+        return (x * n) >> 32
+
+    def V(n, h):
+        return (h * n) >> 16
+
+    def tournament(wi, wj):
+        i, j = U(P, wi), U(P, wj)
         return i if (int(ms[i]), i) < (int(ms[j]), j) else j
 
-    a_idx = tournament()
-    b_idx = tournament()
-    A_cfg, A_perm = list(cfg[a_idx]), list(perm[a_idx])
+    a_idx = tournament(w[0], w[1])
+    b_idx = tournament(w[2], w[3])
+    child_cfg, child_perm = list(cfg[a_idx]), list(perm[a_idx])
     B_cfg, B_perm = list(cfg[b_idx]), list(perm[b_idx])
-    if st.u32() < p_x:
-        words = [st.u32() for _ in range((T + 31) // 32)]
-        child_cfg = [A_cfg[t] if (words[t // 32] >> (t % 32)) & 1 else B_cfg[t] for t in range(T)]
-        a, b = st.below(T), st.below(T)
+    if lo[4] < (p_x >> 16):
+        for t in range(T):
+            if not (w[9 + t // 32] >> (t % 32)) & 1:
+                child_cfg[t] = B_cfg[t]
+        a, b = V(T, hi[4]), V(T, lo[5])
         if a > b:
             a, b = b, a
-        child_perm = [None] * T
-        used = set()
-        for p in range(a, b + 1):
-            child_perm[p] = A_perm[p]
-            used.add(A_perm[p])
+        kept = set(child_perm[a:b + 1])
         pos = (b + 1) % T
-        rd = (b + 1) % T
-        for _ in range(T - (b - a + 1)):
-            while B_perm[rd] in used:
-                rd = (rd + 1) % T
-            child_perm[pos] = B_perm[rd]
-            used.add(B_perm[rd])
-            pos = (pos + 1) % T
-            rd = (rd + 1) % T
-    else:
-        child_cfg, child_perm = A_cfg, A_perm
-    for t in range(T):
-        if st.u32() < p_c:
-            child_cfg[t] = st.below(int(S[t]))
-    if st.u32() < p_m:
-        kind = st.u32() & 1
-        i, j = st.below(T), st.below(T)
+        for k in range(T):
+            x = B_perm[(b + 1 + k) % T]
+            if x not in kept:
+                child_perm[pos] = x
+                pos = (pos + 1) % T
+    if hi[7] < (p_c >> 16):
+        t = V(T, lo[8])
+        child_cfg[t] = V(int(S[t]), hi[8])
+    if hi[5] < (p_m >> 16):
+        kind = lo[6] & 1
+        i, j = V(T, hi[6]), V(T, lo[7])
         if kind == 0:
             child_perm[i], child_perm[j] = child_perm[j], child_perm[i]
         else:

@@ -255,8 +255,8 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   }
   if (sum_max >= (int64_t(1) << 26))
     return fail(p, SATURN_EINVAL, "sum of per-job max runtimes %lld >= 2^26 s", (long long)sum_max);
-  int stride = 0;
-  for (int t = 0; t < T; ++t) stride = std::max(stride, (int)gs[t].size());
+  int stride = 0;  // max_t S_t plus one zero sentinel column (invalid genes decode to it)
+  for (int t = 0; t < T; ++t) stride = std::max(stride, (int)gs[t].size() + 1);
   const int raw = 4 * T * stride + T + T * stride;
   const int bytes = (raw + 15) & ~15;
   if (bytes > 48 * 1024) return fail(p, SATURN_ELIMIT, "packed table %d B > 48 KB", bytes);

@@ -88,37 +88,62 @@ __device__ __forceinline__ void stage_problem(uint8_t* s_blob, const Problem& pb
 }
 
 // ------------------------------------------------------------------ Philox4x32-10
-// Salmon et al. SC'11; counters (c0, c1, c2, block) and key (k0, k1).
+// Salmon et al. SC'11; counters (c0, c1, c2, c3) and key (k0, k1); 10 rounds.
+__device__ __forceinline__ uint4 philox_block(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                              uint32_t c3) {
+  uint32_t x0 = c0, x1 = c1, x2 = c2, x3 = c3, a = k0, b = k1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { a += 0x9E3779B9u; b += 0xBB67AE85u; }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, x0), lo0 = 0xD2511F53u * x0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, x2), lo1 = 0xCD9E8D57u * x2;
+    const uint32_t y0 = hi1 ^ x1 ^ a, y2 = hi0 ^ x3 ^ b;
+    x0 = y0; x1 = lo1; x2 = y2; x3 = lo0;
+  }
+  return make_uint4(x0, x1, x2, x3);
+}
+
+// U(n) = (u32 * n) >> 32, an integer in [0, n)
+__device__ __forceinline__ uint32_t ubelow(uint32_t u, uint32_t n) { return (uint32_t)(((uint64_t)u * n) >> 32); }
+// V(n) on a 16-bit field h: (h * n) >> 16, an integer in [0, n) for n <= 65536
+__device__ __forceinline__ uint32_t v16(uint32_t h, uint32_t n) { return (h * n) >> 16; }
+
+// Sequential stream: word k = word k % 4 of block k / 4 (used where every lane draws the
+// same number of words at the same program points, so refills never diverge).
 struct Philox {
   uint32_t k0, k1, c0, c1, c2, block;
   uint32_t b0, b1, b2, b3;  // unread words of the current block, consumed front first
   int left;
   __device__ __forceinline__ Philox(uint64_t seed, uint32_t a, uint32_t b, uint32_t c)
       : k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), c0(a), c1(b), c2(c), block(0), left(0) {}
-  __device__ __forceinline__ void refill() {
-    uint32_t x0 = c0, x1 = c1, x2 = c2, x3 = block, a = k0, b = k1;
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-      if (r) { a += 0x9E3779B9u; b += 0xBB67AE85u; }
-      uint32_t hi0 = __umulhi(0xD2511F53u, x0), lo0 = 0xD2511F53u * x0;
-      uint32_t hi1 = __umulhi(0xCD9E8D57u, x2), lo1 = 0xCD9E8D57u * x2;
-      uint32_t y0 = hi1 ^ x1 ^ a, y2 = hi0 ^ x3 ^ b;
-      x0 = y0; x1 = lo1; x2 = y2; x3 = lo0;
-    }
-    b0 = x0; b1 = x1; b2 = x2; b3 = x3;
-    ++block;
-    left = 4;
-  }
   __device__ __forceinline__ uint32_t u32() {
-    if (left == 0) refill();
-    uint32_t v = b0;
+    if (left == 0) {
+      const uint4 v = philox_block(k0, k1, c0, c1, c2, block);
+      b0 = v.x; b1 = v.y; b2 = v.z; b3 = v.w;
+      ++block;
+      left = 4;
+    }
+    const uint32_t v = b0;
     b0 = b1; b1 = b2; b2 = b3;
     --left;
     return v;
   }
-  // U(n) = (u32 * n) >> 32
-  __device__ __forceinline__ uint32_t below(uint32_t n) {
-    return (uint32_t)(((uint64_t)u32() * n) >> 32);
+  __device__ __forceinline__ uint32_t below(uint32_t n) { return ubelow(u32(), n); }
+};
+
+// Fixed-position words: word(k) for any k, recomputing block k / 4 only when it changes.
+// Callers request words at warp-uniform program points with warp-uniform k.
+struct PhiloxWords {
+  uint32_t k0, k1, c0, c1, c2;
+  uint32_t blk;
+  uint4 cur;
+  __device__ __forceinline__ PhiloxWords(uint64_t seed, uint32_t a, uint32_t b, uint32_t c)
+      : k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), c0(a), c1(b), c2(c), blk(0xffffffffu) {}
+  __device__ __forceinline__ uint4 block(uint32_t b) const { return philox_block(k0, k1, c0, c1, c2, b); }
+  __device__ __forceinline__ uint32_t word(uint32_t k) {
+    if ((k >> 2) != blk) { blk = k >> 2; cur = block(blk); }
+    const uint32_t j = k & 3u;
+    return j == 0 ? cur.x : (j == 1 ? cur.y : (j == 2 ? cur.z : cur.w));
   }
 };
 

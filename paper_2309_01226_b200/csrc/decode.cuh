@@ -83,11 +83,12 @@ struct IlvGenome {
   __device__ __forceinline__ int perm(int i) const { return at(T + i); }
 };
 
-// T design.  `tab` = packed (g << 24 | R) words [T][stride] in shared memory, `S` the
-// configs per job; `gen` is a genome accessor.
-// With CHECK, invalid genomes (perm not a permutation of 0..T-1, cfg[t] >= S_t) return -1;
-// `mask` is this thread's scratch bit set (ceil(T/32) words, `mstride` words apart).
-template <int NN, int GP, bool CHECK, class G>
+// T design.  `tab` = packed (g << 24 | R) words [T][stride] in shared memory (column
+// stride-1 of every row is a zero sentinel), `S` the configs per job; `gen` a genome accessor.
+// CHECK = 0: genome trusted.  CHECK = 1 (T <= 32) / 2 (any T): invalid genomes (perm not a
+// permutation of 0..T-1, cfg[t] >= S_t) return -1; mode 1 keeps the seen-set in a register,
+// mode 2 in `mask` (this thread's ceil(T/32) scratch words, `mstride` words apart).
+template <int NN, int GP, int CHECK, class G>
 __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
                                              int stride, const G& gen, int T, const Problem& pb,
                                              uint32_t* mask = nullptr, int mstride = 0) {
@@ -98,29 +99,33 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
     for (int i = 0; i < GP; ++i) a[n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
 
   bool bad = false;
-  if constexpr (CHECK) {
+  int maxt = 0;
+  uint32_t seen = 0u, minw = 0xffffffffu;
+  if constexpr (CHECK == 2) {
     for (int w = 0; w < (T + 31) / 32; ++w) mask[w * mstride] = 0u;
   }
   int ms = 0;
   for (int p = 0; p < T; ++p) {
     int t = gen.perm(p);
     int c;
-    if constexpr (CHECK) {
-      bad |= t >= T;
+    if constexpr (CHECK != 0) {
+      maxt = max(maxt, t);
       t = min(t, T - 1);
-      uint32_t* mw = mask + (t >> 5) * mstride;
-      const uint32_t bit = 1u << (t & 31);
-      const uint32_t m = *mw;
-      bad |= (m & bit) != 0;
-      *mw = m | bit;
-      c = gen.cfg(t);
-      const int st = S[t];
-      bad |= c >= st;
-      c = min(c, st - 1);
+      if constexpr (CHECK == 1) {
+        seen |= 1u << t;
+      } else {
+        uint32_t* mw = mask + (t >> 5) * mstride;
+        const uint32_t bit = 1u << (t & 31);
+        const uint32_t m = *mw;
+        bad |= (m & bit) != 0;
+        *mw = m | bit;
+      }
+      c = min(gen.cfg(t), stride - 1);   // out-of-range genes land on the zero sentinel
     } else {
       c = gen.cfg(t);
     }
     const uint32_t w = tab[t * stride + c];
+    if constexpr (CHECK != 0) minw = min(minw, w);
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
     int v;
@@ -153,7 +158,11 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
     }
     ms = max(ms, v);
   }
-  if constexpr (CHECK) return bad ? -1 : ms;
+  if constexpr (CHECK == 1) bad = __popc(seen) != T;
+  if constexpr (CHECK != 0) {
+    bad |= maxt >= T || minw == 0u;
+    return bad ? -1 : ms;
+  }
   return ms;
 }
 

@@ -43,10 +43,10 @@ __device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
 }
 // `lst` is a warp-distributed ascending list (lane k = k-th smallest key seen); insert
 // each lane's `key` if it beats the E-th entry.  Keys are unique.
-__device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E) {
+__device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E, uint64_t cap = ~0ull) {
   const int lane = threadIdx.x & 31;
   uint64_t thr = shfl_u64(lst, E - 1);
-  uint32_t cm = __ballot_sync(0xffffffffu, key < thr);
+  uint32_t cm = __ballot_sync(0xffffffffu, key < thr && key <= cap);
   while (cm) {
     const int src = __ffs(cm) - 1;
     cm &= cm - 1;
@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     }
     if (first + tid < n) {
       RowGenome gen{bc + tid * T, bp + tid * T};
-      out[first + tid] = decode_sorted<NN, GP, true>(tab, S, pb.stride, gen, T, pb, s_mask + tid, EVAL_B);
+      out[first + tid] = (T <= 32) ? decode_sorted<NN, GP, 1>(tab, S, pb.stride, gen, T, pb)
+                                   : decode_sorted<NN, GP, 2>(tab, S, pb.stride, gen, T, pb, s_mask + tid, EVAL_B);
     }
     __syncthreads();
   }
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
       gen.at(T + p) = (uint8_t)x;
     }
     for (uint64_t idx = i0; idx < i1; ++idx) {
-      const int ms = decode_sorted<NN, GP, false>(tab, S, pb.stride, gen, T, pb);
+      const int ms = decode_sorted<NN, GP, 0>(tab, S, pb.stride, gen, T, pb);
       const uint64_t key = ((uint64_t)ms << 38) | idx;
       best = key < best ? key : best;
       // odometer over cfg (job 0 least significant), carry into perm
@@ -352,7 +353,7 @@ cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace&
 // Thread-private genomes live word-interleaved in shared memory: child (GS/4 words) then
 // parent B (GS/4 words), then the OX1 slice bit set (8 words), each row GA_B words wide.
 static size_t ga_smem_bytes(const Problem& pb, int GS) {
-  return (size_t)pb.blob_bytes + (size_t)4 * GA_B * (2 * (GS / 4) + 8) + 8;
+  return (size_t)pb.blob_bytes + (size_t)4 * GA_B * (2 * (GS / 4) + 8) + 8 * GA_B + 8;
 }
 
 // Copy a GS-byte global record into an interleaved smem genome (and back).
@@ -375,8 +376,15 @@ __device__ __forceinline__ void store_ilv(uint8_t* __restrict__ g, const uint8_t
   }
 }
 
+// Child construction follows oracle/ga.py (GA v2): every Philox
+// word has a fixed position, so all lanes draw the same blocks at the same program points
+// and the operators run as uniform loops with predicated writes (no divergent refills).
+template <int STATE>
+struct GaMinBlocks {
+  static constexpr int value = STATE <= 8 ? 6 : (STATE <= 32 ? 4 : 2);
+};
 template <int NN, int GP>
-__global__ void __launch_bounds__(GA_B) k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds,
+__global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value) k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds,
                                              int64_t n_seed, const uint8_t* __restrict__ prev_pop,
                                              const int32_t* __restrict__ prev_ms, const int32_t* __restrict__ rec_ms,
                                              const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
@@ -389,28 +397,32 @@ __global__ void __launch_bounds__(GA_B) k_ga(Problem pb, GaParams gp, const uint
   uint8_t* s_child = sm + pb.blob_bytes;
   uint8_t* s_B = s_child + (GS / 4) * row;
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + (GS / 4) * row);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(s_bits + 8 * GA_B);
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + 8 * GA_B);   // [GA_B / 32][32]
+  uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
   const uint8_t* S = S_of(s_blob, pb);
   const int tid = threadIdx.x, lane = tid & 31;
   IlvGenome ch{s_child + 4 * tid, row, T};
   IlvGenome gb{s_B + 4 * tid, row, T};
-  uint32_t* inA = s_bits + tid;  // word w at inA[w * GA_B]
+  uint32_t* inA = s_bits + tid;  // OX1 slice set for T > 64: word w at inA[w * GA_B]
   const uint32_t P = (uint32_t)gp.P;
+  const int nb = (T + 31) / 32;
 
   uint64_t lst = ~0ull;
+  // The next top-E can only contain keys <= the last elite's key (the elites are carried):
+  // only those are offered to the list.
+  const uint64_t cap = (gp.gen == 0) ? ~0ull : (((uint64_t)(uint32_t)rec_ms[gp.E - 1] << 32) | (uint64_t)(gp.E - 1));
   const int64_t nthr = (int64_t)gridDim.x * GA_B;
   for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P; base += nthr) {
     const int64_t slot = base + lane;
     const bool live = slot < gp.P;
     int msv = INT_MAX;
-    if (live) {
-      bool decode = true;
-      if (gp.gen == 0) {
+    if (gp.gen == 0) {  // ---------------- initial population
+      if (live) {
         if (slot < n_seed) {
           load_ilv(ch.base, row, seeds + slot * GS, GS);
-        } else {  // Philox-initialised genome: cfg[t] = U(S_t), then Fisher-Yates on identity
+        } else {  // cfg[t] = U(S_t), then Fisher-Yates on the identity
           Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
           for (int t = 0; t < T; ++t) ch.at(t) = (uint8_t)rng.below(S[t]);
           for (int t = 0; t < T; ++t) ch.at(T + t) = (uint8_t)t;
@@ -421,83 +433,119 @@ __global__ void __launch_bounds__(GA_B) k_ga(Problem pb, GaParams gp, const uint
             ch.at(T + j) = a;
           }
         }
-      } else if (slot < gp.E) {  // elite: copied with its makespan
-        load_ilv(ch.base, row, rec_gen + slot * GS, GS);
-        msv = rec_ms[slot];
-        decode = false;
-      } else {
-        Philox rng(gp.seed, (uint32_t)slot, gp.gen, (gp.rank << 16) | 0u);
-        uint32_t A, B;
-        {
-          const uint32_t i = rng.below(P), j = rng.below(P);
-          const uint64_t ki = ((uint64_t)(uint32_t)prev_ms[i] << 32) | i;
-          const uint64_t kj = ((uint64_t)(uint32_t)prev_ms[j] << 32) | j;
-          A = ki < kj ? i : j;
-        }
-        {
-          const uint32_t i = rng.below(P), j = rng.below(P);
-          const uint64_t ki = ((uint64_t)(uint32_t)prev_ms[i] << 32) | i;
-          const uint64_t kj = ((uint64_t)(uint32_t)prev_ms[j] << 32) | j;
-          B = ki < kj ? i : j;
-        }
+        msv = decode_sorted<NN, GP, 0>(tab, S, pb.stride, ch, T, pb);
+      }
+    } else {  // ---------------- generation gen >= 1
+      const bool elite = live && slot < gp.E;
+      const bool child = live && slot >= gp.E;
+      PhiloxWords rw(gp.seed, (uint32_t)slot, gp.gen, gp.rank << 16);
+      const uint4 w0 = rw.block(0), w1 = rw.block(1), w2 = rw.block(2);
+      rw.blk = 2;
+      rw.cur = w2;
+      uint32_t A = 0, B = 0;
+      if (child) {  // 1. tournaments
+        const uint32_t i1 = ubelow(w0.x, P), j1 = ubelow(w0.y, P), i2 = ubelow(w0.z, P), j2 = ubelow(w0.w, P);
+        const uint32_t m1 = (uint32_t)prev_ms[i1], n1 = (uint32_t)prev_ms[j1];
+        const uint32_t m2 = (uint32_t)prev_ms[i2], n2 = (uint32_t)prev_ms[j2];
+        A = ((((uint64_t)m1 << 32) | i1) < (((uint64_t)n1 << 32) | j1)) ? i1 : j1;
+        B = ((((uint64_t)m2 << 32) | i2) < (((uint64_t)n2 << 32) | j2)) ? i2 : j2;
+      }
+      // 2. child = A (elites: the elite record)
+      if (elite) load_ilv(ch.base, row, rec_gen + slot * GS, GS);
+      if (child) {
         load_ilv(ch.base, row, prev_pop + (uint64_t)A * GS, GS);
-        if (rng.u32() < gp.px) {
-          load_ilv(gb.base, row, prev_pop + (uint64_t)B * GS, GS);
-          uint32_t word = 0;
-          for (int t = 0; t < T; ++t) {  // uniform crossover of the config genes
-            if ((t & 31) == 0) word = rng.u32();
-            if (!((word >> (t & 31)) & 1u)) ch.at(t) = gb.at(t);
-          }
-          uint32_t a = rng.below(T), b = rng.below(T);  // OX1 on the permutation
-          if (a > b) { const uint32_t x = a; a = b; b = x; }
-          for (int w = 0; w < (T + 31) / 32; ++w) inA[w * GA_B] = 0u;
-          for (uint32_t q = a; q <= b; ++q) {
+        load_ilv(gb.base, row, prev_pop + (uint64_t)B * GS, GS);
+      }
+      const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
+      const bool xo = child && (w1.x & 0xffffu) < px16;
+      uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
+      if (a > b) { const uint32_t x = a; a = b; b = x; }
+      // 3. uniform crossover of the config genes (bits from words 9 .. 9+nb-1)
+      uint32_t bits = 0;
+      for (int t = 0; t < T; ++t) {
+        if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
+        const bool takeB = xo && !((bits >> (t & 31)) & 1u);
+        const uint8_t gA = ch.at(t), gB = gb.at(t);
+        ch.at(t) = takeB ? gB : gA;
+      }
+      // 4. OX1: keep A.perm[a..b], fill the rest with B's order from b+1 (cyclic)
+      if (T <= 64) {
+        uint64_t kept = 0;
+        for (int q = 0; q < T; ++q) {
+          const uint64_t bit = 1ull << ch.at(T + q);
+          kept |= ((uint32_t)q >= a && (uint32_t)q <= b) ? bit : 0ull;
+        }
+        int pos = ((int)b + 1 == T) ? 0 : (int)b + 1;
+        int rd = pos;
+        for (int k = 0; k < T; ++k) {
+          const int x = gb.at(T + rd);
+          rd = (rd + 1 == T) ? 0 : rd + 1;
+          const bool take = xo && !((kept >> x) & 1ull);
+          const uint8_t old = ch.at(T + pos);
+          ch.at(T + pos) = take ? (uint8_t)x : old;
+          pos = take ? ((pos + 1 == T) ? 0 : pos + 1) : pos;
+        }
+      } else {
+        for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
+        for (int q = 0; q < T; ++q)
+          if ((uint32_t)q >= a && (uint32_t)q <= b) {
             const int x = ch.at(T + q);
             inA[(x >> 5) * GA_B] |= 1u << (x & 31);
           }
-          int pos = (b + 1 == (uint32_t)T) ? 0 : (int)b + 1;
-          int rd = pos;
-          const int fill = T - (int)(b - a + 1);
-          for (int k = 0; k < fill; ++k) {
-            int x;
-            while (true) {
-              x = gb.at(T + rd);
-              rd = (rd + 1 == T) ? 0 : rd + 1;
-              if (!((inA[(x >> 5) * GA_B] >> (x & 31)) & 1u)) break;
-            }
-            ch.at(T + pos) = (uint8_t)x;
-            pos = (pos + 1 == T) ? 0 : pos + 1;
-          }
-        }
-        for (int t = 0; t < T; ++t)  // config mutation
-          if (rng.u32() < gp.pc) ch.at(t) = (uint8_t)rng.below(S[t]);
-        if (rng.u32() < gp.pm) {  // permutation mutation: swap or insertion
-          const uint32_t kind = rng.u32() & 1u;
-          const int i = (int)rng.below(T), j = (int)rng.below(T);
-          if (kind == 0) {
-            const uint8_t x = ch.at(T + i);
-            ch.at(T + i) = ch.at(T + j);
-            ch.at(T + j) = x;
-          } else {
-            const uint8_t x = ch.at(T + i);
-            if (i < j) {
-              for (int k = i; k < j; ++k) ch.at(T + k) = ch.at(T + k + 1);
-            } else {
-              for (int k = i; k > j; --k) ch.at(T + k) = ch.at(T + k - 1);
-            }
-            ch.at(T + j) = x;
-          }
+        int pos = ((int)b + 1 == T) ? 0 : (int)b + 1;
+        int rd = pos;
+        for (int k = 0; k < T; ++k) {
+          const int x = gb.at(T + rd);
+          rd = (rd + 1 == T) ? 0 : rd + 1;
+          const bool take = xo && !((inA[(x >> 5) * GA_B] >> (x & 31)) & 1u);
+          const uint8_t old = ch.at(T + pos);
+          ch.at(T + pos) = take ? (uint8_t)x : old;
+          pos = take ? ((pos + 1 == T) ? 0 : pos + 1) : pos;
         }
       }
-      if (decode) msv = decode_sorted<NN, GP, false>(tab, S, pb.stride, ch, T, pb);
+      // 5. config mutation of one job
+      if (child && (w1.w >> 16) < pc16) {
+        const int t = (int)v16(w2.x & 0xffffu, T);
+        ch.at(t) = (uint8_t)v16(w2.x >> 16, S[t]);
+      }
+      // 6. permutation mutation: swap (kind 0) or remove-at-i / insert-at-j (kind 1)
+      const bool pmut = child && (w1.y >> 16) < pm16;
+      if (__any_sync(0xffffffffu, pmut)) {
+        const int kind = (int)(w1.z & 1u);
+        const int mi = (int)v16(w1.z >> 16, T), mj = (int)v16(w1.w & 0xffffu, T);
+        const int xi = ch.at(T + mi), xj = ch.at(T + mj);
+        int carry = 0;
+        int o = ch.at(T);
+        for (int k = 0; k < T; ++k) {
+          const int nx = (k + 1 < T) ? ch.at(T + k + 1) : 0;
+          int val;
+          if (kind == 0) val = (k == mi) ? xj : ((k == mj) ? xi : o);
+          else if (mi < mj) val = (k >= mi && k < mj) ? nx : ((k == mj) ? xi : o);
+          else if (mi > mj) val = (k == mj) ? xi : ((k > mj && k <= mi) ? carry : o);
+          else val = o;
+          ch.at(T + k) = (uint8_t)(pmut ? val : o);
+          carry = o;
+          o = nx;
+        }
+      }
+      if (elite) msv = rec_ms[slot];
+      if (child) msv = decode_sorted<NN, GP, 0>(tab, S, pb.stride, ch, T, pb);
+    }
+    if (live) {
       store_ilv(pop + slot * GS, ch.base, row, GS);
       ms_out[slot] = msv;
     }
     const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
-    topE_insert(lst, key, gp.E);
+    topE_insert(lst, key, gp.E, cap);
   }
-  const int64_t wglob = (int64_t)blockIdx.x * (GA_B / 32) + (tid >> 5);
-  if (lane < gp.E) cand[wglob * gp.E + lane] = lst;
+  // block-level merge of the warps' lists -> one candidate list per block
+  s_lists[tid] = lst;
+  __syncthreads();
+  if (tid < 32) {
+    uint64_t m = ~0ull;
+    for (int w = 0; w < GA_B / 32; ++w) topE_insert(m, s_lists[w * 32 + lane], gp.E);
+    if (lane < gp.E) cand[(int64_t)blockIdx.x * gp.E + lane] = m;
+  }
 }
 
 static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
@@ -509,7 +557,7 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
 #define SAT_GA(a, b)                                                                                        \
   if (NN == a && GP == b) {                                                                                 \
     const int g = grid_for(k_ga<a, b>, GA_B, smem, sms, blocks);                                            \
-    *n_cand = g * (GA_B / 32) * gp.E;                                                                       \
+    *n_cand = g * gp.E;                                                                                     \
     k_ga<a, b><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,   \
                                       cand);                                                                \
     return cudaGetLastError();                                                                              \

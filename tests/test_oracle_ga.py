@@ -53,19 +53,34 @@ def test_ox1_keeps_slice_and_order():
         child_cfg, child_perm = ga.make_child(c.S, cfg, perm, ms, slot, 1, 3, 0,
                                               p_x=0xFFFFFFFF, p_c=0, p_m=0)
         st = Stream((3, 0), slot, 1, 0)
-        i, j = st.below(16), st.below(16)
+        w = [st.u32() for _ in range(10)]
+        i, j = (w[0] * 16) >> 32, (w[1] * 16) >> 32
         A = i if (ms[i], i) < (ms[j], j) else j
-        i, j = st.below(16), st.below(16)
+        i, j = (w[2] * 16) >> 32, (w[3] * 16) >> 32
         B = i if (ms[i], i) < (ms[j], j) else j
-        st.u32()
-        w = st.u32()
-        a, b = sorted((st.below(T), st.below(T)))
+        a, b = sorted((((w[4] >> 16) * T) >> 16, ((w[5] & 0xFFFF) * T) >> 16))
         assert list(child_perm[a:b + 1]) == list(perm[A][a:b + 1])
         rest = [x for x in np.roll(perm[B], -(b + 1)) if x not in set(perm[A][a:b + 1])]
         filled = [child_perm[(b + 1 + k) % T] for k in range(T - (b - a + 1))]
         assert filled == rest
         for t in range(T):
-            assert child_cfg[t] == (cfg[A][t] if (w >> t) & 1 else cfg[B][t])
+            assert child_cfg[t] == (cfg[A][t] if (w[9] >> t) & 1 else cfg[B][t])
+
+
+def test_mutation_only_changes_what_fired():
+    c, cfg, perm, ms = _setup(P=32)
+    T = c.n_jobs
+    for slot in range(4, 32):
+        # no crossover, certain config mutation of one job, no perm mutation
+        cc, cp = ga.make_child(c.S, cfg, perm, ms, slot, 2, 9, 0, p_x=0, p_c=0xFFFFFFFF, p_m=0)
+        cc0, cp0 = ga.make_child(c.S, cfg, perm, ms, slot, 2, 9, 0, p_x=0, p_c=0, p_m=0)
+        assert all(0 <= cc[t] < c.S[t] for t in range(T))
+        assert sum(int(x != y) for x, y in zip(cc, cc0)) <= 1 and list(cp) == list(cp0)
+        cm, pmut = ga.make_child(c.S, cfg, perm, ms, slot, 2, 9, 0, p_x=0, p_c=0, p_m=0xFFFFFFFF)
+        assert sorted(pmut) == list(range(T)) and list(cm) == list(cc0)
+        # nothing fires: the child is parent A
+        cc0, cp0 = ga.make_child(c.S, cfg, perm, ms, slot, 2, 9, 0, p_x=0, p_c=0, p_m=0)
+        assert any((list(cfg[k]) == list(cc0) and list(perm[k]) == list(cp0)) for k in range(32))
 
 
 def test_migration_takes_global_best():
