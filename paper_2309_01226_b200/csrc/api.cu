@@ -14,6 +14,7 @@
 
 #include "../../include/saturn.h"
 #include "kernels.h"
+#include "decode.cuh"
 
 using sat::Problem;
 
@@ -175,7 +176,7 @@ struct DeviceGuard {
   }
 };
 
-int gs_of(int T) { return ((2 * T) + 15) & ~15; }
+int gs_of(int T) { return sat::record_bytes(T); }  // cfg | pad | perm | pad
 
 saturn_status use_decoder_kind(saturn_plan* p, int* kind) {
   int k = p->decoder;
@@ -557,7 +558,7 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     std::vector<uint8_t> packed((size_t)n_seed * GS, 0);
     for (int64_t i = 0; i < n_seed; ++i) {
       memcpy(&packed[i * GS], sp->seed_cfg + i * T, T);
-      memcpy(&packed[i * GS + T], sp->seed_perm + i * T, T);
+      memcpy(&packed[i * GS + sat::perm_offset(T)], sp->seed_perm + i * T, T);
     }
     CU(p, p->seeds.ensure(packed.size()));
     CU(p, cudaMemcpyAsync(p->seeds.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
@@ -650,7 +651,7 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     p->stats.ga_decodes += P - E;
   }
   p->best_cfg.assign(g0.begin(), g0.begin() + T);
-  p->best_perm.assign(g0.begin() + T, g0.begin() + 2 * T);
+  p->best_perm.assign(g0.begin() + sat::perm_offset(T), g0.begin() + sat::perm_offset(T) + T);
   p->best_ms = best;
   p->have_best = true;
   p->have_pop = true;
@@ -694,7 +695,7 @@ saturn_status saturn_search_population(const saturn_plan* p, uint8_t* h_cfg, uin
     return SATURN_ECUDA;
   for (int64_t i = 0; i < P; ++i) {
     if (h_cfg) memcpy(h_cfg + i * T, &buf[i * GS], T);
-    if (h_perm) memcpy(h_perm + i * T, &buf[i * GS + T], T);
+    if (h_perm) memcpy(h_perm + i * T, &buf[i * GS + sat::perm_offset(T)], T);
   }
   return SATURN_OK;
 }

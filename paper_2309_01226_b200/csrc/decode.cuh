@@ -64,24 +64,34 @@ __device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R) {
   return v;
 }
 
-// Genome accessors: RowGenome reads a genome stored as two contiguous T-byte rows (the
-// caller's [n][T] layout, staged tile by tile); IlvGenome reads a thread-private genome kept
-// word-interleaved in shared memory (word w of thread i at base[w * 4 * B + 4 * i]), which is
-// bank-conflict free for any per-lane byte index.  Bytes [0, T) = cfg, [T, 2T) = perm.
+// Genome accessors.  RowGenome reads a genome stored as two T-byte rows (the caller's
+// [n][T] layout, staged tile by tile).  RowG reads a thread-private genome row in shared
+// memory: cfg at bytes [0, T), perm at [Tp, Tp + T) with Tp = roundup4(T) (the GA record
+// layout); rows are an odd number of words apart, so same-index accesses of a warp are
+// bank-conflict free and every byte address is one add.
 struct RowGenome {
   const uint8_t* c;
   const uint8_t* p;
   __device__ __forceinline__ int cfg(int t) const { return c[t]; }
   __device__ __forceinline__ int perm(int i) const { return p[i]; }
 };
-struct IlvGenome {
-  uint8_t* base;   // &smem[4 * tid]
-  int row;         // 4 * blockDim.x
-  int T;
-  __device__ __forceinline__ uint8_t& at(int k) const { return base[(k >> 2) * row + (k & 3)]; }
-  __device__ __forceinline__ int cfg(int t) const { return at(t); }
-  __device__ __forceinline__ int perm(int i) const { return at(T + i); }
+struct RowG {
+  uint8_t* base;
+  int Tp;
+  __device__ __forceinline__ uint8_t& c(int t) const { return base[t]; }
+  __device__ __forceinline__ uint8_t& q(int i) const { return base[Tp + i]; }
+  __device__ __forceinline__ int cfg(int t) const { return base[t]; }
+  __device__ __forceinline__ int perm(int i) const { return base[Tp + i]; }
 };
+__host__ __device__ __forceinline__ int perm_offset(int T) { return (T + 3) & ~3; }
+// record bytes of a genome (cfg | pad | perm | pad), multiple of 16
+__host__ __device__ __forceinline__ int record_bytes(int T) { return (perm_offset(T) + T + 15) & ~15; }
+// smem row stride >= bytes, an odd number of 4-byte words
+__host__ __device__ __forceinline__ int odd_row_stride(int bytes) {
+  int w = (bytes + 3) / 4;
+  if ((w & 1) == 0) ++w;
+  return 4 * w;
+}
 
 // T design.  `tab` = packed (g << 24 | R) words [T][stride] in shared memory (column
 // stride-1 of every row is a zero sentinel), `S` the configs per job; `gen` a genome accessor.

@@ -249,7 +249,7 @@ cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* p
 // Consecutive indices advance cfg like an odometer (job 0 fastest), then perm by
 // next_permutation, so only the first index of a chunk is unranked.
 static size_t enum_smem_bytes(const Problem& pb) {
-  return (size_t)pb.blob_bytes + (size_t)4 * ENUM_B * ((2 * pb.T + 3) / 4) + 32 * 8 + 8;
+  return (size_t)pb.blob_bytes + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) + 32 * 8 + 8;
 }
 
 template <int NN, int GP>
@@ -259,13 +259,13 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
   uint8_t* s_blob = sm;
   uint8_t* s_gen = sm + pb.blob_bytes;
   const int T = pb.T;
-  const int words = (2 * T + 3) / 4;
-  uint64_t* s_red = reinterpret_cast<uint64_t*>(s_gen + 4 * ENUM_B * words);
+  const int RS = odd_row_stride(perm_offset(T) + T);
+  uint64_t* s_red = reinterpret_cast<uint64_t*>(s_gen + ((ENUM_B * RS + 7) & ~7));
   uint64_t* bar = s_red + 32;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
   const uint8_t* S = S_of(s_blob, pb);
-  IlvGenome gen{s_gen + 4 * threadIdx.x, 4 * ENUM_B, T};
+  RowG gen{s_gen + RS * threadIdx.x, perm_offset(T)};
 
   uint64_t best = ~0ull;
   const uint64_t total = end - begin;
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
     // unrank i0
     uint64_t r_cfg = i0 % es.cfg_space;
     uint64_t r_perm = i0 / es.cfg_space;
-    for (int t = 0; t < T; ++t) gen.at(t) = (uint8_t)((r_cfg / es.radix[t]) % (uint64_t)S[t]);
+    for (int t = 0; t < T; ++t) gen.c(t) = (uint8_t)((r_cfg / es.radix[t]) % (uint64_t)S[t]);
     uint32_t avail = (T == 32) ? 0xffffffffu : ((1u << T) - 1u);
     for (int p = 0; p < T; ++p) {
       const uint64_t f = es.fact[T - 1 - p];
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
       for (int k = 0; k < d; ++k) m &= m - 1;
       const int x = __ffs(m) - 1;
       avail &= ~(1u << x);
-      gen.at(T + p) = (uint8_t)x;
+      gen.q(p) = (uint8_t)x;
     }
     for (uint64_t idx = i0; idx < i1; ++idx) {
       const int ms = decode_sorted<NN, GP, 0>(tab, S, pb.stride, gen, T, pb);
@@ -297,19 +297,19 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
       // odometer over cfg (job 0 least significant), carry into perm
       int t = 0;
       for (; t < T; ++t) {
-        const int c = gen.at(t) + 1;
-        if (c < S[t]) { gen.at(t) = (uint8_t)c; break; }
-        gen.at(t) = 0;
+        const int c = gen.c(t) + 1;
+        if (c < S[t]) { gen.c(t) = (uint8_t)c; break; }
+        gen.c(t) = 0;
       }
       if (t == T) {  // next lexicographic permutation of perm
         int k = T - 2;
-        while (k >= 0 && gen.at(T + k) >= gen.at(T + k + 1)) --k;
+        while (k >= 0 && gen.q(k) >= gen.q(k + 1)) --k;
         if (k >= 0) {
           int l = T - 1;
-          while (gen.at(T + l) <= gen.at(T + k)) --l;
-          uint8_t tmp = gen.at(T + k); gen.at(T + k) = gen.at(T + l); gen.at(T + l) = tmp;
+          while (gen.q(l) <= gen.q(k)) --l;
+          uint8_t tmp = gen.q(k); gen.q(k) = gen.q(l); gen.q(l) = tmp;
           for (int a = k + 1, b = T - 1; a < b; ++a, --b) {
-            tmp = gen.at(T + a); gen.at(T + a) = gen.at(T + b); gen.at(T + b) = tmp;
+            tmp = gen.q(a); gen.q(a) = gen.q(b); gen.q(b) = tmp;
           }
         }
       }
@@ -350,62 +350,62 @@ cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace&
 }
 
 // ------------------------------------------------------------------ K3 (+K1): GA
-// Thread-private genomes live word-interleaved in shared memory: child (GS/4 words) then
-// parent B (GS/4 words), then the OX1 slice bit set (8 words), each row GA_B words wide.
+// Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
+// then parent B, then the OX1 slice bit set for T > 32 (8 words, interleaved per thread).
 static size_t ga_smem_bytes(const Problem& pb, int GS) {
-  return (size_t)pb.blob_bytes + (size_t)4 * GA_B * (2 * (GS / 4) + 8) + 8 * GA_B + 8;
+  return (size_t)pb.blob_bytes + (size_t)2 * GA_B * odd_row_stride(GS) + (size_t)4 * 8 * GA_B + 8 * GA_B + 8;
 }
 
-// Copy a GS-byte global record into an interleaved smem genome (and back).
-__device__ __forceinline__ void load_ilv(uint8_t* base, int row, const uint8_t* __restrict__ g, int GS) {
+// Copy a GS-byte global record into a smem row (4-byte stores) and back.
+__device__ __forceinline__ void load_row(uint8_t* row, const uint8_t* __restrict__ g, int GS) {
   const uint4* src = reinterpret_cast<const uint4*>(g);
+  uint32_t* d = reinterpret_cast<uint32_t*>(row);
   for (int k = 0; k < GS / 16; ++k) {
     const uint4 v = src[k];
-    uint32_t* d = reinterpret_cast<uint32_t*>(base + (4 * k) * row);
-    d[0] = v.x;
-    d[row / 4] = v.y;
-    d[2 * (row / 4)] = v.z;
-    d[3 * (row / 4)] = v.w;
+    d[4 * k] = v.x;
+    d[4 * k + 1] = v.y;
+    d[4 * k + 2] = v.z;
+    d[4 * k + 3] = v.w;
   }
 }
-__device__ __forceinline__ void store_ilv(uint8_t* __restrict__ g, const uint8_t* base, int row, int GS) {
+__device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t* row, int GS) {
   uint4* dst = reinterpret_cast<uint4*>(g);
-  for (int k = 0; k < GS / 16; ++k) {
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(base + (4 * k) * row);
-    dst[k] = make_uint4(s[0], s[row / 4], s[2 * (row / 4)], s[3 * (row / 4)]);
-  }
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(row);
+  for (int k = 0; k < GS / 16; ++k) dst[k] = make_uint4(s[4 * k], s[4 * k + 1], s[4 * k + 2], s[4 * k + 3]);
 }
 
-// Child construction follows oracle/ga.py (GA v2): every Philox
-// word has a fixed position, so all lanes draw the same blocks at the same program points
-// and the operators run as uniform loops with predicated writes (no divergent refills).
 template <int STATE>
 struct GaMinBlocks {
   static constexpr int value = STATE <= 8 ? 6 : (STATE <= 32 ? 4 : 2);
 };
+
+// Child construction follows oracle/ga.py (GA v3): every Philox
+// word has a fixed position, so all lanes draw the same blocks at the same program points
+// and the operators run as uniform loops with predicated writes (no divergent refills).
 template <int NN, int GP>
-__global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value) k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds,
-                                             int64_t n_seed, const uint8_t* __restrict__ prev_pop,
-                                             const int32_t* __restrict__ prev_ms, const int32_t* __restrict__ rec_ms,
-                                             const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
-                                             int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand) {
+__global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
+    k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
+         const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
+         const int32_t* __restrict__ rec_ms, const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
+         int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int T = pb.T;
   const int GS = gp.GS;
-  const int row = 4 * GA_B;
+  const int RS = odd_row_stride(GS);
+  const int Tp = perm_offset(T);
   uint8_t* s_blob = sm;
   uint8_t* s_child = sm + pb.blob_bytes;
-  uint8_t* s_B = s_child + (GS / 4) * row;
-  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + (GS / 4) * row);
+  uint8_t* s_B = s_child + GA_B * RS;
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + 8 * GA_B);   // [GA_B / 32][32]
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
   const uint8_t* S = S_of(s_blob, pb);
   const int tid = threadIdx.x, lane = tid & 31;
-  IlvGenome ch{s_child + 4 * tid, row, T};
-  IlvGenome gb{s_B + 4 * tid, row, T};
-  uint32_t* inA = s_bits + tid;  // OX1 slice set for T > 64: word w at inA[w * GA_B]
+  const RowG ch{s_child + RS * tid, Tp};
+  const RowG gb{s_B + RS * tid, Tp};
+  uint32_t* inA = s_bits + tid;  // OX1 slice set for T > 32: word w at inA[w * GA_B]
   const uint32_t P = (uint32_t)gp.P;
   const int nb = (T + 31) / 32;
 
@@ -421,16 +421,17 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value) k_ga(Proble
     if (gp.gen == 0) {  // ---------------- initial population
       if (live) {
         if (slot < n_seed) {
-          load_ilv(ch.base, row, seeds + slot * GS, GS);
+          load_row(ch.base, seeds + slot * GS, GS);
         } else {  // cfg[t] = U(S_t), then Fisher-Yates on the identity
           Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
-          for (int t = 0; t < T; ++t) ch.at(t) = (uint8_t)rng.below(S[t]);
-          for (int t = 0; t < T; ++t) ch.at(T + t) = (uint8_t)t;
+          for (int t = 0; t < GS; ++t) ch.base[t] = 0;
+          for (int t = 0; t < T; ++t) ch.c(t) = (uint8_t)rng.below(S[t]);
+          for (int t = 0; t < T; ++t) ch.q(t) = (uint8_t)t;
           for (int i = T - 1; i > 0; --i) {
             const int j = (int)rng.below(i + 1);
-            const uint8_t a = ch.at(T + i);
-            ch.at(T + i) = ch.at(T + j);
-            ch.at(T + j) = a;
+            const uint8_t a = ch.q(i);
+            ch.q(i) = ch.q(j);
+            ch.q(j) = a;
           }
         }
         msv = decode_sorted<NN, GP, 0>(tab, S, pb.stride, ch, T, pb);
@@ -451,88 +452,92 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value) k_ga(Proble
         B = ((((uint64_t)m2 << 32) | i2) < (((uint64_t)n2 << 32) | j2)) ? i2 : j2;
       }
       // 2. child = A (elites: the elite record)
-      if (elite) load_ilv(ch.base, row, rec_gen + slot * GS, GS);
+      if (elite) load_row(ch.base, rec_gen + slot * GS, GS);
       if (child) {
-        load_ilv(ch.base, row, prev_pop + (uint64_t)A * GS, GS);
-        load_ilv(gb.base, row, prev_pop + (uint64_t)B * GS, GS);
+        load_row(ch.base, prev_pop + (uint64_t)A * GS, GS);
+        load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
       }
       const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
       const bool xo = child && (w1.x & 0xffffu) < px16;
       uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
       if (a > b) { const uint32_t x = a; a = b; b = x; }
-      // 3. uniform crossover of the config genes (bits from words 9 .. 9+nb-1)
-      uint32_t bits = 0;
-      for (int t = 0; t < T; ++t) {
-        if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
-        const bool takeB = xo && !((bits >> (t & 31)) & 1u);
-        const uint8_t gA = ch.at(t), gB = gb.at(t);
-        ch.at(t) = takeB ? gB : gA;
+      // 3. uniform crossover of the config genes (bits from words 9 .. 9+nb-1), 4 genes per step
+      {
+        const uint32_t* ca = reinterpret_cast<const uint32_t*>(ch.base);
+        const uint32_t* cb = reinterpret_cast<const uint32_t*>(gb.base);
+        uint32_t* cw = reinterpret_cast<uint32_t*>(ch.base);
+        uint32_t bits = 0;
+        for (int t = 0; t < T; t += 4) {
+          if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
+          const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;     // 1 -> take B's gene
+          const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;  // nibble -> byte mask
+          const uint32_t wa = ca[t >> 2], wb = cb[t >> 2];
+          cw[t >> 2] = (wa & ~m) | (wb & m);                               // pad bytes: 0 in both
+        }
       }
       // 4. OX1: keep A.perm[a..b], fill the rest with B's order from b+1 (cyclic)
-      if (T <= 64) {
-        uint64_t kept = 0;
+      if (T <= 32) {
+        uint32_t kept = 0;
         for (int q = 0; q < T; ++q) {
-          const uint64_t bit = 1ull << ch.at(T + q);
-          kept |= ((uint32_t)q >= a && (uint32_t)q <= b) ? bit : 0ull;
+          const uint32_t bit = 1u << ch.q(q);
+          kept |= ((uint32_t)q - a <= b - a) ? bit : 0u;
         }
         int pos = ((int)b + 1 == T) ? 0 : (int)b + 1;
         int rd = pos;
         for (int k = 0; k < T; ++k) {
-          const int x = gb.at(T + rd);
+          const int x = gb.q(rd);
           rd = (rd + 1 == T) ? 0 : rd + 1;
-          const bool take = xo && !((kept >> x) & 1ull);
-          const uint8_t old = ch.at(T + pos);
-          ch.at(T + pos) = take ? (uint8_t)x : old;
+          const bool take = xo && !((kept >> x) & 1u);
+          uint8_t& dst = ch.q(pos);
+          dst = take ? (uint8_t)x : dst;
           pos = take ? ((pos + 1 == T) ? 0 : pos + 1) : pos;
         }
       } else {
         for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
-        for (int q = 0; q < T; ++q)
-          if ((uint32_t)q >= a && (uint32_t)q <= b) {
-            const int x = ch.at(T + q);
-            inA[(x >> 5) * GA_B] |= 1u << (x & 31);
-          }
+        for (int q = (int)a; q <= (int)b; ++q) {
+          const int x = ch.q(q);
+          inA[(x >> 5) * GA_B] |= 1u << (x & 31);
+        }
         int pos = ((int)b + 1 == T) ? 0 : (int)b + 1;
         int rd = pos;
         for (int k = 0; k < T; ++k) {
-          const int x = gb.at(T + rd);
+          const int x = gb.q(rd);
           rd = (rd + 1 == T) ? 0 : rd + 1;
           const bool take = xo && !((inA[(x >> 5) * GA_B] >> (x & 31)) & 1u);
-          const uint8_t old = ch.at(T + pos);
-          ch.at(T + pos) = take ? (uint8_t)x : old;
+          uint8_t& dst = ch.q(pos);
+          dst = take ? (uint8_t)x : dst;
           pos = take ? ((pos + 1 == T) ? 0 : pos + 1) : pos;
         }
       }
       // 5. config mutation of one job
       if (child && (w1.w >> 16) < pc16) {
         const int t = (int)v16(w2.x & 0xffffu, T);
-        ch.at(t) = (uint8_t)v16(w2.x >> 16, S[t]);
+        ch.c(t) = (uint8_t)v16(w2.x >> 16, S[t]);
       }
-      // 6. permutation mutation: swap (kind 0) or remove-at-i / insert-at-j (kind 1)
+      // 6. permutation mutation: new[k] = old[src(k)], old kept in B's (now free) row.
+      //    swap i<->j: src(i) = j, src(j) = i; insertion i->j: src(j) = i and the positions
+      //    between shift by one toward i.
       const bool pmut = child && (w1.y >> 16) < pm16;
       if (__any_sync(0xffffffffu, pmut)) {
         const int kind = (int)(w1.z & 1u);
         const int mi = (int)v16(w1.z >> 16, T), mj = (int)v16(w1.w & 0xffffu, T);
-        const int xi = ch.at(T + mi), xj = ch.at(T + mj);
-        int carry = 0;
-        int o = ch.at(T);
+        const int lo = min(mi, mj), hi = max(mi, mj);
+        const int d = (mi < mj) ? 1 : -1;
+        for (int k = 0; k < T; ++k) gb.q(k) = ch.q(k);
         for (int k = 0; k < T; ++k) {
-          const int nx = (k + 1 < T) ? ch.at(T + k + 1) : 0;
-          int val;
-          if (kind == 0) val = (k == mi) ? xj : ((k == mj) ? xi : o);
-          else if (mi < mj) val = (k >= mi && k < mj) ? nx : ((k == mj) ? xi : o);
-          else if (mi > mj) val = (k == mj) ? xi : ((k > mj && k <= mi) ? carry : o);
-          else val = o;
-          ch.at(T + k) = (uint8_t)(pmut ? val : o);
-          carry = o;
-          o = nx;
+          int src = k;
+          src = (kind == 1 && k >= lo && k <= hi) ? k + d : src;
+          src = (k == mj) ? mi : src;
+          src = (kind == 0 && k == mi) ? mj : src;
+          src = pmut ? src : k;
+          ch.q(k) = gb.q(src);
         }
       }
       if (elite) msv = rec_ms[slot];
       if (child) msv = decode_sorted<NN, GP, 0>(tab, S, pb.stride, ch, T, pb);
     }
     if (live) {
-      store_ilv(pop + slot * GS, ch.base, row, GS);
+      store_row(pop + slot * GS, ch.base, GS);
       ms_out[slot] = msv;
     }
     const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
