@@ -195,7 +195,7 @@ def _traffic(workload: str):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="saturn", choices=["saturn", "reference"])
     ap.add_argument("--workload", default="TXT", choices=sorted(WORKLOADS))

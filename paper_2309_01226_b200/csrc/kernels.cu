@@ -376,7 +376,7 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
 
 template <int STATE>
 struct GaMinBlocks {
-  static constexpr int value = STATE <= 8 ? 6 : (STATE <= 32 ? 4 : 2);
+  static constexpr int value = STATE <= 8 ? 8 : (STATE <= 32 ? 4 : 2);
 };
 
 // Child construction follows oracle/ga.py (GA v3): every Philox
