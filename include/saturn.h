@@ -99,8 +99,10 @@ typedef struct {
 } saturn_search_params;
 
 /* Create a handle for a cluster of n_nodes nodes with node_gpus[n] GPUs each (Table 1: N,
- * GPU_n) on CUDA device `cuda_device`.
- * EINVAL: n_nodes < 1, any GPU_n < 1, sum GPU_n > 32.  ECUDA: device not usable. */
+ * GPU_n) on CUDA device `cuda_device`.  cuda_device = -1 creates a
+ * HOST-ONLY handle: table loading/compaction, baselines and the other host calls work, every
+ * device call returns ESTATE.  EINVAL: n_nodes < 1, any GPU_n < 1, sum GPU_n > 32.
+ * ECUDA: device not usable. */
 saturn_status saturn_plan_create(const int32_t *node_gpus, int32_t n_nodes, int32_t cuda_device,
                                  saturn_plan **out);
 
@@ -183,6 +185,16 @@ saturn_status saturn_search_population(const saturn_plan *p, uint8_t *h_cfg, uin
 /* The best plan of the last enumerate/search (row a8): placements host [T] (job-id order),
  * genome_out host [2T] (cfg then perm) or NULL, makespan.  ESTATE before any search. */
 saturn_status saturn_best_plan(saturn_plan *p, saturn_placement *out, uint8_t *genome_out, int64_t *makespan);
+
+/* The paper's baseline heuristics (row f2; Alg. 1 at 949-962) as genomes
+ * for the decoder, and as GA seeds: MAX = every job on a full node, MIN = one GPU each plus
+ * the surplus dealt round-robin, OPTIMUS = Optimus*-Greedy (Alg. 1, per node), RANDOM = a
+ * uniform random genome.  Configs: best runtime at the chosen width (ties to the lower UPP
+ * index); order: LPT.  Multi-node job groups are drawn with probability GPU_n / sum GPU
+ * (PAPER.md:1002).  Exact rules: DESIGN.md "Baselines" / oracle/baselines.py.
+ * cfg, perm: host uint8 [T].  Host-only (works on host-only handles).  ESTATE without a table. */
+enum { SATURN_BASELINE_MAX = 1, SATURN_BASELINE_MIN = 2, SATURN_BASELINE_OPTIMUS = 3, SATURN_BASELINE_RANDOM = 4 };
+saturn_status saturn_baseline_genome(const saturn_plan *p, int32_t kind, uint64_t seed, uint8_t *cfg, uint8_t *perm);
 
 /* Multi-GPU (row e): rank 0 creates an NCCL unique id (128 bytes), the caller broadcasts it
  * (e.g. torch.distributed), then every rank attaches.  ENCCL if NCCL cannot be loaded. */

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <memory>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -108,6 +109,7 @@ struct saturn_plan {
   DevBuf<uint8_t> pop[2];
   DevBuf<int32_t> pms[2];
   DevBuf<unsigned long long> cand;
+  DevBuf<int> n_cand;
   DevBuf<int32_t> rec_ms, all_ms;
   DevBuf<uint8_t> rec_gen, all_gen, seeds;
   DevBuf<int> sink;
@@ -178,7 +180,16 @@ struct DeviceGuard {
 
 int gs_of(int T) { return sat::record_bytes(T); }  // cfg | pad | perm | pad
 
+bool host_only(saturn_plan* p) {
+  if (p->device < 0) {
+    fail(p, SATURN_ESTATE, "host-only handle (created with cuda_device = -1)");
+    return true;
+  }
+  return false;
+}
+
 saturn_status use_decoder_kind(saturn_plan* p, int* kind) {
+  if (host_only(p)) return SATURN_ESTATE;
   int k = p->decoder;
   if (k == SATURN_DECODER_AUTO) k = p->sorted_ok ? SATURN_DECODER_THREAD : SATURN_DECODER_WARP;
   if (k == SATURN_DECODER_THREAD && !p->sorted_ok)
@@ -202,6 +213,15 @@ saturn_status saturn_plan_create(const int32_t* node_gpus, int32_t n_nodes, int3
     mx = std::max(mx, (int)node_gpus[n]);
   }
   if (sum > sat::MAX_GPUS) return SATURN_EINVAL;
+  if (cuda_device == -1) {  // host-only handle
+    saturn_plan* p = new saturn_plan();
+    p->device = -1;
+    p->gpu_n.assign(node_gpus, node_gpus + n_nodes);
+    p->sumG = sum;
+    p->maxG = mx;
+    *out = p;
+    return SATURN_OK;
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
     cudaGetLastError();
@@ -229,7 +249,6 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   if (n_jobs < 1 || n_jobs > sat::MAX_JOBS) return fail(p, SATURN_EINVAL, "n_jobs=%d not in [1,255]", n_jobs);
   if (n_upps < 1) return fail(p, SATURN_EINVAL, "n_upps=%d < 1", n_upps);
   if (max_gpus < 1) return fail(p, SATURN_EINVAL, "max_gpus=%d < 1", max_gpus);
-  DeviceGuard dg(p->device);
   p->loaded = false;
   p->have_best = false;
   p->have_pop = false;
@@ -261,6 +280,8 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   const int raw = 4 * T * stride + T + T * stride;
   const int bytes = (raw + 15) & ~15;
   if (bytes > 48 * 1024) return fail(p, SATURN_ELIMIT, "packed table %d B > 48 KB", bytes);
+  std::unique_ptr<DeviceGuard> dg;
+  if (p->device >= 0) dg.reset(new DeviceGuard(p->device));
 
   std::vector<uint8_t> blob(bytes, 0);
   uint32_t* tab = reinterpret_cast<uint32_t*>(blob.data());
@@ -281,9 +302,11 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
       p->cfg_u[t * stride + s] = us[t][s];
     }
   }
-  CU(p, p->blob.ensure(bytes));
-  CU(p, cudaMemcpy(p->blob.p, blob.data(), bytes, cudaMemcpyHostToDevice));
-  p->stats.h2d_bytes += bytes;
+  if (p->device >= 0) {
+    CU(p, p->blob.ensure(bytes));
+    CU(p, cudaMemcpy(p->blob.p, blob.data(), bytes, cudaMemcpyHostToDevice));
+    p->stats.h2d_bytes += bytes;
+  }
   p->T = T;
   p->stride = stride;
   p->blob_bytes = bytes;
@@ -381,6 +404,7 @@ saturn_status saturn_evaluate_host(saturn_plan* p, const uint8_t* h_cfg, const u
 
 saturn_status saturn_trace(saturn_plan* p, const uint8_t* d_cfg, const uint8_t* d_perm, int64_t n,
                            saturn_placement* d_placements, int32_t* d_makespan, void* stream) {
+  if (p && host_only(p)) return SATURN_ESTATE;
   if (!p) return SATURN_EINVAL;
   if (!p->loaded) return fail(p, SATURN_ESTATE, "trace before load_runtime_table");
   if (n < 0) return fail(p, SATURN_EINVAL, "n < 0");
@@ -518,6 +542,7 @@ saturn_status saturn_enumerate_range(saturn_plan* p, uint64_t begin, uint64_t en
 }
 
 saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out) {
+  if (p && host_only(p)) return SATURN_ESTATE;
   if (!p) return SATURN_EINVAL;
   if (!p->loaded) return fail(p, SATURN_ESTATE, "search before load_runtime_table");
   if (!sp) return fail(p, SATURN_EINVAL, "params is NULL");
@@ -548,7 +573,9 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     CU(p, p->pop[b].ensure((size_t)P * GS));
     CU(p, p->pms[b].ensure((size_t)P));
   }
-  CU(p, p->cand.ensure((size_t)p->sms * 64 * 4 * 32 + 1024));
+  CU(p, p->cand.ensure((size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64));
+  CU(p, p->n_cand.ensure(1));
+  CU(p, cudaMemsetAsync(p->n_cand.p, 0, sizeof(int), st));
   CU(p, p->rec_ms.ensure(E));
   CU(p, p->rec_gen.ensure((size_t)E * GS));
   CU(p, p->all_ms.ensure((size_t)E * p->world));
@@ -574,12 +601,10 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   gp.px = sp->p_xover_q32;
   gp.pc = sp->p_cfg_mut_q32;
   gp.pm = sp->p_perm_mut_q32;
-  int n_cand = 0;
   uint64_t evaluated = (uint64_t)P;
   CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p, p->pms[0].p,
-                            p->cand.p, &n_cand, p->sms, st));
-  if ((size_t)n_cand > p->cand.n) return fail(p, SATURN_ELIMIT, "candidate buffer too small");
-  CU(p, sat::launch_select(p->cand.p, n_cand, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
+                            p->cand.p, p->n_cand.p, p->sms, st));
+  CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
   p->stats.kernel_launches += 2;
   // profiling: event pairs around the GA generation kernels (first 512 per search)
   const int64_t n_prof = p->profiling ? std::min<int64_t>(sp->max_generations, 512) : 0;
@@ -619,9 +644,9 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     const bool timed = gen <= n_prof;
     if (timed) CU(p, cudaEventRecord(p->ev_pool[2 * (gen - 1)], st));
     CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
-                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, &n_cand, p->sms, st));
+                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st));
     if (timed) CU(p, cudaEventRecord(p->ev_pool[2 * (gen - 1) + 1], st));
-    CU(p, sat::launch_select(p->cand.p, n_cand, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st));
+    CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st));
     p->stats.kernel_launches += 2;
     evaluated += (uint64_t)(P - E);
     cur = nxt;
@@ -701,6 +726,7 @@ saturn_status saturn_search_population(const saturn_plan* p, uint8_t* h_cfg, uin
 }
 
 saturn_status saturn_best_plan(saturn_plan* p, saturn_placement* out, uint8_t* genome_out, int64_t* makespan) {
+  if (p && host_only(p)) return SATURN_ESTATE;
   if (!p) return SATURN_EINVAL;
   if (!p->have_best) return fail(p, SATURN_ESTATE, "best_plan before enumerate/search");
   DeviceGuard dg(p->device);
@@ -730,6 +756,160 @@ saturn_status saturn_best_plan(saturn_plan* p, saturn_placement* out, uint8_t* g
   return SATURN_OK;
 }
 
+namespace {
+
+// ------------------------------------------------------------------ f2: baseline genomes (host)
+void philox_host(uint32_t k0, uint32_t k1, const uint32_t c[4], uint32_t out[4]) {
+  uint32_t x0 = c[0], x1 = c[1], x2 = c[2], x3 = c[3];
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * x0, p1 = (uint64_t)0xCD9E8D57u * x2;
+    const uint32_t y0 = (uint32_t)(p1 >> 32) ^ x1 ^ k0, y2 = (uint32_t)(p0 >> 32) ^ x3 ^ k1;
+    x0 = y0; x1 = (uint32_t)p1; x2 = y2; x3 = (uint32_t)p0;
+  }
+  out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+// word k of the stream (c0, c1, c2) under key seed
+uint32_t stream_word(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t k) {
+  const uint32_t c[4] = {c0, c1, c2, k >> 2};
+  uint32_t o[4];
+  philox_host((uint32_t)seed, (uint32_t)(seed >> 32), c, o);
+  return o[k & 3];
+}
+uint32_t ubelow_host(uint32_t u, uint32_t n) { return (uint32_t)(((uint64_t)u * n) >> 32); }
+
+// best config of job t at g GPUs: least runtime, ties to the lower UPP (= lower index); -1 if none
+int best_cfg(const saturn_plan* p, int t, int g) {
+  int best = -1;
+  for (int s = 0; s < p->S[t]; ++s) {
+    const int k = t * p->stride + s;
+    if (p->cfg_g[k] != g) continue;
+    if (best < 0) { best = s; continue; }
+    const int kb = t * p->stride + best;
+    if (p->cfg_r[k] < p->cfg_r[kb] || (p->cfg_r[k] == p->cfg_r[kb] && p->cfg_u[k] < p->cfg_u[kb])) best = s;
+  }
+  return best;
+}
+// widest width <= limit that has a config (else the narrowest width of the job)
+int widest_upto(const saturn_plan* p, int t, int limit) {
+  int w = -1, narrow = 1 << 30;
+  for (int s = 0; s < p->S[t]; ++s) {
+    const int g = p->cfg_g[t * p->stride + s];
+    if (g <= limit && g > w) w = g;
+    narrow = std::min(narrow, g);
+  }
+  return w > 0 ? w : narrow;
+}
+std::vector<int> distribute_jobs(const saturn_plan* p, uint64_t seed) {
+  const int N = (int)p->gpu_n.size();
+  std::vector<int> node(p->T, 0);
+  if (N == 1) return node;
+  for (int t = 0; t < p->T; ++t) {
+    const uint32_t u = ubelow_host(stream_word(seed, (uint32_t)t, 0u, 3u << 16, 0), (uint32_t)p->sumG);
+    int acc = 0;
+    for (int n = 0; n < N; ++n) {
+      acc += p->gpu_n[n];
+      if ((int)u < acc) { node[t] = n; break; }
+    }
+  }
+  return node;
+}
+void lpt_genome(const saturn_plan* p, const std::vector<int>& cfg, uint8_t* out_cfg, uint8_t* out_perm) {
+  std::vector<int> order(p->T);
+  for (int t = 0; t < p->T; ++t) { order[t] = t; out_cfg[t] = (uint8_t)cfg[t]; }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return p->cfg_r[a * p->stride + cfg[a]] > p->cfg_r[b * p->stride + cfg[b]];
+  });
+  for (int i = 0; i < p->T; ++i) out_perm[i] = (uint8_t)order[i];
+}
+
+}  // namespace
+
+saturn_status saturn_baseline_genome(const saturn_plan* cp, int32_t kind, uint64_t seed, uint8_t* cfg, uint8_t* perm) {
+  saturn_plan* p = const_cast<saturn_plan*>(cp);
+  if (!p || !cfg || !perm) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "baseline before load_runtime_table");
+  const int T = p->T, N = (int)p->gpu_n.size();
+  std::vector<int> chosen(T, 0);
+  if (kind == SATURN_BASELINE_RANDOM) {  // = the GA's initial genome of slot 0
+    uint32_t k = 0;
+    for (int t = 0; t < T; ++t) cfg[t] = (uint8_t)ubelow_host(stream_word(seed, 0, 0, 1, k++), (uint32_t)p->S[t]);
+    for (int t = 0; t < T; ++t) perm[t] = (uint8_t)t;
+    for (int i = T - 1; i > 0; --i) {
+      const int j = (int)ubelow_host(stream_word(seed, 0, 0, 1, k++), (uint32_t)(i + 1));
+      std::swap(perm[i], perm[j]);
+    }
+    return SATURN_OK;
+  }
+  const std::vector<int> node = distribute_jobs(p, seed);
+  if (kind == SATURN_BASELINE_MAX) {
+    for (int t = 0; t < T; ++t) chosen[t] = best_cfg(p, t, widest_upto(p, t, p->gpu_n[node[t]]));
+  } else if (kind == SATURN_BASELINE_MIN) {
+    std::vector<int> share(T, 1);
+    for (int n = 0; n < N; ++n) {
+      std::vector<int> jobs;
+      for (int t = 0; t < T; ++t)
+        if (node[t] == n) jobs.push_back(t);
+      if (jobs.empty()) continue;
+      std::vector<int> cap;
+      for (int t : jobs) {
+        int c = 0;
+        for (int s = 0; s < p->S[t]; ++s) {
+          const int g = p->cfg_g[t * p->stride + s];
+          if (g <= p->gpu_n[n]) c = std::max(c, g);
+        }
+        cap.push_back(c > 0 ? c : 1);
+      }
+      int surplus = p->gpu_n[n] - (int)jobs.size();
+      while (surplus > 0) {
+        bool progressed = false;
+        for (size_t i = 0; i < jobs.size(); ++i)
+          if (surplus > 0 && share[jobs[i]] < cap[i]) { ++share[jobs[i]]; --surplus; progressed = true; }
+        if (!progressed) break;
+      }
+    }
+    for (int t = 0; t < T; ++t) chosen[t] = best_cfg(p, t, widest_upto(p, t, share[t]));
+  } else if (kind == SATURN_BASELINE_OPTIMUS) {  // Alg. 1, one node at a time
+    std::vector<int> alloc(T, 1);
+    for (int n = 0; n < N; ++n) {
+      std::vector<int> jobs;
+      for (int t = 0; t < T; ++t)
+        if (node[t] == n) jobs.push_back(t);
+      if (jobs.empty()) continue;
+      auto Rbest = [&](int t, int g) -> int64_t {  // -1: no config at g GPUs on this node
+        if (g > p->gpu_n[n]) return -1;
+        const int s = best_cfg(p, t, g);
+        return s < 0 ? -1 : p->cfg_r[t * p->stride + s];
+      };
+      std::vector<int> L(jobs.size(), 1);
+      int sum = (int)jobs.size();
+      while (sum < p->gpu_n[n]) {
+        int arg = -1;
+        int64_t best = 0;
+        for (size_t i = 0; i < jobs.size(); ++i) {
+          const int64_t cur = Rbest(jobs[i], L[i]), nxt = Rbest(jobs[i], L[i] + 1);
+          if (cur < 0 || nxt < 0) continue;  // gain -inf
+          const int64_t gain = cur - nxt;
+          if (arg < 0 || gain > best) { arg = (int)i; best = gain; }
+        }
+        if (arg < 0) break;
+        ++L[arg];
+        ++sum;
+      }
+      for (size_t i = 0; i < jobs.size(); ++i) alloc[jobs[i]] = L[i];
+    }
+    for (int t = 0; t < T; ++t) {
+      int s = best_cfg(p, t, alloc[t]);
+      if (s < 0) s = best_cfg(p, t, widest_upto(p, t, alloc[t]));
+      chosen[t] = s;
+    }
+  } else {
+    return fail(p, SATURN_EINVAL, "unknown baseline kind %d", kind);
+  }
+  lpt_genome(p, chosen, cfg, perm);
+  return SATURN_OK;
+}
+
 saturn_status saturn_get_unique_id(uint8_t* id128) {
   if (!id128) return SATURN_EINVAL;
   if (!nccl().ok) return SATURN_ENCCL;
@@ -741,6 +921,7 @@ saturn_status saturn_get_unique_id(uint8_t* id128) {
 }
 
 saturn_status saturn_plan_attach_comm(saturn_plan* p, const uint8_t* id128, int32_t rank, int32_t world) {
+  if (p && host_only(p)) return SATURN_ESTATE;
   if (!p) return SATURN_EINVAL;
   if (!id128 || world < 1 || rank < 0 || rank >= world) return fail(p, SATURN_EINVAL, "bad rank/world");
   if (!nccl().ok) return fail(p, SATURN_ENCCL, "%s", nccl().why.c_str());
@@ -766,6 +947,7 @@ saturn_status saturn_partition(uint64_t total, int32_t rank, int32_t world, uint
 }
 
 saturn_status saturn_probe_int_peak(saturn_plan* p, double* int_ops_per_s) {
+  if (p && host_only(p)) return SATURN_ESTATE;
   if (!p || !int_ops_per_s) return SATURN_EINVAL;
   DeviceGuard dg(p->device);
   CU(p, p->sink.ensure(p->sms * 8));
@@ -813,6 +995,10 @@ const char* saturn_last_error(const saturn_plan* p) { return p ? p->err.c_str() 
 
 void saturn_plan_destroy(saturn_plan* p) {
   if (!p) return;
+  if (p->device < 0) {
+    delete p;
+    return;
+  }
   {
     DeviceGuard dg(p->device);
     if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
@@ -827,6 +1013,7 @@ void saturn_plan_destroy(saturn_plan* p) {
       p->pms[b].release();
     }
     p->cand.release();
+    p->n_cand.release();
     p->rec_ms.release();
     p->all_ms.release();
     p->rec_gen.release();

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
     k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
          const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
          const int32_t* __restrict__ rec_ms, const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
-         int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand) {
+         int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand, int* __restrict__ n_cand) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int T = pb.T;
   const int GS = gp.GS;
@@ -414,6 +414,19 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
   // only those are offered to the list.
   const uint64_t cap = (gp.gen == 0) ? ~0ull : (((uint64_t)(uint32_t)rec_ms[gp.E - 1] << 32) | (uint64_t)(gp.E - 1));
   const int64_t nthr = (int64_t)gridDim.x * GA_B;
+  // Tournament prefetch: the candidates' makespans of the NEXT child of this thread are
+  // loaded one iteration ahead, so their latency hides behind the current decode.
+  uint32_t t_i1 = 0, t_j1 = 0, t_i2 = 0, t_j2 = 0, t_m1 = 0, t_n1 = 0, t_m2 = 0, t_n2 = 0;
+  auto prefetch = [&](int64_t nslot) {
+    if (gp.gen != 0 && nslot >= gp.E && nslot < gp.P) {
+      const uint4 w0 = philox_block((uint32_t)gp.seed, (uint32_t)(gp.seed >> 32), (uint32_t)nslot, gp.gen,
+                                    gp.rank << 16, 0u);
+      t_i1 = ubelow(w0.x, P); t_j1 = ubelow(w0.y, P); t_i2 = ubelow(w0.z, P); t_j2 = ubelow(w0.w, P);
+      t_m1 = (uint32_t)prev_ms[t_i1]; t_n1 = (uint32_t)prev_ms[t_j1];
+      t_m2 = (uint32_t)prev_ms[t_i2]; t_n2 = (uint32_t)prev_ms[t_j2];
+    }
+  };
+  prefetch((int64_t)blockIdx.x * GA_B + (tid & ~31) + lane);
   for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P; base += nthr) {
     const int64_t slot = base + lane;
     const bool live = slot < gp.P;
@@ -440,17 +453,15 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
       const bool elite = live && slot < gp.E;
       const bool child = live && slot >= gp.E;
       PhiloxWords rw(gp.seed, (uint32_t)slot, gp.gen, gp.rank << 16);
-      const uint4 w0 = rw.block(0), w1 = rw.block(1), w2 = rw.block(2);
+      uint32_t A = 0, B = 0;
+      if (child) {  // 1. tournaments (words 0..3, makespans prefetched)
+        A = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
+        B = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
+      }
+      prefetch(slot + nthr);
+      const uint4 w1 = rw.block(1), w2 = rw.block(2);
       rw.blk = 2;
       rw.cur = w2;
-      uint32_t A = 0, B = 0;
-      if (child) {  // 1. tournaments
-        const uint32_t i1 = ubelow(w0.x, P), j1 = ubelow(w0.y, P), i2 = ubelow(w0.z, P), j2 = ubelow(w0.w, P);
-        const uint32_t m1 = (uint32_t)prev_ms[i1], n1 = (uint32_t)prev_ms[j1];
-        const uint32_t m2 = (uint32_t)prev_ms[i2], n2 = (uint32_t)prev_ms[j2];
-        A = ((((uint64_t)m1 << 32) | i1) < (((uint64_t)n1 << 32) | j1)) ? i1 : j1;
-        B = ((((uint64_t)m2 << 32) | i2) < (((uint64_t)n2 << 32) | j2)) ? i2 : j2;
-      }
       // 2. child = A (elites: the elite record)
       if (elite) load_row(ch.base, rec_gen + slot * GS, GS);
       if (child) {
@@ -549,22 +560,27 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
   if (tid < 32) {
     uint64_t m = ~0ull;
     for (int w = 0; w < GA_B / 32; ++w) topE_insert(m, s_lists[w * 32 + lane], gp.E);
-    if (lane < gp.E) cand[(int64_t)blockIdx.x * gp.E + lane] = m;
+    // append only the real keys (after the first generation most blocks have none)
+    const bool real = lane < gp.E && m != ~0ull;
+    const uint32_t mask = __ballot_sync(0xffffffffu, real);
+    int off = 0;
+    if (lane == 0 && mask) off = atomicAdd(n_cand, __popc(mask));
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (real) cand[off + __popc(mask & ((1u << lane) - 1u))] = m;
   }
 }
 
 static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
                              int64_t n_seed, const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
                              const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand,
-                             int* n_cand, int sms, cudaStream_t st) {
+                             int* d_n_cand, int sms, cudaStream_t st) {
   const size_t smem = ga_smem_bytes(pb, gp.GS);
   const int64_t blocks = (gp.P + GA_B - 1) / GA_B;
 #define SAT_GA(a, b)                                                                                        \
   if (NN == a && GP == b) {                                                                                 \
     const int g = grid_for(k_ga<a, b>, GA_B, smem, sms, blocks);                                            \
-    *n_cand = g * gp.E;                                                                                     \
     k_ga<a, b><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,   \
-                                      cand);                                                                \
+                                      cand, d_n_cand);                                                      \
     return cudaGetLastError();                                                                              \
   }
   SAT_SHAPES(SAT_GA)
@@ -572,27 +588,46 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
   return cudaErrorInvalidConfiguration;
 }
 
+int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms) {
+  const size_t smem = ga_smem_bytes(pb, GS);
+  const int64_t blocks = (P + GA_B - 1) / GA_B;
+#define SAT_GAC(a, b) \
+  if (NN == a && GP == b) return grid_for(k_ga<a, b>, GA_B, smem, sms, blocks) * E;
+  SAT_SHAPES(SAT_GAC)
+#undef SAT_GAC
+  return 0;
+}
+
 cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
-                           int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* n_cand, int sms,
+                           int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms,
                            cudaStream_t st) {
-  return launch_ga(pb, NN, GP, gp, seeds, n_seed, nullptr, nullptr, nullptr, nullptr, pop, ms, cand, n_cand, sms, st);
+  return launch_ga(pb, NN, GP, gp, seeds, n_seed, nullptr, nullptr, nullptr, nullptr, pop, ms, cand, d_n_cand, sms,
+                   st);
 }
 cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
                                  const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen, uint8_t* pop,
-                                 int32_t* ms, unsigned long long* cand, int* n_cand, int sms, cudaStream_t st) {
-  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, n_cand, sms, st);
+                                 int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms, cudaStream_t st) {
+  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, st);
 }
 
 // ------------------------------------------------------------------ K4: select / merge
-__global__ void __launch_bounds__(1024) k_select(const unsigned long long* __restrict__ cand, int n, int E, int GS,
-                                                 const uint8_t* __restrict__ pop, int32_t* __restrict__ rec_ms,
-                                                 uint8_t* __restrict__ rec_gen) {
+__global__ void __launch_bounds__(1024) k_select(const unsigned long long* __restrict__ cand, int* __restrict__ n_cand,
+                                                 int E, int GS, const uint8_t* __restrict__ pop,
+                                                 int32_t* __restrict__ rec_ms, uint8_t* __restrict__ rec_gen) {
   __shared__ uint64_t s_l[32][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = *n_cand;
   uint64_t lst = ~0ull;
-  for (int base = warp * 32; base < n; base += 1024) {
-    const uint64_t key = (base + lane < n) ? cand[base + lane] : ~0ull;
-    topE_insert(lst, key, E);
+  constexpr int U = 8;  // independent loads in flight per thread
+  for (int base = warp * 32; base < n; base += 1024 * U) {
+    uint64_t k[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = base + j * 1024 + lane;
+      k[j] = (i < n) ? cand[i] : ~0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) topE_insert(lst, k[j], E);
   }
   s_l[warp][lane] = lst;
   __syncthreads();
@@ -604,12 +639,13 @@ __global__ void __launch_bounds__(1024) k_select(const unsigned long long* __res
       rec_ms[lane] = (int32_t)(lst >> 32);
       const uint4* src = reinterpret_cast<const uint4*>(pop + (uint64_t)slot * GS);
       uint4* dst = reinterpret_cast<uint4*>(rec_gen + (uint64_t)lane * GS);
-      for (int k = 0; k < GS / 16; ++k) dst[k] = src[k];
+      for (int k2 = 0; k2 < GS / 16; ++k2) dst[k2] = src[k2];
     }
+    if (lane == 0) *n_cand = 0;  // ready for the next generation
   }
 }
 
-cudaError_t launch_select(const unsigned long long* cand, int n_cand, int E, int GS, const uint8_t* pop,
+cudaError_t launch_select(const unsigned long long* cand, int* n_cand, int E, int GS, const uint8_t* pop,
                           int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st) {
   k_select<<<1, 1024, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);
   return cudaGetLastError();

@@ -43,17 +43,21 @@ struct GaParams {
   uint32_t px, pc, pm;
 };
 
-// Generation 0: seed genomes then Philox-initialised genomes, all decoded.
+// Generation 0: seed genomes then Philox-initialised genomes, all decoded.  Each CTA appends
+// its top-E keys (ms << 32 | slot) that can still enter the elite set to cand[] and bumps the
+// device counter *d_n_cand (zero on entry; k_select resets it).
 cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
-                           int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* n_cand,
+                           int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand,
                            int sms, cudaStream_t st);
 // Generation gen >= 1 from the previous population and the elite records.
 cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
                                  const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen,
-                                 uint8_t* pop, int32_t* ms, unsigned long long* cand, int* n_cand, int sms,
+                                 uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms,
                                  cudaStream_t st);
-// Top-E of the candidate keys -> elite records (ms, genome) copied from `pop`.
-cudaError_t launch_select(const unsigned long long* cand, int n_cand, int E, int GS, const uint8_t* pop,
+// Upper bound of the candidates one GA launch can append (grid x E).
+int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms);
+// Top-E of the *d_n_cand candidate keys -> elite records (ms, genome) copied from `pop`.
+cudaError_t launch_select(const unsigned long long* cand, int* d_n_cand, int E, int GS, const uint8_t* pop,
                           int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st);
 // Island migration: the E best of W ranks' gathered records by (ms, rank, position).
 cudaError_t launch_merge_elites(const int32_t* all_ms, const uint8_t* all_gen, int W, int E, int GS,

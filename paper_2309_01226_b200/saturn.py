@@ -29,8 +29,9 @@ EXPORTS = (
     "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
-    "saturn_reset_stats", "saturn_last_error", "saturn_plan_destroy",
+    "saturn_reset_stats", "saturn_baseline_genome", "saturn_last_error", "saturn_plan_destroy",
 )
+BASELINES = {"max": 1, "min": 2, "optimus": 3, "random": 4}
 
 
 class SaturnError(RuntimeError):
@@ -112,6 +113,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_set_profiling": [h, i32],
         "saturn_get_stats": [h, P(Stats)],
         "saturn_reset_stats": [h],
+        "saturn_baseline_genome": [h, i32, u64, P(u8), P(u8)],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
@@ -178,7 +180,7 @@ class SearchConfig:
     elites: int = 16
     generations_per_epoch: int = 8
     p_xover: float = 0.9
-    p_cfg_mut: float | None = None   # default 1/T
+    p_cfg_mut: float | None = 0.5    # per-child probability of re-drawing one job's config
     p_perm_mut: float = 0.5
 
 
@@ -202,6 +204,11 @@ class Plan:
         self.n_jobs = 0
 
     # -- plumbing
+    def _stream(self, stream):
+        if stream is None and self.device < 0:   # host-only handle: no CUDA stream
+            return ctypes.c_void_p(0)
+        return _stream_ptr(stream)
+
     def _check(self, st, what):
         if st != OK:
             raise SaturnError(st, f"{what}: {self._lib.saturn_last_error(self._h).decode()}")
@@ -265,7 +272,7 @@ class Plan:
             out = torch.empty(n, dtype=torch.int32, device=cfg.device)
         self._check(self._lib.saturn_evaluate(self._h, _dev_ptr(cfg, "uint8", (n, self.n_jobs)),
                                               _dev_ptr(perm, "uint8", (n, self.n_jobs)), n,
-                                              _dev_ptr(out, "int32", (n,)), _stream_ptr(stream)),
+                                              _dev_ptr(out, "int32", (n,)), self._stream(stream)),
                     "saturn_evaluate")
         return out
 
@@ -275,7 +282,7 @@ class Plan:
         n = cfg.shape[0]
         out = np.empty(n, np.int32)
         self._check(self._lib.saturn_evaluate_host(self._h, _np_ptr(cfg, ctypes.c_uint8), _np_ptr(perm, ctypes.c_uint8),
-                                                   n, _np_ptr(out, ctypes.c_int32), _stream_ptr(stream)),
+                                                   n, _np_ptr(out, ctypes.c_int32), self._stream(stream)),
                     "saturn_evaluate_host")
         return out
 
@@ -287,19 +294,19 @@ class Plan:
         pl = torch.zeros((n, T, 32), dtype=torch.uint8, device=cfg.device)
         ms = torch.empty(n, dtype=torch.int32, device=cfg.device)
         self._check(self._lib.saturn_trace(self._h, _dev_ptr(cfg, "uint8", (n, T)), _dev_ptr(perm, "uint8", (n, T)), n,
-                                           _dev_ptr(pl, "uint8"), _dev_ptr(ms, "int32"), _stream_ptr(stream)),
+                                           _dev_ptr(pl, "uint8"), _dev_ptr(ms, "int32"), self._stream(stream)),
                     "saturn_trace")
         return pl, ms
 
     def enumerate(self, max_genomes: int = 1 << 34, stream=None) -> dict:
         r = Result()
-        self._check(self._lib.saturn_enumerate(self._h, int(max_genomes), _stream_ptr(stream), ctypes.byref(r)),
+        self._check(self._lib.saturn_enumerate(self._h, int(max_genomes), self._stream(stream), ctypes.byref(r)),
                     "saturn_enumerate")
         return r.as_dict()
 
     def enumerate_range(self, begin: int, end: int, stream=None) -> dict:
         r = Result()
-        self._check(self._lib.saturn_enumerate_range(self._h, int(begin), int(end), _stream_ptr(stream),
+        self._check(self._lib.saturn_enumerate_range(self._h, int(begin), int(end), self._stream(stream),
                                                      ctypes.byref(r)), "saturn_enumerate_range")
         return r.as_dict()
 
@@ -320,7 +327,7 @@ class Plan:
             sp.seed_perm = _np_ptr(sq, ctypes.c_uint8)
             sp.n_seed = sc.shape[0]
         r = Result()
-        self._check(self._lib.saturn_search(self._h, ctypes.byref(sp), _stream_ptr(stream), ctypes.byref(r)),
+        self._check(self._lib.saturn_search(self._h, ctypes.byref(sp), self._stream(stream), ctypes.byref(r)),
                     "saturn_search")
         del keep
         return r.as_dict()
@@ -358,6 +365,15 @@ class Plan:
     def attach_comm(self, uid: bytes, rank: int, world: int):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         self._check(self._lib.saturn_plan_attach_comm(self._h, buf, rank, world), "saturn_plan_attach_comm")
+
+    def baseline_genome(self, kind: str, seed: int = 0):
+        """The paper's baselines as genomes (row f2): kind in max | min | optimus | random."""
+        T = self.n_jobs
+        c = np.zeros(T, np.uint8)
+        q = np.zeros(T, np.uint8)
+        self._check(self._lib.saturn_baseline_genome(self._h, BASELINES[kind], int(seed), _np_ptr(c, ctypes.c_uint8),
+                                                     _np_ptr(q, ctypes.c_uint8)), "saturn_baseline_genome")
+        return c, q
 
     def set_profiling(self, on: bool = True):
         self._check(self._lib.saturn_set_profiling(self._h, int(bool(on))), "saturn_set_profiling")

@@ -284,3 +284,23 @@ def test_int_probe_runs(sat, torch):
     plan = _plan(sat, synth.txt(0))
     v = plan.probe_int_peak()
     assert 1e12 < v < 1e14
+
+
+def test_nccl_single_rank_communicator_path(sat, torch):
+    """The multi-GPU code path (NCCL MIN all-reduce for enumeration, elite all-gather +
+    device merge for search) run with a 1-rank communicator on the one GPU: identical
+    results to the communicator-free path."""
+    inst = synth.tiny_variant(45, 5, (2, 2))
+    a = _plan(sat, inst)
+    b = _plan(sat, inst)
+    b.attach_comm(sat.get_unique_id(), 0, 1)
+    ra, rb = a.enumerate(), b.enumerate()
+    assert (ra["makespan"], ra["genome_index"]) == (rb["makespan"], rb["genome_index"])
+    txt = synth.txt(0)
+    a, b = _plan(sat, txt), _plan(sat, txt)
+    b.attach_comm(sat.get_unique_id(), 0, 1)
+    cfgs = sat.SearchConfig(seed=5, population=4096, max_generations=12, elites=8, generations_per_epoch=3)
+    sa, sb = a.search(cfgs), b.search(cfgs)
+    assert sa["makespan"] == sb["makespan"]
+    assert (a.best_plan()[2] == b.best_plan()[2]).all()
+    assert (a.search_population(4096)[0] == b.search_population(4096)[0]).all()
