@@ -196,6 +196,33 @@ saturn_status saturn_best_plan(saturn_plan *p, saturn_placement *out, uint8_t *g
 enum { SATURN_BASELINE_MAX = 1, SATURN_BASELINE_MIN = 2, SATURN_BASELINE_OPTIMUS = 3, SATURN_BASELINE_RANDOM = 4 };
 saturn_status saturn_baseline_genome(const saturn_plan *p, int32_t kind, uint64_t seed, uint8_t *cfg, uint8_t *perm);
 
+/* Round introspection (row f1; PAPER.md:241-262 App. algorithm, §4.4) on
+ * the loaded workload W:  S = solve(W), M = makespan(S), time = 0; while M > I: W = W after I
+ * seconds of S (residual runtimes, reading A10: a job that ran a s of its config with runtime
+ * R0 keeps every config with R' = ceil(R (R0 - a) / R0); finished jobs leave), S = S[I:],
+ * M -= I, time += I, P = solve(W), adopt P iff makespan(P) <= M - T.  E2E makespan =
+ * time + M at the end.  solve = saturn_search (SATURN_SOLVER_SEARCH, with `search`) or
+ * saturn_enumerate (SATURN_SOLVER_ENUMERATE, exact; tiny workloads).  The loaded table is
+ * restored afterwards.  round_log (host, may be NULL): per round {time, M after the
+ * shift, makespan(P), adopted} as 4 int64.  Synchronous. */
+enum { SATURN_SOLVER_SEARCH = 0, SATURN_SOLVER_ENUMERATE = 1 };
+typedef struct {
+  int64_t interval_s;                 /* I (the paper uses 1000 s)   */
+  int64_t threshold_s;                /* T (500 s)             */
+  int32_t solver;
+  int32_t max_rounds;
+  const saturn_search_params *search; /* SEARCH: parameters of every round's solve  */
+} saturn_introspect_params;
+typedef struct {
+  int64_t one_shot_makespan;  /* makespan of the round-0 plan                       */
+  int64_t e2e_makespan;       /* time until the workload is exhausted              */
+  int32_t rounds;
+  int32_t adopted;
+  uint64_t evaluated;         /* decodes of all solves                              */
+} saturn_introspect_result;
+saturn_status saturn_introspect(saturn_plan *p, const saturn_introspect_params *ip, void *stream,
+                                saturn_introspect_result *out, int64_t *round_log);
+
 /* Multi-GPU (row e): rank 0 creates an NCCL unique id (128 bytes), the caller broadcasts it
  * (e.g. torch.distributed), then every rank attaches.  ENCCL if NCCL cannot be loaded. */
 saturn_status saturn_get_unique_id(uint8_t *id128);

@@ -95,6 +95,8 @@ struct saturn_plan {
   bool loaded = false;
   int T = 0, stride = 0;
   std::vector<int> S, cfg_g, cfg_r, cfg_u;   // [T], [T*stride] x3
+  std::vector<int32_t> dense;                // the loaded runtime table [T][U][Gmax]
+  int U = 0, Gmax = 0;
   int NN = 0, GP = 0;
   bool sorted_ok = false;
   int decoder = SATURN_DECODER_AUTO;
@@ -310,6 +312,9 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   p->T = T;
   p->stride = stride;
   p->blob_bytes = bytes;
+  p->dense.assign(runtime_s, runtime_s + (size_t)T * n_upps * max_gpus);
+  p->U = n_upps;
+  p->Gmax = max_gpus;
   Problem pb{};
   pb.blob = p->blob.p;
   pb.blob_bytes = bytes;
@@ -907,6 +912,101 @@ saturn_status saturn_baseline_genome(const saturn_plan* cp, int32_t kind, uint64
     return fail(p, SATURN_EINVAL, "unknown baseline kind %d", kind);
   }
   lpt_genome(p, chosen, cfg, perm);
+  return SATURN_OK;
+}
+
+saturn_status saturn_introspect(saturn_plan* p, const saturn_introspect_params* ip, void* stream,
+                                saturn_introspect_result* out, int64_t* round_log) {
+  if (!p) return SATURN_EINVAL;
+  if (host_only(p)) return SATURN_ESTATE;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "introspect before load_runtime_table");
+  if (!ip || ip->interval_s < 1 || ip->threshold_s < 0 || ip->max_rounds < 0)
+    return fail(p, SATURN_EINVAL, "bad introspection parameters");
+  if (ip->solver == SATURN_SOLVER_SEARCH && !ip->search) return fail(p, SATURN_EINVAL, "search params missing");
+  const std::vector<int32_t> orig = p->dense;
+  const int U = p->U, G = p->Gmax;
+  const int64_t I = ip->interval_s, Tthr = ip->threshold_s;
+  std::vector<int32_t> W = orig;
+  int Tn = p->T;
+  uint64_t evaluated = 0;
+  std::vector<saturn_placement> S;
+  // solve the currently loaded workload -> S (placements, job-id order) and its makespan
+  auto solve = [&](std::vector<saturn_placement>& plan, int64_t& ms) -> saturn_status {
+    saturn_status st;
+    saturn_result r;
+    if (ip->solver == SATURN_SOLVER_ENUMERATE) st = saturn_enumerate(p, uint64_t(1) << 38, stream, &r);
+    else st = saturn_search(p, ip->search, stream, &r);
+    if (st != SATURN_OK) return st;
+    evaluated += r.evaluated;
+    plan.resize(p->T);
+    return saturn_best_plan(p, plan.data(), nullptr, &ms);
+  };
+  auto restore = [&](saturn_status st) {
+    const std::string keep = p->err;
+    saturn_load_runtime_table(p, orig.data(), (int32_t)(orig.size() / ((size_t)U * G)), U, G);
+    if (st != SATURN_OK) p->err = keep;
+    return st;
+  };
+  int64_t M = 0;
+  saturn_status st = solve(S, M);
+  if (st != SATURN_OK) return restore(st);
+  const int64_t one_shot = M;
+  int64_t time = 0;
+  int rounds = 0, adopted = 0;
+  while (M > I && rounds < ip->max_rounds) {
+    // W after I seconds of S; S = S[I:]
+    std::vector<int32_t> W2;
+    std::vector<saturn_placement> S2;
+    for (int t = 0; t < Tn; ++t) {
+      const saturn_placement& pl = S[t];
+      if (pl.end_s <= I) continue;
+      const int32_t* row = &W[(size_t)t * U * G];
+      if (pl.start_s < I) {
+        const int64_t R0 = pl.end_s - pl.start_s, a = I - pl.start_s;
+        for (int k = 0; k < U * G; ++k)
+          W2.push_back(row[k] > 0 ? (int32_t)(((int64_t)row[k] * (R0 - a) + R0 - 1) / R0) : 0);
+      } else {
+        W2.insert(W2.end(), row, row + U * G);
+      }
+      saturn_placement q = pl;
+      q.start_s = (int32_t)std::max<int64_t>(pl.start_s - I, 0);
+      q.end_s = (int32_t)(pl.end_s - I);
+      S2.push_back(q);
+    }
+    W.swap(W2);
+    S.swap(S2);
+    Tn = (int)S.size();
+    M -= I;
+    time += I;
+    ++rounds;
+    st = saturn_load_runtime_table(p, W.data(), Tn, U, G);
+    if (st != SATURN_OK) return restore(st);
+    std::vector<saturn_placement> P;
+    int64_t Mp = 0;
+    st = solve(P, Mp);
+    if (st != SATURN_OK) return restore(st);
+    const bool take = Mp <= M - Tthr;
+    if (round_log) {
+      round_log[4 * (rounds - 1) + 0] = time;
+      round_log[4 * (rounds - 1) + 1] = M;
+      round_log[4 * (rounds - 1) + 2] = Mp;
+      round_log[4 * (rounds - 1) + 3] = take ? 1 : 0;
+    }
+    if (take) {
+      S.swap(P);
+      M = Mp;
+      ++adopted;
+    }
+  }
+  st = restore(SATURN_OK);
+  if (st != SATURN_OK) return st;
+  if (out) {
+    out->one_shot_makespan = one_shot;
+    out->e2e_makespan = time + M;
+    out->rounds = rounds;
+    out->adopted = adopted;
+    out->evaluated = evaluated;
+  }
   return SATURN_OK;
 }
 

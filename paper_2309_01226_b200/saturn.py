@@ -29,7 +29,8 @@ EXPORTS = (
     "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
-    "saturn_reset_stats", "saturn_baseline_genome", "saturn_last_error", "saturn_plan_destroy",
+    "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_last_error",
+    "saturn_plan_destroy",
 )
 BASELINES = {"max": 1, "min": 2, "optimus": 3, "random": 4}
 
@@ -61,6 +62,19 @@ class Result(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("ga_launches", ctypes.c_int64), ("ga_kernel_ms", ctypes.c_double), ("ga_decodes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class IntrospectParams(ctypes.Structure):
+    _fields_ = [("interval_s", ctypes.c_int64), ("threshold_s", ctypes.c_int64), ("solver", ctypes.c_int32),
+                ("max_rounds", ctypes.c_int32), ("search", ctypes.c_void_p)]
+
+
+class IntrospectResult(ctypes.Structure):
+    _fields_ = [("one_shot_makespan", ctypes.c_int64), ("e2e_makespan", ctypes.c_int64), ("rounds", ctypes.c_int32),
+                ("adopted", ctypes.c_int32), ("evaluated", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -114,6 +128,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_get_stats": [h, P(Stats)],
         "saturn_reset_stats": [h],
         "saturn_baseline_genome": [h, i32, u64, P(u8), P(u8)],
+        "saturn_introspect": [h, P(IntrospectParams), vp, P(IntrospectResult), P(i64)],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
@@ -309,6 +324,29 @@ class Plan:
         self._check(self._lib.saturn_enumerate_range(self._h, int(begin), int(end), self._stream(stream),
                                                      ctypes.byref(r)), "saturn_enumerate_range")
         return r.as_dict()
+
+    def _search_params(self, cfg: SearchConfig):
+        T = self.n_jobs
+        p_c = cfg.p_cfg_mut if cfg.p_cfg_mut is not None else 1.0 / max(T, 1)
+        return SearchParams(seed=cfg.seed, population=cfg.population, max_generations=cfg.max_generations,
+                            time_budget_s=cfg.time_budget_s, elites=cfg.elites,
+                            generations_per_epoch=cfg.generations_per_epoch, p_xover_q32=q32(cfg.p_xover),
+                            p_cfg_mut_q32=q32(p_c), p_perm_mut_q32=q32(cfg.p_perm_mut))
+
+    def introspect(self, interval_s: int = 1000, threshold_s: int = 500, solver: str = "search",
+                   search: SearchConfig | None = None, max_rounds: int = 100000, stream=None):
+        """Round introspection (row f1) on the loaded workload; -> (result dict, round log)."""
+        sp = self._search_params(search or SearchConfig())
+        cap = min(int(max_rounds), 1 << 16)
+        ip = IntrospectParams(interval_s=int(interval_s), threshold_s=int(threshold_s),
+                              solver={"search": 0, "enumerate": 1}[solver], max_rounds=cap,
+                              search=ctypes.cast(ctypes.pointer(sp), ctypes.c_void_p))
+        r = IntrospectResult()
+        log = np.zeros((cap, 4), np.int64)
+        self._check(self._lib.saturn_introspect(self._h, ctypes.byref(ip), self._stream(stream), ctypes.byref(r),
+                                                _np_ptr(log, ctypes.c_int64)), "saturn_introspect")
+        d = r.as_dict()
+        return d, [tuple(int(x) for x in row) for row in log[:d["rounds"]]]
 
     def search(self, cfg: SearchConfig | None = None, seed_genomes=None, stream=None) -> dict:
         cfg = cfg or SearchConfig()
