@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -324,10 +325,24 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   pb.sumG = p->sumG;
   for (int n = 0; n < pb.N; ++n) pb.gpu_n[n] = (int8_t)p->gpu_n[n];
   p->pb = pb;
+  // Decoder shape: node vectors in registers when that shape is compiled (faster: measured
+  // r1 on MIX 2x8 and SWEEP 4x8, profiles/r1/README.md), else node vectors in shared
+  // memory with a runtime node count (NN = 0).  SATURN_MULTINODE_SMEM=1 forces the latter.
   p->GP = std::max(2, pow2_at_least(p->maxG));
-  p->NN = pow2_at_least((int)p->gpu_n.size());
+  p->NN = 1;
+  if (p->gpu_n.size() > 1) {
+    const char* env = getenv("SATURN_MULTINODE_SMEM");
+    const int nn = pow2_at_least((int)p->gpu_n.size());
+    if (!(env && env[0] == '1') && sat::have_sorted_shape(nn, p->GP)) {
+      p->NN = nn;
+    } else {
+      p->NN = 0;
+      p->GP = std::max(4, p->GP);
+    }
+  }
   p->sorted_ok = sat::have_sorted_shape(p->NN, p->GP);
-  if (sat::eval_smem_bytes(pb) > 227 * 1024) return fail(p, SATURN_ELIMIT, "evaluate tile exceeds shared memory");
+  if (sat::eval_smem_bytes(pb, p->NN, p->GP) > 227 * 1024)
+    return fail(p, SATURN_ELIMIT, "evaluate tile exceeds shared memory");
   p->loaded = true;
   return SATURN_OK;
 }

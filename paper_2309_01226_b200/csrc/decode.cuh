@@ -39,6 +39,22 @@ __device__ __forceinline__ int mux(const int (&a)[GP], int k) {
   }
 }
 
+// Select on the FMA pipe: p in {0, 1} -> p ? b : a, as a + p * (b - a) with two IMADs.
+// The decode is ALU-pipe bound (SEL / VIMNMX / ISETP all issue there at half rate); moving
+// part of the barrel shift onto the otherwise idle FMA pipe lets both pipes issue.
+__device__ __forceinline__ int sel_fma(int p, int a, int b) {
+  int d, r;
+  asm("mad.lo.s32 %0, %1, -1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(p), "r"(d), "r"(a));
+  return r;
+}
+#ifndef SAT_FMA_SEL_STAGES
+#define SAT_FMA_SEL_STAGES 8   // all barrel-shift stages (measured r1: +5 % TXT, +8 % MIX evaluate)
+#endif
+#ifndef SAT_FMA_MULTI
+#define SAT_FMA_MULTI 0        // multi-node gather / scatter on the FMA pipe too
+#endif
+
 // In-place update of one node's sorted free-time vector after placing (g, R) at its
 // g-th smallest free time.  Returns s + R.
 template <int GP>
@@ -47,11 +63,18 @@ __device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R) {
   int b[GP];
 #pragma unroll
   for (int i = 0; i < GP; ++i) b[i] = x[i];
+  int stage = 0;
 #pragma unroll
-  for (int sh = 1; sh < GP; sh <<= 1) {
+  for (int sh = 1; sh < GP; sh <<= 1, ++stage) {
     const bool on = (k & sh) != 0;
+    if (stage >= (int)(__builtin_ctz(GP)) - SAT_FMA_SEL_STAGES) {
+      const int p = (k >> stage) & 1;
 #pragma unroll
-    for (int i = 0; i < GP; ++i) b[i] = on ? (i + sh < GP ? b[i + sh] : INF) : b[i];
+      for (int i = 0; i < GP; ++i) b[i] = sel_fma(p, b[i], i + sh < GP ? b[i + sh] : INF);
+    } else {
+#pragma unroll
+      for (int i = 0; i < GP; ++i) b[i] = on ? (i + sh < GP ? b[i + sh] : INF) : b[i];
+    }
   }
   const int s = b[0];
   const int v = s + R;
@@ -153,19 +176,123 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
         bn = lt ? n : bn;
       }
       int x[GP];
+      if constexpr (SAT_FMA_MULTI) {
+        int on[NN];
 #pragma unroll
-      for (int i = 0; i < GP; ++i) {
-        int y = a[0][i];
+        for (int n = 0; n < NN; ++n) on[n] = (bn == n) ? 1 : 0;
 #pragma unroll
-        for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
-        x[i] = y;
+        for (int i = 0; i < GP; ++i) {
+          int y = a[0][i];
+#pragma unroll
+          for (int n = 1; n < NN; ++n) y = sel_fma(on[n], y, a[n][i]);
+          x[i] = y;
+        }
+        v = place_sorted<GP>(x, g, R);
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int i = 0; i < GP; ++i) a[n][i] = sel_fma(on[n], a[n][i], x[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < GP; ++i) {
+          int y = a[0][i];
+#pragma unroll
+          for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
+          x[i] = y;
+        }
+        v = place_sorted<GP>(x, g, R);
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
       }
-      v = place_sorted<GP>(x, g, R);
-#pragma unroll
-      for (int n = 0; n < NN; ++n)
-#pragma unroll
-        for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
     }
+    ms = max(ms, v);
+  }
+  if constexpr (CHECK == 1) bad = __popc(seen) != T;
+  if constexpr (CHECK != 0) {
+    bad |= maxt >= T || minw == 0u;
+    return bad ? -1 : ms;
+  }
+  return ms;
+}
+
+// Thread-private node-state stride (words) for decode_smem: >= N * GP words and 4 x odd,
+// so a quarter-warp's 16-byte accesses at the same offset hit 8 distinct bank groups.
+__host__ __device__ __forceinline__ int node_state_words(int N, int GP) {
+  int q = (N * GP + 3) / 4;
+  if ((q & 1) == 0) ++q;
+  return 4 * q;
+}
+
+// T design for multi-node clusters: each node's sorted free-time vector lives in this
+// thread's shared-memory slice `ns` (node n at ns[n * GP], 16-byte aligned), so the chosen
+// node is read and written with dynamic indexing (2 x GP/4 vector accesses) instead of
+// register gather/scatter selects over every node.  Starts: one load per node.
+template <int GP, int CHECK, class G>
+__device__ __forceinline__ int decode_smem(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
+                                           int stride, const G& gen, int T, const Problem& pb, int* ns,
+                                           uint32_t* mask = nullptr, int mstride = 0) {
+  static_assert(GP % 4 == 0, "vector node rows");
+  const int N = pb.N;
+  for (int n = 0; n < N; ++n) {
+    int4* row = reinterpret_cast<int4*>(ns + n * GP);
+#pragma unroll
+    for (int j = 0; j < GP / 4; ++j) {
+      const int i = 4 * j;
+      const int gn = pb.gpu_n[n];
+      row[j] = make_int4(i < gn ? 0 : INF, i + 1 < gn ? 0 : INF, i + 2 < gn ? 0 : INF, i + 3 < gn ? 0 : INF);
+    }
+  }
+  bool bad = false;
+  int maxt = 0;
+  uint32_t seen = 0u, minw = 0xffffffffu;
+  if constexpr (CHECK == 2) {
+    for (int w = 0; w < (T + 31) / 32; ++w) mask[w * mstride] = 0u;
+  }
+  int ms = 0;
+  for (int p = 0; p < T; ++p) {
+    int t = gen.perm(p);
+    int c;
+    if constexpr (CHECK != 0) {
+      maxt = max(maxt, t);
+      t = min(t, T - 1);
+      if constexpr (CHECK == 1) {
+        seen |= 1u << t;
+      } else {
+        uint32_t* mw = mask + (t >> 5) * mstride;
+        const uint32_t bit = 1u << (t & 31);
+        const uint32_t m = *mw;
+        bad |= (m & bit) != 0;
+        *mw = m | bit;
+      }
+      c = min(gen.cfg(t), stride - 1);
+    } else {
+      c = gen.cfg(t);
+    }
+    const uint32_t w = tab[t * stride + c];
+    if constexpr (CHECK != 0) minw = min(minw, w);
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    // start of every node (its g-th smallest free time; +inf padding if it has fewer GPUs)
+    int best = ns[g - 1];
+    int bn = 0;
+    for (int n = 1; n < N; ++n) {
+      const int st = ns[n * GP + g - 1];
+      const bool lt = st < best;  // strict: ties keep the lowest node id
+      best = lt ? st : best;
+      bn = lt ? n : bn;
+    }
+    int4* row = reinterpret_cast<int4*>(ns + bn * GP);
+    int x[GP];
+#pragma unroll
+    for (int j = 0; j < GP / 4; ++j) {
+      const int4 q = row[j];
+      x[4 * j] = q.x; x[4 * j + 1] = q.y; x[4 * j + 2] = q.z; x[4 * j + 3] = q.w;
+    }
+    const int v = place_sorted<GP>(x, g, R);
+#pragma unroll
+    for (int j = 0; j < GP / 4; ++j) row[j] = make_int4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
     ms = max(ms, v);
   }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;

@@ -18,9 +18,24 @@ constexpr int GA_B = 128;
 constexpr int WARP_B = 128;
 
 // ------------------------------------------------------------------ shapes
+// (NN, GP): NN >= 1 keeps NN nodes' sorted vectors in registers (decode_sorted); NN == 0 is
+// the multi-node path with node vectors in shared memory and a runtime node count
+// (decode_smem).  GP = GPUs per node padded to a power of two.
 #define SAT_SHAPES(X) \
-  X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(1, 32) X(2, 2) X(2, 4) X(2, 8) X(2, 16) X(2, 32) X(4, 2) X(4, 4) X(4, 8) \
-  X(4, 16) X(8, 2) X(8, 4) X(8, 8) X(16, 2) X(16, 4)
+  X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(1, 32) X(2, 8) X(4, 8) X(0, 4) X(0, 8) X(0, 16) X(0, 32)
+
+// Shared-memory bytes of the NN == 0 node states for a block of B threads.
+__host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, int NN, int GP, int B) {
+  return NN == 0 ? (size_t)4 * node_state_words(pb.N, GP) * B : 0;
+}
+
+// Decode one genome with the (NN, GP) design; `ns` = this thread's node-state slice (NN == 0).
+template <int NN, int GP, int CHECK, class G>
+__device__ __forceinline__ int decode_T(const uint32_t* tab, const uint8_t* S, int stride, const G& gen, int T,
+                                        const Problem& pb, int* ns, uint32_t* mask = nullptr, int mstride = 0) {
+  if constexpr (NN == 0) return decode_smem<GP, CHECK>(tab, S, stride, gen, T, pb, ns, mask, mstride);
+  else return decode_sorted<NN, GP, CHECK>(tab, S, stride, gen, T, pb, mask, mstride);
+}
 
 bool have_sorted_shape(int NN, int GP) {
 #define SAT_HAVE(a, b) if (NN == a && GP == b) return true;
@@ -62,8 +77,9 @@ __device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E, 
 }
 
 // ------------------------------------------------------------------ K1: evaluate (T design)
-size_t eval_smem_bytes(const Problem& pb) {
-  return (size_t)pb.blob_bytes + 4u * EVAL_B * pb.T + 4u * EVAL_B * ((pb.T + 31) / 32) + 3 * 8;
+size_t eval_smem_bytes(const Problem& pb, int NN, int GP) {
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B) + 4u * EVAL_B * pb.T + 4u * EVAL_B * ((pb.T + 31) / 32) +
+         3 * 8;
 }
 
 template <int NN, int GP>
@@ -74,7 +90,8 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
   const int T = pb.T;
   const int tileB = EVAL_B * T;  // bytes per array per tile (multiple of 16)
   uint8_t* s_blob = sm;
-  uint8_t* s_g = sm + pb.blob_bytes;                          // [2 buffers][cfg | perm]
+  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B);   // [2 buffers][cfg | perm]
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 4 * tileB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_mask + EVAL_B * ((T + 31) / 32));
   const int64_t ntiles = (n + EVAL_B - 1) / EVAL_B;
@@ -128,8 +145,9 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     }
     if (first + tid < n) {
       RowGenome gen{bc + tid * T, bp + tid * T};
-      out[first + tid] = (T <= 32) ? decode_sorted<NN, GP, 1>(tab, S, pb.stride, gen, T, pb)
-                                   : decode_sorted<NN, GP, 2>(tab, S, pb.stride, gen, T, pb, s_mask + tid, EVAL_B);
+      int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+      out[first + tid] = (T <= 32) ? decode_T<NN, GP, 1>(tab, S, pb.stride, gen, T, pb, ns)
+                                   : decode_T<NN, GP, 2>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
     }
     __syncthreads();
   }
@@ -209,7 +227,7 @@ cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const u
                             int64_t n, int32_t* out, int sms, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (kind == 1) {
-    const size_t smem = eval_smem_bytes(pb);
+    const size_t smem = eval_smem_bytes(pb, NN, GP);
     const int use_bulk = ((((uintptr_t)cfg) | ((uintptr_t)perm)) & 15u) == 0;
     const int64_t ntiles = (n + EVAL_B - 1) / EVAL_B;
 #define SAT_EVAL(a, b)                                                                   \
@@ -248,8 +266,9 @@ cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* p
 // cfg[t] = (r_cfg div radix[t]) mod S_t, perm = lexicographic unrank of r_perm.
 // Consecutive indices advance cfg like an odometer (job 0 fastest), then perm by
 // next_permutation, so only the first index of a chunk is unranked.
-static size_t enum_smem_bytes(const Problem& pb) {
-  return (size_t)pb.blob_bytes + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) + 32 * 8 + 8;
+static size_t enum_smem_bytes(const Problem& pb, int NN, int GP) {
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, ENUM_B) + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) +
+         32 * 8 + 8;
 }
 
 template <int NN, int GP>
@@ -257,7 +276,8 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
                                                       uint64_t chunk, unsigned long long* best_key) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint8_t* s_blob = sm;
-  uint8_t* s_gen = sm + pb.blob_bytes;
+  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint8_t* s_gen = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, ENUM_B);
   const int T = pb.T;
   const int RS = odd_row_stride(perm_offset(T) + T);
   uint64_t* s_red = reinterpret_cast<uint64_t*>(s_gen + ((ENUM_B * RS + 7) & ~7));
@@ -291,7 +311,8 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
       gen.q(p) = (uint8_t)x;
     }
     for (uint64_t idx = i0; idx < i1; ++idx) {
-      const int ms = decode_sorted<NN, GP, 0>(tab, S, pb.stride, gen, T, pb);
+      const int ms = decode_T<NN, GP, 0>(tab, S, pb.stride, gen, T, pb,
+                                         s_ns + (NN == 0 ? node_state_words(pb.N, GP) * threadIdx.x : 0));
       const uint64_t key = ((uint64_t)ms << 38) | idx;
       best = key < best ? key : best;
       // odometer over cfg (job 0 least significant), carry into perm
@@ -329,7 +350,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
 cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace& es, uint64_t begin, uint64_t end,
                              unsigned long long* best_key, int sms, cudaStream_t st) {
   if (end <= begin) return cudaSuccess;
-  const size_t smem = enum_smem_bytes(pb);
+  const size_t smem = enum_smem_bytes(pb, NN, GP);
   const uint64_t total = end - begin;
 #define SAT_ENUM(a, b)                                                                           \
   if (NN == a && GP == b) {                                                                      \
@@ -352,8 +373,9 @@ cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace&
 // ------------------------------------------------------------------ K3 (+K1): GA
 // Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
 // then parent B, then the OX1 slice bit set for T > 32 (8 words, interleaved per thread).
-static size_t ga_smem_bytes(const Problem& pb, int GS) {
-  return (size_t)pb.blob_bytes + (size_t)2 * GA_B * odd_row_stride(GS) + (size_t)4 * 8 * GA_B + 8 * GA_B + 8;
+static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)2 * GA_B * odd_row_stride(GS) +
+         (size_t)4 * 8 * GA_B + 8 * GA_B + 8;
 }
 
 // Copy a GS-byte global record into a smem row (4-byte stores) and back.
@@ -374,16 +396,18 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
   for (int k = 0; k < GS / 16; ++k) dst[k] = make_uint4(s[4 * k], s[4 * k + 1], s[4 * k + 2], s[4 * k + 3]);
 }
 
-template <int STATE>
+template <int NN, int GP>
 struct GaMinBlocks {
-  static constexpr int value = STATE <= 8 ? 8 : (STATE <= 32 ? 4 : 2);
+  static constexpr int STATE = (NN == 0 ? 1 : NN) * GP;
+  static constexpr int value = NN == 0 ? (GP <= 8 ? 6 : (GP <= 16 ? 4 : 2))
+                                       : (STATE <= 8 ? 8 : (STATE <= 32 ? 4 : 2));
 };
 
 // Child construction follows oracle/ga.py (GA v3): every Philox
 // word has a fixed position, so all lanes draw the same blocks at the same program points
 // and the operators run as uniform loops with predicated writes (no divergent refills).
 template <int NN, int GP>
-__global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
+__global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
          const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
          const int32_t* __restrict__ rec_ms, const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
@@ -394,7 +418,8 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
   const int RS = odd_row_stride(GS);
   const int Tp = perm_offset(T);
   uint8_t* s_blob = sm;
-  uint8_t* s_child = sm + pb.blob_bytes;
+  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint8_t* s_child = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
   uint8_t* s_B = s_child + GA_B * RS;
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + 8 * GA_B);   // [GA_B / 32][32]
@@ -408,6 +433,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
   uint32_t* inA = s_bits + tid;  // OX1 slice set for T > 32: word w at inA[w * GA_B]
   const uint32_t P = (uint32_t)gp.P;
   const int nb = (T + 31) / 32;
+  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
 
   uint64_t lst = ~0ull;
   // The next top-E can only contain keys <= the last elite's key (the elites are carried):
@@ -447,7 +473,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
             ch.q(j) = a;
           }
         }
-        msv = decode_sorted<NN, GP, 0>(tab, S, pb.stride, ch, T, pb);
+        msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
       }
     } else {  // ---------------- generation gen >= 1
       const bool elite = live && slot < gp.E;
@@ -545,7 +571,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN * GP>::value)
         }
       }
       if (elite) msv = rec_ms[slot];
-      if (child) msv = decode_sorted<NN, GP, 0>(tab, S, pb.stride, ch, T, pb);
+      if (child) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
     }
     if (live) {
       store_row(pop + slot * GS, ch.base, GS);
@@ -574,7 +600,7 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
                              int64_t n_seed, const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
                              const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand,
                              int* d_n_cand, int sms, cudaStream_t st) {
-  const size_t smem = ga_smem_bytes(pb, gp.GS);
+  const size_t smem = ga_smem_bytes(pb, NN, GP, gp.GS);
   const int64_t blocks = (gp.P + GA_B - 1) / GA_B;
 #define SAT_GA(a, b)                                                                                        \
   if (NN == a && GP == b) {                                                                                 \
@@ -589,7 +615,7 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
 }
 
 int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms) {
-  const size_t smem = ga_smem_bytes(pb, GS);
+  const size_t smem = ga_smem_bytes(pb, NN, GP, GS);
   const int64_t blocks = (P + GA_B - 1) / GA_B;
 #define SAT_GAC(a, b) \
   if (NN == a && GP == b) return grid_for(k_ga<a, b>, GA_B, smem, sms, blocks) * E;

@@ -11,8 +11,8 @@ namespace sat {
 // library.  Anything else runs on the warp decoder.
 bool have_sorted_shape(int NN, int GP);
 
-// Shared-memory bytes of each kernel for a given problem.
-size_t eval_smem_bytes(const Problem& pb);
+// Shared-memory bytes of the evaluate kernel for a given problem and shape.
+size_t eval_smem_bytes(const Problem& pb, int NN, int GP);
 
 // saturn_evaluate: one makespan per genome (rows of T bytes).  kind: 1 = thread, 2 = warp.
 cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const uint8_t* cfg,
