@@ -525,9 +525,9 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           const int x = gb.q(rd);
           rd = (rd + 1 == T) ? 0 : rd + 1;
           const bool take = xo && !((kept >> x) & 1u);
-          uint8_t& dst = ch.q(pos);
-          dst = take ? (uint8_t)x : dst;
-          pos = take ? ((pos + 1 == T) ? 0 : pos + 1) : pos;
+          if (take) ch.q(pos) = (uint8_t)x;
+          pos += take ? 1 : 0;
+          pos = (pos == T) ? 0 : pos;
         }
       } else {
         for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
@@ -541,9 +541,9 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           const int x = gb.q(rd);
           rd = (rd + 1 == T) ? 0 : rd + 1;
           const bool take = xo && !((inA[(x >> 5) * GA_B] >> (x & 31)) & 1u);
-          uint8_t& dst = ch.q(pos);
-          dst = take ? (uint8_t)x : dst;
-          pos = take ? ((pos + 1 == T) ? 0 : pos + 1) : pos;
+          if (take) ch.q(pos) = (uint8_t)x;
+          pos += take ? 1 : 0;
+          pos = (pos == T) ? 0 : pos;
         }
       }
       // 5. config mutation of one job
@@ -551,23 +551,33 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         const int t = (int)v16(w2.x & 0xffffu, T);
         ch.c(t) = (uint8_t)v16(w2.x >> 16, S[t]);
       }
-      // 6. permutation mutation: new[k] = old[src(k)], old kept in B's (now free) row.
-      //    swap i<->j: src(i) = j, src(j) = i; insertion i->j: src(j) = i and the positions
-      //    between shift by one toward i.
+      // 6. permutation mutation.  Swap (kind 0): two byte moves.  Insertion (kind 1, remove
+      //    the gene at i, reinsert it at j): positions between i and j shift by one toward i,
+      //    done a word (4 genes) at a time with funnel shifts and byte masks, then x -> j.
       const bool pmut = child && (w1.y >> 16) < pm16;
-      if (__any_sync(0xffffffffu, pmut)) {
+      if (pmut) {
         const int kind = (int)(w1.z & 1u);
         const int mi = (int)v16(w1.z >> 16, T), mj = (int)v16(w1.w & 0xffffu, T);
-        const int lo = min(mi, mj), hi = max(mi, mj);
-        const int d = (mi < mj) ? 1 : -1;
-        for (int k = 0; k < T; ++k) gb.q(k) = ch.q(k);
-        for (int k = 0; k < T; ++k) {
-          int src = k;
-          src = (kind == 1 && k >= lo && k <= hi) ? k + d : src;
-          src = (k == mj) ? mi : src;
-          src = (kind == 0 && k == mi) ? mj : src;
-          src = pmut ? src : k;
-          ch.q(k) = gb.q(src);
+        const uint8_t xi = ch.q(mi), xj = ch.q(mj);
+        if (kind == 0) {
+          ch.q(mi) = xj;
+          ch.q(mj) = xi;
+        } else if (mi != mj) {
+          const int lo = min(mi, mj), hi = max(mi, mj);
+          const int nw = (T + 3) >> 2;
+          uint32_t* pw = reinterpret_cast<uint32_t*>(ch.base + Tp);
+          int w = lo >> 2;
+          uint32_t prev = (w > 0) ? pw[w - 1] : 0u, cur = pw[w];
+          for (; w <= (hi >> 2); ++w) {
+            const uint32_t next = (w + 1 < nw) ? pw[w + 1] : 0u;
+            const uint32_t sh = (mi < mj) ? __funnelshift_r(cur, next, 8) : __funnelshift_l(prev, cur, 8);
+            const int bl = max(lo - 4 * w, 0), bh = min(hi - 4 * w + 1, 4);
+            const uint32_t m = (bh >= 4 ? 0xffffffffu : ((1u << (8 * bh)) - 1u)) & ~((1u << (8 * bl)) - 1u);
+            pw[w] = (sh & m) | (cur & ~m);
+            prev = cur;
+            cur = next;
+          }
+          ch.q(mj) = xi;
         }
       }
       if (elite) msv = rec_ms[slot];
