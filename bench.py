@@ -324,6 +324,17 @@ def main():
             torch.cuda.synchronize()
             kernel_only[name] = n * reps / (a.elapsed_time(b) * 1e-3)
         plan.set_decoder(sat.DECODER_AUTO)
+        # exhaustive enumeration (row a4-ii): a 7-job TINY-shaped instance, 6^7 * 7! genomes
+        tv = synth.tiny_variant(7, 7, (4,))
+        ep = sat.Plan(tv.node_gpus, local).load_runtime_table(tv.runtime)
+        ep.enumerate()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        er = ep.enumerate()
+        b.record()
+        torch.cuda.synchronize()
+        kernel_only["enumerate"] = {"genomes": er["evaluated"], "plans_per_s": er["evaluated"] / (a.elapsed_time(b) * 1e-3),
+                                    "optimum": er["makespan"], "instance": "TINY-shaped 7 jobs on 1x4 (seed 7)"}
         kernel_only["unit"] = UNIT
         kernel_only["genomes"] = n
         kernel_only["int_probe_ops_per_s"] = plan.probe_int_peak()

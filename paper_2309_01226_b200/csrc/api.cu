@@ -113,6 +113,7 @@ struct saturn_plan {
   DevBuf<int32_t> pms[2];
   DevBuf<unsigned long long> cand;
   DevBuf<int> n_cand;
+  DevBuf<int> flag;
   DevBuf<int32_t> rec_ms, all_ms;
   DevBuf<uint8_t> rec_gen, all_gen, seeds;
   DevBuf<int> sink;
@@ -673,9 +674,21 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     if (gen % sp->generations_per_epoch == 0) {
       if ((s = exchange()) != SATURN_OK) return s;
       if ((s = record()) != SATURN_OK) return s;
-      if (sp->time_budget_s > 0 && now_s() - t0 >= sp->time_budget_s) {
-        ++gen;
-        break;
+      if (sp->time_budget_s > 0) {
+        // The stop decision must be collective: every island runs the same number of
+        // epochs, or the elite all-gathers would mismatch.  MAX-all-reduce of the flag.
+        int stop = (now_s() - t0 >= sp->time_budget_s) ? 1 : 0;
+        if (p->comm && p->world > 1) {
+          CU(p, p->flag.ensure(1));
+          CU(p, cudaMemcpyAsync(p->flag.p, &stop, sizeof stop, cudaMemcpyHostToDevice, st));
+          NC(p, nccl().allReduce(p->flag.p, p->flag.p, 1, ncclInt32, ncclMax, p->comm, st));
+          CU(p, cudaMemcpyAsync(&stop, p->flag.p, sizeof stop, cudaMemcpyDeviceToHost, st));
+          CU(p, cudaStreamSynchronize(st));
+        }
+        if (stop) {
+          ++gen;
+          break;
+        }
       }
     }
   }
@@ -1129,6 +1142,7 @@ void saturn_plan_destroy(saturn_plan* p) {
     }
     p->cand.release();
     p->n_cand.release();
+    p->flag.release();
     p->rec_ms.release();
     p->all_ms.release();
     p->rec_gen.release();

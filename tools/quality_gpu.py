@@ -54,7 +54,7 @@ def main():
             assert ms == best and oracle.validate(c, pl, best) == []
             t, h = plan.search_history()
             marks = {}
-            for target in (1.0, 2.0, 5.0, 10.0):
+            for target in (0.01, 0.1, 1.0, 2.0, 5.0, 10.0):
                 k = np.searchsorted(t, target, side="right") - 1
                 if k >= 0:
                     marks[f"{target:g}s"] = int(h[k])
