@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 from conftest import ROOT
@@ -96,3 +97,58 @@ def test_binding_fails_loudly_without_library(tmp_path):
             mod.load_library(str(tmp_path / "missing.so"))
         finally:
             mod._lib = old
+
+
+# ---------------------------------------------------------------- host-only handle (no GPU)
+def _host(nodes):
+    return sat.Plan(nodes, device=-1)
+
+
+def test_table_validation_errors(lib):
+    p = _host([4])
+    with pytest.raises(sat.SaturnError) as e:
+        p.num_configs()
+    assert e.value.status == sat.ESTATE
+    table = np.ones((2, 1, 4), np.int32) * 5
+    bad = table.copy()
+    bad[1] = 0                                   # job 1: no feasible config
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(bad)
+    assert e.value.status == sat.EUNSCHEDULABLE and "job 1" in str(e.value)
+    wide = np.zeros((1, 1, 8), np.int32)
+    wide[0, 0, 7] = 9                            # only an 8-GPU config on a 4-GPU node (A8)
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(wide)
+    assert e.value.status == sat.EUNSCHEDULABLE
+    big = table.copy()
+    big[0, 0, 0] = 1 << 24                       # R >= 2^24
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(big)
+    assert e.value.status == sat.EINVAL
+    many = np.full((200, 1, 4), (1 << 19), np.int32)   # sum of max R >= 2^26
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(many)
+    assert e.value.status == sat.EINVAL
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(np.ones((256, 1, 1), np.int32))   # > 255 jobs (u8 genes)
+    assert e.value.status == sat.EINVAL
+    huge = np.ones((255, 64, 4), np.int32)       # 255 configs/job -> packed table > 48 KB
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(huge)
+    assert e.value.status in (sat.ELIMIT, sat.EINVAL)
+    p.load_runtime_table(table)                  # a good table still loads afterwards
+    assert list(p.num_configs()) == [4, 4]
+
+
+def test_compaction_order_matches_spec(lib):
+    """UPP-major, ascending g, g <= max node (A8), through the real library."""
+    import oracle
+    import synth
+    for inst in (synth.txt(0), synth.mix(0), synth.sweep(0, nodes=[2, 2, 4, 8])):
+        p = _host(inst.node_gpus).load_runtime_table(inst.runtime)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        S = p.num_configs()
+        assert list(S) == list(c.S)
+        for t in range(0, inst.n_jobs, 7):
+            for s in range(int(S[t])):
+                assert p.config(t, s) == c.config(t, s)
