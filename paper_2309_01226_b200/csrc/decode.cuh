@@ -217,6 +217,80 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
   return ms;
 }
 
+// K genomes per thread, decoded in lock-step (same T): K independent dependency chains per
+// step give the scheduler instruction-level parallelism (register-resident designs only).
+template <int NN, int GP, int CHECK, int K, class G>
+__device__ __forceinline__ void decode_sorted_k(const uint32_t* __restrict__ tab, int stride, const G (&gen)[K],
+                                                int T, const Problem& pb, int (&out)[K]) {
+  int a[K][NN][GP];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+#pragma unroll
+      for (int i = 0; i < GP; ++i) a[k][n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
+  int maxt[K], ms[K];
+  uint32_t seen[K], minw[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) { maxt[k] = 0; ms[k] = 0; seen[k] = 0u; minw[k] = 0xffffffffu; }
+  for (int p = 0; p < T; ++p) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int t = gen[k].perm(p);
+      int c;
+      if constexpr (CHECK != 0) {
+        maxt[k] = max(maxt[k], t);
+        t = min(t, T - 1);
+        seen[k] |= 1u << t;
+        c = min(gen[k].cfg(t), stride - 1);
+      } else {
+        c = gen[k].cfg(t);
+      }
+      const uint32_t w = tab[t * stride + c];
+      if constexpr (CHECK != 0) minw[k] = min(minw[k], w);
+      const int g = (int)(w >> 24);
+      const int R = (int)(w & R_MASK);
+      int v;
+      if constexpr (NN == 1) {
+        v = place_sorted<GP>(a[k][0], g, R);
+      } else {
+        int best = mux<GP>(a[k][0], g - 1);
+        int bn = 0;
+#pragma unroll
+        for (int n = 1; n < NN; ++n) {
+          const int st = mux<GP>(a[k][n], g - 1);
+          const bool lt = st < best;
+          best = lt ? st : best;
+          bn = lt ? n : bn;
+        }
+        int x[GP];
+#pragma unroll
+        for (int i = 0; i < GP; ++i) {
+          int y = a[k][0][i];
+#pragma unroll
+          for (int n = 1; n < NN; ++n) y = (bn == n) ? a[k][n][i] : y;
+          x[i] = y;
+        }
+        v = place_sorted<GP>(x, g, R);
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int i = 0; i < GP; ++i) a[k][n][i] = (bn == n) ? x[i] : a[k][n][i];
+      }
+      ms[k] = max(ms[k], v);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if constexpr (CHECK != 0) {
+      const bool bad = __popc(seen[k]) != T || maxt[k] >= T || minw[k] == 0u;
+      out[k] = bad ? -1 : ms[k];
+    } else {
+      out[k] = ms[k];
+    }
+  }
+}
+
 // Thread-private node-state stride (words) for decode_smem: >= N * GP words and 4 x odd,
 // so a quarter-warp's 16-byte accesses at the same offset hit 8 distinct bank groups.
 __host__ __device__ __forceinline__ int node_state_words(int N, int GP) {

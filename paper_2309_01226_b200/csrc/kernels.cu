@@ -12,7 +12,12 @@
 
 namespace sat {
 
-constexpr int EVAL_B = 128;  // threads (= genomes per tile) of the evaluate kernel
+constexpr int EVAL_B = 128;  // threads of the evaluate kernel
+#ifndef SAT_EVAL_X
+#define SAT_EVAL_X 1          // genomes per thread in k_evaluate (register designs, T <= 32)
+#endif
+constexpr int EVAL_X = SAT_EVAL_X;
+constexpr int EVAL_TILE = EVAL_B * EVAL_X;  // genomes per tile
 constexpr int ENUM_B = 128;
 constexpr int GA_B = 128;
 constexpr int WARP_B = 128;
@@ -78,8 +83,8 @@ __device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E, 
 
 // ------------------------------------------------------------------ K1: evaluate (T design)
 size_t eval_smem_bytes(const Problem& pb, int NN, int GP) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B) + 4u * EVAL_B * pb.T + 4u * EVAL_B * ((pb.T + 31) / 32) +
-         3 * 8;
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B) + 4u * EVAL_TILE * pb.T +
+         4u * EVAL_B * ((pb.T + 31) / 32) + 3 * 8;
 }
 
 template <int NN, int GP>
@@ -88,13 +93,13 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
                                                      int32_t* __restrict__ out, int use_bulk) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int T = pb.T;
-  const int tileB = EVAL_B * T;  // bytes per array per tile (multiple of 16)
+  const int tileB = EVAL_TILE * T;  // bytes per array per tile (multiple of 16)
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B);   // [2 buffers][cfg | perm]
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 4 * tileB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_mask + EVAL_B * ((T + 31) / 32));
-  const int64_t ntiles = (n + EVAL_B - 1) / EVAL_B;
+  const int64_t ntiles = (n + EVAL_TILE - 1) / EVAL_TILE;
   const int tid = threadIdx.x;
 
   if (tid == 0) {
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     mbar_expect_tx(&bars[2], pb.blob_bytes);
     bulk_g2s(s_blob, pb.blob, pb.blob_bytes, &bars[2]);
     const int64_t tile = blockIdx.x;
-    if (use_bulk && tile < ntiles && (tile + 1) * EVAL_B <= n) {
+    if (use_bulk && tile < ntiles && (tile + 1) * EVAL_TILE <= n) {
       mbar_expect_tx(&bars[0], 2 * tileB);
       bulk_g2s(s_g, gcfg + tile * tileB, tileB, &bars[0]);
       bulk_g2s(s_g + tileB, gperm + tile * tileB, tileB, &bars[0]);
@@ -121,12 +126,12 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     const int buf = it & 1;
     uint8_t* bc = s_g + buf * 2 * tileB;
     uint8_t* bp = bc + tileB;
-    const int64_t first = tile * EVAL_B;
-    const bool full = use_bulk && first + EVAL_B <= n;
+    const int64_t first = tile * EVAL_TILE;
+    const bool full = use_bulk && first + EVAL_TILE <= n;
     if (full) {
       mbar_wait(&bars[buf], (it >> 1) & 1);
     } else {  // ragged last tile (or unaligned caller buffers): plain cooperative loads
-      const int cnt = (int)min((int64_t)EVAL_B, n - first) * T;
+      const int cnt = (int)min((int64_t)EVAL_TILE, n - first) * T;
       for (int k = tid; k < cnt; k += EVAL_B) {
         bc[k] = gcfg[first * T + k];
         bp[k] = gperm[first * T + k];
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     }
     if (tid == 0) {  // prefetch the next tile into the other buffer
       const int64_t nt = tile + gridDim.x;
-      if (use_bulk && nt < ntiles && (nt + 1) * EVAL_B <= n) {
+      if (use_bulk && nt < ntiles && (nt + 1) * EVAL_TILE <= n) {
         uint8_t* nc = s_g + (buf ^ 1) * 2 * tileB;
         fence_proxy_async();
         mbar_expect_tx(&bars[buf ^ 1], 2 * tileB);
@@ -143,11 +148,32 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
         bulk_g2s(nc + tileB, gperm + nt * tileB, tileB, &bars[buf ^ 1]);
       }
     }
-    if (first + tid < n) {
-      RowGenome gen{bc + tid * T, bp + tid * T};
-      int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
-      out[first + tid] = (T <= 32) ? decode_T<NN, GP, 1>(tab, S, pb.stride, gen, T, pb, ns)
+    if constexpr (EVAL_X > 1 && NN >= 1) {
+      if (T <= 32) {
+        RowGenome gens[EVAL_X];
+        int res[EVAL_X];
+#pragma unroll
+        for (int k = 0; k < EVAL_X; ++k) {
+          const int j = tid + k * EVAL_B;
+          const int jj = (first + j < n) ? j : tid;   // dead lanes decode a live genome, result dropped
+          gens[k] = RowGenome{bc + jj * T, bp + jj * T};
+        }
+        decode_sorted_k<NN, GP, 1, EVAL_X>(tab, pb.stride, gens, T, pb, res);
+#pragma unroll
+        for (int k = 0; k < EVAL_X; ++k)
+          if (first + tid + k * EVAL_B < n) out[first + tid + k * EVAL_B] = res[k];
+        __syncthreads();
+        continue;
+      }
+    }
+    for (int k = 0; k < EVAL_X; ++k) {
+      const int j = tid + k * EVAL_B;
+      if (first + j < n) {
+        RowGenome gen{bc + j * T, bp + j * T};
+        int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+        out[first + j] = (T <= 32) ? decode_T<NN, GP, 1>(tab, S, pb.stride, gen, T, pb, ns)
                                    : decode_T<NN, GP, 2>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
+      }
     }
     __syncthreads();
   }
@@ -229,7 +255,7 @@ cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const u
   if (kind == 1) {
     const size_t smem = eval_smem_bytes(pb, NN, GP);
     const int use_bulk = ((((uintptr_t)cfg) | ((uintptr_t)perm)) & 15u) == 0;
-    const int64_t ntiles = (n + EVAL_B - 1) / EVAL_B;
+    const int64_t ntiles = (n + EVAL_TILE - 1) / EVAL_TILE;
 #define SAT_EVAL(a, b)                                                                   \
   if (NN == a && GP == b) {                                                              \
     const int g = grid_for(k_evaluate<a, b>, EVAL_B, smem, sms, ntiles);                 \
