@@ -96,6 +96,9 @@ typedef struct {
   const uint8_t *seed_cfg;       /* host [n_seed][T] genomes placed first, or NULL        */
   const uint8_t *seed_perm;      /* host [n_seed][T]                                      */
   int64_t n_seed;
+  int32_t local_search_iters;    /* >0: memetic step -- at every epoch boundary the E elites
+                                    get this many best-improvement local-search iterations
+                                    (saturn_improve) before the exchange; 0 = off        */
 } saturn_search_params;
 
 /* Create a handle for a cluster of n_nodes nodes with node_gpus[n] GPUs each (Table 1: N,
@@ -176,6 +179,15 @@ saturn_status saturn_search(saturn_plan *p, const saturn_search_params *sp, void
  * pairs, one per epoch; *n_out = number written. */
 saturn_status saturn_search_history(const saturn_plan *p, int64_t n_max, double *t_s, int64_t *makespan,
                                     int64_t *n_out);
+
+/* Best-improvement local search (row f4): each of n genomes
+ * (host cfg/perm [n][T], updated in place) repeatedly moves to its best neighbour --
+ * insertion moves of the permutation, then single-job config changes, smallest (makespan,
+ * move index) -- while that strictly improves its makespan, at most `iters` times; one CTA
+ * per genome, every neighbour decoded on the device.  h_makespan [n] receives the results.
+ * Invalid genomes: EINVAL.  Synchronous. */
+saturn_status saturn_improve(saturn_plan *p, uint8_t *h_cfg, uint8_t *h_perm, int64_t n, int32_t iters,
+                             int32_t *h_makespan, void *stream);
 
 /* Final population of the last search on this device: host uint8 cfg [P][T], perm [P][T],
  * int32 makespan [P].  (Used for operator-replay parity.)  ESTATE before a search. */

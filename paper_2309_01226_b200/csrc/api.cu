@@ -114,6 +114,8 @@ struct saturn_plan {
   DevBuf<unsigned long long> cand;
   DevBuf<int> n_cand;
   DevBuf<int> flag;
+  DevBuf<uint8_t> ls_gen;
+  DevBuf<int32_t> ls_ms;
   DevBuf<int32_t> rec_ms, all_ms;
   DevBuf<uint8_t> rec_gen, all_gen, seeds;
   DevBuf<int> sink;
@@ -635,7 +637,19 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     p->ev_pool.push_back(e);
   }
 
+  saturn_status s0 = SATURN_OK;
+  // memetic step (row f4): improve the E elites, then re-sort them by (ms, position)
+  auto memetic = [&]() -> saturn_status {
+    if (sp->local_search_iters <= 0) return SATURN_OK;
+    CU(p, cudaMemcpyAsync(p->all_ms.p, p->rec_ms.p, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CU(p, cudaMemcpyAsync(p->all_gen.p, p->rec_gen.p, (size_t)E * GS, cudaMemcpyDeviceToDevice, st));
+    CU(p, sat::launch_local_search(p->pb, p->NN, p->GP, p->all_gen.p, p->all_ms.p, E, GS, sp->local_search_iters, st));
+    CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, 1, E, GS, p->rec_ms.p, p->rec_gen.p, st));
+    p->stats.kernel_launches += 2;
+    return SATURN_OK;
+  };
   auto exchange = [&]() -> saturn_status {
+    if ((s0 = memetic()) != SATURN_OK) return s0;
     if (!p->comm || p->world < 2) return SATURN_OK;
     NC(p, nccl().allGather(p->rec_ms.p, p->all_ms.p, (size_t)E, ncclInt32, p->comm, st));
     NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
@@ -723,6 +737,52 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     out->seconds = now_s() - t0;
     out->flags = SATURN_INCUMBENT;
     out->generations = (int32_t)gens_run;
+  }
+  return SATURN_OK;
+}
+
+saturn_status saturn_improve(saturn_plan* p, uint8_t* h_cfg, uint8_t* h_perm, int64_t n, int32_t iters,
+                             int32_t* h_makespan, void* stream) {
+  if (!p) return SATURN_EINVAL;
+  if (host_only(p)) return SATURN_ESTATE;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "improve before load_runtime_table");
+  if (n < 0 || iters < 0 || (n > 0 && (!h_cfg || !h_perm || !h_makespan)))
+    return fail(p, SATURN_EINVAL, "bad arguments");
+  if (n == 0) return SATURN_OK;
+  if (!p->sorted_ok) return fail(p, SATURN_EINVAL, "local search needs the thread decoder for this cluster shape");
+  const int T = p->T, GS = gs_of(T), Tp = sat::perm_offset(T);
+  std::vector<uint8_t> packed((size_t)n * GS, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    std::vector<int> seen(T, 0);
+    for (int k = 0; k < T; ++k) {
+      const int t = h_perm[i * T + k];
+      if (t >= T || seen[t]++) return fail(p, SATURN_EINVAL, "genome %lld: perm is not a permutation", (long long)i);
+      if (h_cfg[i * T + t] >= p->S[t]) return fail(p, SATURN_EINVAL, "genome %lld: cfg out of range", (long long)i);
+    }
+    memcpy(&packed[i * GS], h_cfg + i * T, T);
+    memcpy(&packed[i * GS + Tp], h_perm + i * T, T);
+  }
+  DeviceGuard dg(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CU(p, p->ls_gen.ensure(packed.size()));
+  CU(p, p->ls_ms.ensure((size_t)n));
+  CU(p, p->ws_cfg.ensure((size_t)n * T));
+  CU(p, p->ws_perm.ensure((size_t)n * T));
+  CU(p, cudaMemcpyAsync(p->ws_cfg.p, h_cfg, (size_t)n * T, cudaMemcpyHostToDevice, st));
+  CU(p, cudaMemcpyAsync(p->ws_perm.p, h_perm, (size_t)n * T, cudaMemcpyHostToDevice, st));
+  CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, SATURN_DECODER_THREAD, p->ws_cfg.p, p->ws_perm.p, n, p->ls_ms.p,
+                             p->sms, st));
+  CU(p, cudaMemcpyAsync(p->ls_gen.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
+  CU(p, sat::launch_local_search(p->pb, p->NN, p->GP, p->ls_gen.p, p->ls_ms.p, (int)n, GS, iters, st));
+  CU(p, cudaMemcpyAsync(packed.data(), p->ls_gen.p, packed.size(), cudaMemcpyDeviceToHost, st));
+  CU(p, cudaMemcpyAsync(h_makespan, p->ls_ms.p, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CU(p, cudaStreamSynchronize(st));
+  p->stats.kernel_launches += 2;
+  p->stats.h2d_bytes += (int64_t)packed.size() + 2 * n * T;
+  p->stats.d2h_bytes += (int64_t)packed.size() + n * 4;
+  for (int64_t i = 0; i < n; ++i) {
+    memcpy(h_cfg + i * T, &packed[i * GS], T);
+    memcpy(h_perm + i * T, &packed[i * GS + Tp], T);
   }
   return SATURN_OK;
 }
@@ -1143,6 +1203,8 @@ void saturn_plan_destroy(saturn_plan* p) {
     p->cand.release();
     p->n_cand.release();
     p->flag.release();
+    p->ls_gen.release();
+    p->ls_ms.release();
     p->rec_ms.release();
     p->all_ms.release();
     p->rec_gen.release();

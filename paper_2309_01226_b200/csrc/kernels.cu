@@ -672,6 +672,126 @@ cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaPara
   return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, st);
 }
 
+// ------------------------------------------------------------------ f4: local search
+// One CTA per genome: every thread decodes neighbours (insertion moves, then config moves;
+// numbering as in oracle/local_search.py), the CTA moves to the best (ms, move) if it is a
+// strict improvement, up to `iters` times.  Records are updated in place.
+constexpr int LS_B = 128;
+static size_t ls_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, LS_B) + (size_t)(LS_B + 1) * odd_row_stride(GS) +
+         (size_t)4 * (pb.T + 1) + 8 * (LS_B / 32) + 16 + 8;
+}
+
+template <int NN, int GP>
+__global__ void __launch_bounds__(LS_B) k_local_search(Problem pb, uint8_t* __restrict__ gen, int32_t* __restrict__ ms_io,
+                                                       int GS, int iters) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int T = pb.T, Tp = perm_offset(T), RS = odd_row_stride(GS);
+  uint8_t* s_blob = sm;
+  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint8_t* s_base = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, LS_B);
+  uint8_t* s_rows = s_base + RS;
+  int* s_pre = reinterpret_cast<int*>(s_rows + LS_B * RS);       // prefix of (S_t - 1), T + 1 entries
+  uint64_t* s_red = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_pre + T + 1) + 7) & ~uintptr_t(7));
+  uint64_t* bar = s_red + LS_B / 32 + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* rec = gen + (size_t)blockIdx.x * GS;
+  for (int k = tid; k < GS / 4; k += LS_B)
+    reinterpret_cast<uint32_t*>(s_base)[k] = reinterpret_cast<const uint32_t*>(rec)[k];
+  stage_problem(s_blob, pb, bar);   // its __syncthreads also publishes s_base
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  if (tid == 0) {
+    int acc = 0;
+    for (int t = 0; t < T; ++t) { s_pre[t] = acc; acc += S[t] - 1; }
+    s_pre[T] = acc;
+  }
+  __syncthreads();
+  const int n_ins = T * (T - 1), n_mov = n_ins + s_pre[T];
+  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  const RowG row{s_rows + RS * tid, Tp};
+  const RowG base{s_base, Tp};
+  int cur = ms_io[blockIdx.x];
+  for (int it = 0; it < iters; ++it) {
+    uint64_t best = ~0ull;
+    for (int m = tid; m < n_mov; m += LS_B) {
+      for (int k = 0; k < Tp / 4; ++k)
+        reinterpret_cast<uint32_t*>(row.base)[k] = reinterpret_cast<const uint32_t*>(base.base)[k];
+      if (m < n_ins) {
+        const int i = m / (T - 1), jj = m - i * (T - 1), j = jj < i ? jj : jj + 1;
+        const int lo = min(i, j), hi = max(i, j), d = (i < j) ? 1 : -1;
+        for (int k = 0; k < T; ++k) {
+          int src = (k >= lo && k <= hi) ? k + d : k;
+          src = (k == j) ? i : src;
+          row.q(k) = base.q(src);
+        }
+      } else {
+        const int k2 = m - n_ins;
+        int t = 0;
+        while (s_pre[t + 1] <= k2) ++t;
+        const int r = k2 - s_pre[t];
+        row.c(t) = (uint8_t)(r < base.c(t) ? r : r + 1);
+        for (int k = 0; k < T; ++k) row.q(k) = base.q(k);
+      }
+      const int msn = decode_T<NN, GP, 0>(tab, S, pb.stride, row, T, pb, ns);
+      const uint64_t key = ((uint64_t)(uint32_t)msn << 32) | (uint32_t)m;
+      best = key < best ? key : best;
+    }
+    best = warp_min_u64(best);
+    if (lane == 0) s_red[warp] = best;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t b = s_red[0];
+      for (int w = 1; w < LS_B / 32; ++w) b = s_red[w] < b ? s_red[w] : b;
+      s_red[LS_B / 32] = b;
+    }
+    __syncthreads();
+    const uint64_t b = s_red[LS_B / 32];
+    const int bms = (int)(b >> 32);
+    if (b == ~0ull || bms >= cur) break;  // local optimum (uniform across the CTA)
+    if (tid == 0) {  // apply move b to the base genome
+      const int m = (int)(b & 0xffffffffu);
+      if (m < n_ins) {
+        const int i = m / (T - 1), jj = m - i * (T - 1), j = jj < i ? jj : jj + 1;
+        const int lo = min(i, j), hi = max(i, j), d = (i < j) ? 1 : -1;
+        for (int k = 0; k < T; ++k) row.q(k) = base.q(k);
+        for (int k = 0; k < T; ++k) {
+          int src = (k >= lo && k <= hi) ? k + d : k;
+          src = (k == j) ? i : src;
+          base.q(k) = row.q(src);
+        }
+      } else {
+        const int k2 = m - n_ins;
+        int t = 0;
+        while (s_pre[t + 1] <= k2) ++t;
+        const int r = k2 - s_pre[t];
+        base.c(t) = (uint8_t)(r < base.c(t) ? r : r + 1);
+      }
+    }
+    cur = bms;
+    __syncthreads();
+  }
+  for (int k = tid; k < GS / 4; k += LS_B)
+    reinterpret_cast<uint32_t*>(rec)[k] = reinterpret_cast<const uint32_t*>(s_base)[k];
+  if (tid == 0) ms_io[blockIdx.x] = cur;
+}
+
+cudaError_t launch_local_search(const Problem& pb, int NN, int GP, uint8_t* gen, int32_t* ms, int n, int GS, int iters,
+                                cudaStream_t st) {
+  if (n <= 0 || iters <= 0) return cudaSuccess;
+  const size_t smem = ls_smem_bytes(pb, NN, GP, GS);
+#define SAT_LS(a, b)                                                                        \
+  if (NN == a && GP == b) {                                                                 \
+    cudaFuncSetAttribute(k_local_search<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                        \
+    k_local_search<a, b><<<n, LS_B, smem, st>>>(pb, gen, ms, GS, iters);                    \
+    return cudaGetLastError();                                                              \
+  }
+  SAT_SHAPES(SAT_LS)
+#undef SAT_LS
+  return cudaErrorInvalidConfiguration;
+}
+
 // ------------------------------------------------------------------ K4: select / merge
 __global__ void __launch_bounds__(1024) k_select(const unsigned long long* __restrict__ cand, int* __restrict__ n_cand,
                                                  int E, int GS, const uint8_t* __restrict__ pop,

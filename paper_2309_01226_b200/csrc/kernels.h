@@ -63,6 +63,11 @@ cudaError_t launch_select(const unsigned long long* cand, int* d_n_cand, int E, 
 cudaError_t launch_merge_elites(const int32_t* all_ms, const uint8_t* all_gen, int W, int E, int GS,
                                 int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st);
 
+// Best-improvement local search (row f4) on n genome records (GS bytes each) in place; ms[]
+// holds their makespans on entry and the improved ones on exit.
+cudaError_t launch_local_search(const Problem& pb, int NN, int GP, uint8_t* gen, int32_t* ms, int n, int GS, int iters,
+                                cudaStream_t st);
+
 // Integer-ALU throughput probe (independent IMNMX/ISETP/IADD3/SEL chains).  Returns the
 // number of integer operations one launch performs.
 double launch_int_probe(int sms, int* sink, cudaStream_t st);

@@ -29,7 +29,7 @@ EXPORTS = (
     "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
-    "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_last_error",
+    "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_improve", "saturn_last_error",
     "saturn_plan_destroy",
 )
 BASELINES = {"max": 1, "min": 2, "optimus": 3, "random": 4}
@@ -86,7 +86,7 @@ class SearchParams(ctypes.Structure):
                 ("generations_per_epoch", ctypes.c_int32), ("p_xover_q32", ctypes.c_uint32),
                 ("p_cfg_mut_q32", ctypes.c_uint32), ("p_perm_mut_q32", ctypes.c_uint32),
                 ("seed_cfg", ctypes.POINTER(ctypes.c_uint8)), ("seed_perm", ctypes.POINTER(ctypes.c_uint8)),
-                ("n_seed", ctypes.c_int64)]
+                ("n_seed", ctypes.c_int64), ("local_search_iters", ctypes.c_int32)]
 
 
 _lib = None
@@ -129,6 +129,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_reset_stats": [h],
         "saturn_baseline_genome": [h, i32, u64, P(u8), P(u8)],
         "saturn_introspect": [h, P(IntrospectParams), vp, P(IntrospectResult), P(i64)],
+        "saturn_improve": [h, P(u8), P(u8), i64, i32, P(i32), vp],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
@@ -197,6 +198,7 @@ class SearchConfig:
     p_xover: float = 0.9
     p_cfg_mut: float | None = 0.5    # per-child probability of re-drawing one job's config
     p_perm_mut: float = 0.5
+    local_search_iters: int = 0      # memetic elite improvement per epoch (row f4)
 
 
 def q32(p: float) -> int:
@@ -331,7 +333,8 @@ class Plan:
         return SearchParams(seed=cfg.seed, population=cfg.population, max_generations=cfg.max_generations,
                             time_budget_s=cfg.time_budget_s, elites=cfg.elites,
                             generations_per_epoch=cfg.generations_per_epoch, p_xover_q32=q32(cfg.p_xover),
-                            p_cfg_mut_q32=q32(p_c), p_perm_mut_q32=q32(cfg.p_perm_mut))
+                            p_cfg_mut_q32=q32(p_c), p_perm_mut_q32=q32(cfg.p_perm_mut),
+                            local_search_iters=cfg.local_search_iters)
 
     def introspect(self, interval_s: int = 1000, threshold_s: int = 500, solver: str = "search",
                    search: SearchConfig | None = None, max_rounds: int = 100000, stream=None):
@@ -350,12 +353,7 @@ class Plan:
 
     def search(self, cfg: SearchConfig | None = None, seed_genomes=None, stream=None) -> dict:
         cfg = cfg or SearchConfig()
-        T = self.n_jobs
-        p_c = cfg.p_cfg_mut if cfg.p_cfg_mut is not None else 1.0 / max(T, 1)
-        sp = SearchParams(seed=cfg.seed, population=cfg.population, max_generations=cfg.max_generations,
-                          time_budget_s=cfg.time_budget_s, elites=cfg.elites,
-                          generations_per_epoch=cfg.generations_per_epoch, p_xover_q32=q32(cfg.p_xover),
-                          p_cfg_mut_q32=q32(p_c), p_perm_mut_q32=q32(cfg.p_perm_mut))
+        sp = self._search_params(cfg)
         keep = None
         if seed_genomes is not None:
             sc = np.ascontiguousarray(seed_genomes[0], dtype=np.uint8)
@@ -369,6 +367,16 @@ class Plan:
                     "saturn_search")
         del keep
         return r.as_dict()
+
+    def improve(self, cfg, perm, iters: int = 8, stream=None):
+        """Best-improvement local search (row f4) of host genomes [n][T]; -> (cfg, perm, ms)."""
+        c = np.array(cfg, dtype=np.uint8, copy=True, order="C").reshape(-1, self.n_jobs)
+        q = np.array(perm, dtype=np.uint8, copy=True, order="C").reshape(-1, self.n_jobs)
+        ms = np.zeros(c.shape[0], np.int32)
+        self._check(self._lib.saturn_improve(self._h, _np_ptr(c, ctypes.c_uint8), _np_ptr(q, ctypes.c_uint8),
+                                             c.shape[0], int(iters), _np_ptr(ms, ctypes.c_int32), self._stream(stream)),
+                    "saturn_improve")
+        return c, q, ms
 
     def search_history(self, n_max: int = 1 << 16):
         t = np.zeros(n_max, np.float64)

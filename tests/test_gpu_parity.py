@@ -327,3 +327,51 @@ def test_multinode_shared_memory_decoder(sat, torch, monkeypatch):
                                  p_xover=0.9, p_cfg_mut=0.5, p_perm_mut=0.5))
     gc, gq, gm = plan.search_population(P)
     assert np.array_equal(gc, rc) and np.array_equal(gq, rq) and np.array_equal(gm, oracle.decode_batch(c, rc, rq))
+
+
+# ------------------------------------------------------------------ f4: local search
+@pytest.mark.parametrize("name,n,iters", [("TXT", 24, 6), ("MIX", 8, 3), ("TINY", 16, 4)])
+def test_improve_matches_oracle_local_search(sat, torch, name, n, iters):
+    from oracle.local_search import improve
+    inst = synth.by_name(name, seed=3)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    plan = _plan(sat, inst)
+    cfg, perm = synth.random_genomes(c.S, n, seed=21)
+    gc, gq, gm = plan.improve(cfg, perm, iters)
+    before = oracle.decode_batch(c, cfg, perm)
+    for i in range(n):
+        rc, rq, rm = improve(c, cfg[i], perm[i], iters)
+        assert (list(gc[i]), list(gq[i]), int(gm[i])) == (list(rc), list(rq), rm), i
+        assert rm <= before[i]
+
+
+def test_memetic_search_replays(sat, torch):
+    """Search with the memetic elite step: population after 2 generations = oracle replay of
+    (top-E -> local search -> re-sort) at every epoch boundary."""
+    from oracle.local_search import improve
+    inst = synth.txt(1)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    P, E, seed, iters = 128, 4, 31, 2
+    px, pc, pm = oga.q32(0.9), oga.q32(0.5), oga.q32(0.5)
+    cfg, perm = oga.initial_population(c.S, P, seed)
+    ms = oracle.decode_batch(c, cfg, perm)
+
+    def elites_after_ls(cfg, perm, ms):
+        recs = []
+        for i in oga.elites(ms, E):
+            rc, rq, rm = improve(c, cfg[i], perm[i], iters)
+            recs.append((rm, rc, rq))
+        order = sorted(range(E), key=lambda k: (recs[k][0], k))
+        return [recs[k] for k in order]
+
+    for gen in (1, 2):
+        recs = elites_after_ls(cfg, perm, ms)
+        cfg, perm, _ = oga.next_generation(c.S, cfg, perm, ms, gen, seed, 0, E, px, pc, pm, elite_records=recs)
+        ms = oracle.decode_batch(c, cfg, perm)
+    plan = _plan(sat, inst)
+    r = plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=2, elites=E, generations_per_epoch=1,
+                                     p_xover=0.9, p_cfg_mut=0.5, p_perm_mut=0.5, local_search_iters=iters))
+    gc, gq, gm = plan.search_population(P)
+    assert np.array_equal(gc, cfg) and np.array_equal(gq, perm) and np.array_equal(gm, ms)
+    best, pl, bc, bp = plan.best_plan()
+    assert oracle.decode(c, bc, bp)[0] == best == r["makespan"] <= int(ms.min())
