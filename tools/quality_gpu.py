@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--populations", type=int, nargs="+", default=[1 << 20])
     ap.add_argument("--elites", type=int, default=16)
     ap.add_argument("--epoch", type=int, default=32)
+    ap.add_argument("--ls", type=int, nargs="+", default=[0], help="memetic local-search iterations per epoch")
     ap.add_argument("--bar", default=None, help="quality_bar.json to compare against")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -45,9 +46,9 @@ def main():
             seeds_c.append(gc)
             seeds_p.append(gq)
             base[kind] = int(plan.evaluate_host(gc[None], gq[None])[0])
-        for P in args.populations:
+        for P, ls in [(P, ls) for P in args.populations for ls in args.ls]:
             cfg = sat.SearchConfig(seed=100 + s, population=P, max_generations=1 << 30, time_budget_s=args.budget,
-                                   elites=args.elites, generations_per_epoch=args.epoch)
+                                   elites=args.elites, generations_per_epoch=args.epoch, local_search_iters=ls)
             r = plan.search(cfg, seed_genomes=(np.stack(seeds_c), np.stack(seeds_p)))
             best, pl, bc, bp = plan.best_plan()
             ms, opl = oracle.decode(c, bc, bp)
@@ -58,7 +59,7 @@ def main():
                 k = np.searchsorted(t, target, side="right") - 1
                 if k >= 0:
                     marks[f"{target:g}s"] = int(h[k])
-            run = {"seed": s, "population": P, "best": best, "lower_bound": oracle.lower_bound(c),
+            run = {"seed": s, "population": P, "local_search_iters": ls, "best": best, "lower_bound": oracle.lower_bound(c),
                    "seconds": r["seconds"], "evaluated": r["evaluated"], "generations": r["generations"],
                    "plans_per_s": r["evaluated"] / r["seconds"], "anytime": marks, "baselines": base}
             if bar:
