@@ -346,6 +346,25 @@ def main():
     import oracle
     c = oracle.compact(inst.node_gpus, inst.runtime)
     lb = oracle.lower_bound(c)
+    # "best makespan vs oracle": on TINY the GPU enumeration and a short GPU search against
+    # the oracle's brute-force optimum; on the bench workload the best found against the
+    # area lower bound and the committed 5-minute CPU bar (tools/quality_bar.py).
+    tiny = synth.tiny(0)
+    tplan = sat.Plan(tiny.node_gpus, local).load_runtime_table(tiny.runtime)
+    ct = oracle.compact(tiny.node_gpus, tiny.runtime)
+    t_enum = tplan.enumerate()
+    t_srch = tplan.search(sat.SearchConfig(seed=1, population=1024, max_generations=20, elites=8))
+    bar = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "quality_bar.json" if args.workload == "TXT"
+                               else f"quality_bar_{args.workload}.json")) as f:
+            bar = json.load(f)["seeds"]["0"]["bar"]
+    except Exception:
+        pass
+    vs_oracle = {"TINY": {"oracle_brute_force": oracle.brute_force(ct)[0], "gpu_enumerate": t_enum["makespan"],
+                          "gpu_search": t_srch["makespan"]},
+                 args.workload: {"gpu_best_this_run": best_ms, "lower_bound": lb,
+                                 "cpu_5min_bar_seed0": bar}}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.workload, args.cpu_seconds)
@@ -356,7 +375,7 @@ def main():
             "config": _config(args, {"best_makespan_s": best_ms, "lower_bound_s": lb,
                                      "best_over_lb": best_ms / lb}),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"],
-            "clocks": clk.summary(), "kernel_only": kernel_only}
+            "clocks": clk.summary(), "kernel_only": kernel_only, "best_vs_oracle": vs_oracle}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
