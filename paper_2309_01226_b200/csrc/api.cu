@@ -628,10 +628,10 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p, p->pms[0].p,
                             p->cand.p, p->n_cand.p, p->sms, st));
   CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
-  p->stats.kernel_launches += 2;
+  p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
   // profiling: event pairs around the GA generation kernels (first 512 per search)
   const int64_t n_prof = p->profiling ? std::min<int64_t>(sp->max_generations, 512) : 0;
-  while ((int64_t)p->ev_pool.size() < 2 * n_prof) {
+  while ((int64_t)p->ev_pool.size() < 3 * n_prof) {
     cudaEvent_t e;
     CU(p, cudaEventCreate(&e));
     p->ev_pool.push_back(e);
@@ -677,12 +677,13 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     gp.gen = (uint32_t)gen;
     const int nxt = cur ^ 1;
     const bool timed = gen <= n_prof;
-    if (timed) CU(p, cudaEventRecord(p->ev_pool[2 * (gen - 1)], st));
+    if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * (gen - 1)], st));
     CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
-                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st));
-    if (timed) CU(p, cudaEventRecord(p->ev_pool[2 * (gen - 1) + 1], st));
+                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st,
+                                    timed ? p->ev_pool[3 * (gen - 1) + 1] : nullptr));
+    if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * (gen - 1) + 2], st));
     CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st));
-    p->stats.kernel_launches += 2;
+    p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
     evaluated += (uint64_t)(P - E);
     cur = nxt;
     if (gen % sp->generations_per_epoch == 0) {
@@ -716,11 +717,18 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   CU(p, cudaStreamSynchronize(st));
   p->stats.d2h_bytes += GS + sizeof best;
   for (int64_t g = 1; g <= std::min<int64_t>(n_prof, gens_run); ++g) {
-    float ms = 0.f;
-    CU(p, cudaEventElapsedTime(&ms, p->ev_pool[2 * (g - 1)], p->ev_pool[2 * (g - 1) + 1]));
+    float ms = 0.f, m1 = 0.f;
+    CU(p, cudaEventElapsedTime(&ms, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 2]));
+    CU(p, cudaEventElapsedTime(&m1, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 1]));
     p->stats.ga_kernel_ms += ms;
     p->stats.ga_launches += 1;
     p->stats.ga_decodes += P - E;
+    if (sat::ga_is_split()) {
+      p->stats.breed_kernel_ms += m1;
+      p->stats.decode_kernel_ms += ms - m1;
+    } else {
+      p->stats.decode_kernel_ms += ms;
+    }
   }
   p->best_cfg.assign(g0.begin(), g0.begin() + T);
   p->best_perm.assign(g0.begin() + sat::perm_offset(T), g0.begin() + sat::perm_offset(T) + T);

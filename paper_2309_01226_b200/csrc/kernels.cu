@@ -4,7 +4,9 @@
 //
 // Every kernel stages the problem blob (packed config table + S_t + UPP ids, <= 48 KB)
 // into shared memory once per persistent CTA with a 1-D TMA bulk copy (row a3).
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 
 #include "decode.cuh"
@@ -432,7 +434,7 @@ struct GaMinBlocks {
 // Child construction follows oracle/ga.py (GA v3): every Philox
 // word has a fixed position, so all lanes draw the same blocks at the same program points
 // and the operators run as uniform loops with predicated writes (no divergent refills).
-template <int NN, int GP>
+template <int NN, int GP, bool DECODE>
 __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
          const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
@@ -499,7 +501,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
             ch.q(j) = a;
           }
         }
-        msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+        if constexpr (DECODE) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
       }
     } else {  // ---------------- generation gen >= 1
       const bool elite = live && slot < gp.E;
@@ -606,16 +608,21 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           ch.q(mj) = xi;
         }
       }
-      if (elite) msv = rec_ms[slot];
-      if (child) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      if constexpr (DECODE) {
+        if (elite) msv = rec_ms[slot];
+        if (child) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      }
     }
     if (live) {
       store_row(pop + slot * GS, ch.base, GS);
-      ms_out[slot] = msv;
+      if constexpr (DECODE) ms_out[slot] = msv;
     }
-    const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
-    topE_insert(lst, key, gp.E, cap);
+    if constexpr (DECODE) {
+      const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
+      topE_insert(lst, key, gp.E, cap);
+    }
   }
+  if constexpr (!DECODE) return;
   // block-level merge of the warps' lists -> one candidate list per block
   s_lists[tid] = lst;
   __syncthreads();
@@ -632,17 +639,114 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   }
 }
 
+// The split generation (SATURN_GA_SPLIT=1): k_ga<..., false> breeds children into the
+// population (GA operators only), then k_decode_pop decodes the whole population like
+// k_evaluate (register-light decoder, full occupancy), keeping the elites' makespans and
+// the top-E bookkeeping.  Measured r1: breed 0.198 + decode 0.186 ms vs fused 0.361 ms per
+// TXT generation of 4.2M children, so the fused kernel (GA operators and decode of
+// different warps overlap on the SM) is the default.
+constexpr int DP_B = 128;
+static size_t dp_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, DP_B) + (size_t)DP_B * odd_row_stride(GS) + 8 * DP_B + 8;
+}
+
+template <int NN, int GP>
+__global__ void __launch_bounds__(DP_B) k_decode_pop(Problem pb, GaParams gp, const uint8_t* __restrict__ pop,
+                                                     const int32_t* __restrict__ rec_ms, int32_t* __restrict__ ms_out,
+                                                     unsigned long long* __restrict__ cand, int* __restrict__ n_cand) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int T = pb.T, GS = gp.GS, RS = odd_row_stride(GS), Tp = perm_offset(T);
+  uint8_t* s_blob = sm;
+  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, DP_B);
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_rows + DP_B * RS + ((8 - (DP_B * RS) % 8) % 8));
+  uint64_t* bar = s_lists + DP_B;
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const RowG g{s_rows + RS * tid, Tp};
+  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  const uint64_t cap = (gp.gen == 0) ? ~0ull : (((uint64_t)(uint32_t)rec_ms[gp.E - 1] << 32) | (uint64_t)(gp.E - 1));
+  uint64_t lst = ~0ull;
+  const int per_rec = GS / 16;
+  for (int64_t base = (int64_t)blockIdx.x * DP_B; base < gp.P; base += (int64_t)gridDim.x * DP_B) {
+    const int cnt = (int)min((int64_t)DP_B, gp.P - base);
+    // coalesced tile load: uint4 k of the tile -> row k / per_rec, bytes 16 (k % per_rec) ..
+    const uint4* src = reinterpret_cast<const uint4*>(pop + base * GS);
+    for (int k = tid; k < cnt * per_rec; k += DP_B) {
+      const uint4 v = src[k];
+      uint32_t* d = reinterpret_cast<uint32_t*>(s_rows + RS * (k / per_rec) + 16 * (k % per_rec));
+      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    }
+    __syncthreads();
+    const int64_t slot = base + tid;
+    int msv = INT_MAX;
+    if (tid < cnt) {
+      msv = (gp.gen != 0 && slot < gp.E) ? rec_ms[slot] : decode_T<NN, GP, 0>(tab, S, pb.stride, g, T, pb, ns);
+      ms_out[slot] = msv;
+    }
+    const uint64_t key = (tid < cnt) ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
+    topE_insert(lst, key, gp.E, cap);
+    __syncthreads();
+  }
+  s_lists[tid] = lst;
+  __syncthreads();
+  if (tid < 32) {
+    uint64_t m = ~0ull;
+    for (int w = 0; w < DP_B / 32; ++w) topE_insert(m, s_lists[w * 32 + lane], gp.E);
+    const bool real = lane < gp.E && m != ~0ull;
+    const uint32_t mask = __ballot_sync(0xffffffffu, real);
+    int off = 0;
+    if (lane == 0 && mask) off = atomicAdd(n_cand, __popc(mask));
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (real) cand[off + __popc(mask & ((1u << lane) - 1u))] = m;
+  }
+}
+
+static bool ga_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SATURN_GA_SPLIT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
                              int64_t n_seed, const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
                              const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand,
-                             int* d_n_cand, int sms, cudaStream_t st) {
-  const size_t smem = ga_smem_bytes(pb, NN, GP, gp.GS);
+                             int* d_n_cand, int sms, cudaStream_t st, cudaEvent_t mid) {
   const int64_t blocks = (gp.P + GA_B - 1) / GA_B;
+  if (ga_split()) {
+    {
+      const size_t smem = ga_smem_bytes(pb, 1, 2, gp.GS);
+      const int g = grid_for(k_ga<1, 2, false>, GA_B, smem, sms, blocks);
+      k_ga<1, 2, false><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
+                                               cand, d_n_cand);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    if (mid) cudaEventRecord(mid, st);
+    const size_t smem = dp_smem_bytes(pb, NN, GP, gp.GS);
+    const int64_t dblocks = (gp.P + DP_B - 1) / DP_B;
+#define SAT_DP(a, b)                                                                                   \
+  if (NN == a && GP == b) {                                                                            \
+    const int g = grid_for(k_decode_pop<a, b>, DP_B, smem, sms, dblocks);                              \
+    k_decode_pop<a, b><<<g, DP_B, smem, st>>>(pb, gp, pop, rec_ms, ms, cand, d_n_cand);                \
+    return cudaGetLastError();                                                                         \
+  }
+    SAT_SHAPES(SAT_DP)
+#undef SAT_DP
+    return cudaErrorInvalidConfiguration;
+  }
+  const size_t smem = ga_smem_bytes(pb, NN, GP, gp.GS);
 #define SAT_GA(a, b)                                                                                        \
   if (NN == a && GP == b) {                                                                                 \
-    const int g = grid_for(k_ga<a, b>, GA_B, smem, sms, blocks);                                            \
-    k_ga<a, b><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,   \
-                                      cand, d_n_cand);                                                      \
+    const int g = grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks);                                      \
+    k_ga<a, b, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, \
+                                            ms, cand, d_n_cand);                                            \
+    if (mid) cudaEventRecord(mid, st);                                                                      \
     return cudaGetLastError();                                                                              \
   }
   SAT_SHAPES(SAT_GA)
@@ -651,26 +755,41 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
 }
 
 int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms) {
-  const size_t smem = ga_smem_bytes(pb, NN, GP, GS);
   const int64_t blocks = (P + GA_B - 1) / GA_B;
+  int g1 = 0, g2 = 0;
+  {
+    const size_t smem = dp_smem_bytes(pb, NN, GP, GS);
+    const int64_t dblocks = (P + DP_B - 1) / DP_B;
 #define SAT_GAC(a, b) \
-  if (NN == a && GP == b) return grid_for(k_ga<a, b>, GA_B, smem, sms, blocks) * E;
-  SAT_SHAPES(SAT_GAC)
+    if (NN == a && GP == b) g1 = grid_for(k_decode_pop<a, b>, DP_B, smem, sms, dblocks);
+    SAT_SHAPES(SAT_GAC)
 #undef SAT_GAC
-  return 0;
+  }
+  {
+    const size_t smem = ga_smem_bytes(pb, NN, GP, GS);
+#define SAT_GAC(a, b) \
+    if (NN == a && GP == b) g2 = grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks);
+    SAT_SHAPES(SAT_GAC)
+#undef SAT_GAC
+  }
+  return std::max(g1, g2) * E;
 }
 
 cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
                            int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms,
                            cudaStream_t st) {
   return launch_ga(pb, NN, GP, gp, seeds, n_seed, nullptr, nullptr, nullptr, nullptr, pop, ms, cand, d_n_cand, sms,
-                   st);
+                   st, nullptr);
 }
 cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
                                  const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen, uint8_t* pop,
-                                 int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms, cudaStream_t st) {
-  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, st);
+                                 int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms, cudaStream_t st,
+                                 cudaEvent_t mid) {
+  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, st,
+                   mid);
 }
+
+bool ga_is_split() { return ga_split(); }
 
 // ------------------------------------------------------------------ f4: local search
 // One CTA per genome: every thread decodes neighbours (insertion moves, then config moves;
