@@ -375,3 +375,33 @@ def test_memetic_search_replays(sat, torch):
     assert np.array_equal(gc, cfg) and np.array_equal(gq, perm) and np.array_equal(gm, ms)
     best, pl, bc, bp = plan.best_plan()
     assert oracle.decode(c, bc, bp)[0] == best == r["makespan"] <= int(ms.min())
+
+
+def test_split_generation_mode_replays(sat, torch):
+    """SATURN_GA_SPLIT=1 (breed kernel + population decode kernel) reproduces the same GA
+    trajectory as the oracle (run in a subprocess: the mode is read once per process)."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = r'''
+import sys; sys.path.insert(0, %r)
+import numpy as np, oracle, synth
+from oracle import ga as oga
+import paper_2309_01226_b200 as sat
+inst = synth.txt(2); c = oracle.compact(inst.node_gpus, inst.runtime)
+P, E, seed = 256, 8, 5
+cfg, perm = oga.initial_population(c.S, P, seed); ms = oracle.decode_batch(c, cfg, perm)
+for gen in (1, 2, 3):
+    cfg, perm, _ = oga.next_generation(c.S, cfg, perm, ms, gen, seed, 0, E, oga.q32(0.9), oga.q32(0.5), oga.q32(0.5))
+    ms = oracle.decode_batch(c, cfg, perm)
+plan = sat.Plan(inst.node_gpus, 0).load_runtime_table(inst.runtime)
+plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=3, elites=E, generations_per_epoch=1,
+                             p_xover=0.9, p_cfg_mut=0.5, p_perm_mut=0.5))
+gc, gq, gm = plan.search_population(P)
+assert np.array_equal(gc, cfg) and np.array_equal(gq, perm) and np.array_equal(gm, ms)
+print("SPLIT-OK")
+''' % ROOT
+    import os
+    env = dict(os.environ, SATURN_GA_SPLIT="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert "SPLIT-OK" in out.stdout, out.stderr[-2000:]
