@@ -140,6 +140,14 @@ saturn_status saturn_set_decoder(saturn_plan *p, int32_t kind);
 saturn_status saturn_evaluate(saturn_plan *p, const uint8_t *d_cfg, const uint8_t *d_perm, int64_t n,
                               int32_t *d_makespan, void *stream);
 
+/* Node-gene variant (row f4): d_node device uint8 [n][T] gives each job's node (0xFF = the
+ * decoder's greedy choice for that job).  With node genes the decoder space provably
+ * contains the SPASE optimum.  A node gene naming a missing node or a
+ * node with fewer than g GPUs makes the genome invalid (-1).  EINVAL for cluster shapes
+ * without a compiled register decoder. */
+saturn_status saturn_evaluate_nodes(saturn_plan *p, const uint8_t *d_cfg, const uint8_t *d_perm,
+                                    const uint8_t *d_node, int64_t n, int32_t *d_makespan, void *stream);
+
 /* Same with HOST buffers: copies genomes host->device and makespans device->host inside the
  * call (staged through the handle's device workspace); synchronous. */
 saturn_status saturn_evaluate_host(saturn_plan *p, const uint8_t *h_cfg, const uint8_t *h_perm, int64_t n,

@@ -18,7 +18,7 @@ Pieces:
 Parity status per function is listed in DESIGN.md ("Oracle pins").
 """
 from .decoder import (  # noqa: F401
-    Compacted, compact, decode, decode_batch, brute_force, brute_force_node_gene,
+    Compacted, compact, decode, decode_batch, decode_batch_nodes, brute_force, brute_force_node_gene,
     space_size, unrank, rank, build_library,
 )
 from .checks import validate, lower_bound  # noqa: F401

@@ -46,6 +46,9 @@ def _L():
         _lib.or_decode_batch.restype = None
         _lib.or_decode_batch.argtypes = [i32, P(i32), i32, i32, P(i32), P(i32), P(i32), ctypes.c_int64,
                                          P(u8), P(u8), P(i32)]
+        _lib.or_decode_batch_nodes.restype = None
+        _lib.or_decode_batch_nodes.argtypes = [i32, P(i32), i32, i32, P(i32), P(i32), P(i32), ctypes.c_int64,
+                                               P(u8), P(u8), P(u8), P(i32)]
         _lib.or_unrank.restype = ctypes.c_int
         _lib.or_unrank.argtypes = [i32, P(i32), u64, P(u8), P(u8)]
         _lib.or_brute_force.restype = i32
@@ -141,6 +144,21 @@ def decode_batch(c: Compacted, cfg, perm) -> np.ndarray:
     lib.or_decode_batch(len(c.node_gpus), _p(c.node_gpus, ctypes.c_int32), c.n_jobs, c.stride,
                         _p(c.gpus, ctypes.c_int32), _p(c.runtime, ctypes.c_int32), _p(c.S, ctypes.c_int32),
                         n, _p(cfg, ctypes.c_uint8), _p(perm, ctypes.c_uint8), _p(out, ctypes.c_int32))
+    return out
+
+
+def decode_batch_nodes(c: Compacted, cfg, perm, node) -> np.ndarray:
+    """O1 with node genes (0xFF = greedy for that job) over genome rows -> makespans."""
+    lib = _L()
+    cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
+    perm = np.ascontiguousarray(perm, dtype=np.uint8)
+    node = np.ascontiguousarray(node, dtype=np.uint8)
+    n = cfg.shape[0]
+    out = np.empty(n, np.int32)
+    lib.or_decode_batch_nodes(len(c.node_gpus), _p(c.node_gpus, ctypes.c_int32), c.n_jobs, c.stride,
+                              _p(c.gpus, ctypes.c_int32), _p(c.runtime, ctypes.c_int32), _p(c.S, ctypes.c_int32),
+                              n, _p(cfg, ctypes.c_uint8), _p(perm, ctypes.c_uint8), _p(node, ctypes.c_uint8),
+                              _p(out, ctypes.c_int32))
     return out
 
 

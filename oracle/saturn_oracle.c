@@ -53,8 +53,9 @@ typedef struct {
  *   cg[t*stride+s], cr[...]     G_{t,s} GPUs and runtime R_{t,s}; n_cfg[t] = S_t
  *   cfg[t], perm[p]           the genome
  *   node_gene[t]              NULL -> greedy node choice (O1); else job t must run on
- *                             node node_gene[t] (node-gene variant used by the
- *                             completeness checks)
+ *                             node node_gene[t], or choose greedily if it is 0xFF
+ *                             (node-gene variant: the completeness checks of SURVEY.md
+ *                             §8c O2 and row f4)
  *   out[t]                    optional per-job placement record (job-id order)
  * Returns the makespan, or -1 if the genome is invalid (cfg out of range, perm not a
  * permutation, node gene out of range or too small for the config).
@@ -94,7 +95,7 @@ int32_t or_decode(int32_t n_nodes, const int32_t *gpu_n, int32_t n_jobs, int32_t
         int32_t best_s = 0;
         for (int n = 0; n < n_nodes; ++n) {
             if (gpu_n[n] < g) continue;
-            if (node_gene && node_gene[t] != n) continue;
+            if (node_gene && node_gene[t] != 0xFF && node_gene[t] != n) continue;
             int32_t sorted_free[OR_MAX_GPUS];
             int k = gpu_n[n];
             for (int i = 0; i < k; ++i) sorted_free[i] = free_t[first[n] + i];
@@ -152,6 +153,17 @@ void or_decode_batch(int32_t n_nodes, const int32_t *gpu_n, int32_t n_jobs, int3
     for (int64_t i = 0; i < n; ++i)
         makespan[i] = or_decode(n_nodes, gpu_n, n_jobs, stride, cg, cr, n_cfg,
                                 cfg + i * n_jobs, perm + i * n_jobs, NULL, NULL);
+}
+
+/* O1 with node genes over n genomes: node[i*n_jobs + t] (0xFF = greedy for that job). */
+void or_decode_batch_nodes(int32_t n_nodes, const int32_t *gpu_n, int32_t n_jobs, int32_t stride,
+                           const int32_t *cg, const int32_t *cr, const int32_t *n_cfg,
+                           int64_t n, const uint8_t *cfg, const uint8_t *perm, const uint8_t *node,
+                           int32_t *makespan)
+{
+    for (int64_t i = 0; i < n; ++i)
+        makespan[i] = or_decode(n_nodes, gpu_n, n_jobs, stride, cg, cr, n_cfg,
+                                cfg + i * n_jobs, perm + i * n_jobs, node + i * n_jobs, NULL);
 }
 
 /*

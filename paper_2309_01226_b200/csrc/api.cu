@@ -395,6 +395,26 @@ saturn_status saturn_evaluate(saturn_plan* p, const uint8_t* d_cfg, const uint8_
   return SATURN_OK;
 }
 
+saturn_status saturn_evaluate_nodes(saturn_plan* p, const uint8_t* d_cfg, const uint8_t* d_perm,
+                                    const uint8_t* d_node, int64_t n, int32_t* d_makespan, void* stream) {
+  if (!p) return SATURN_EINVAL;
+  if (host_only(p)) return SATURN_ESTATE;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "evaluate before load_runtime_table");
+  if (n < 0) return fail(p, SATURN_EINVAL, "n < 0");
+  if (n == 0) return SATURN_OK;
+  if (!d_cfg || !d_perm || !d_node || !d_makespan) return fail(p, SATURN_EINVAL, "NULL buffer");
+  // node genes need a register decoder shape; pick the one for the real node count
+  const int nn = pow2_at_least((int)p->gpu_n.size());
+  const int gp = std::max(2, pow2_at_least(p->maxG));
+  if (!sat::have_sorted_shape(nn, gp))
+    return fail(p, SATURN_EINVAL, "node genes need a compiled register shape (%d x %d)", nn, gp);
+  DeviceGuard dg(p->device);
+  CU(p, sat::launch_evaluate_nodes(p->pb, nn, gp, d_cfg, d_perm, d_node, n, d_makespan, p->sms,
+                                   static_cast<cudaStream_t>(stream)));
+  p->stats.kernel_launches += 1;
+  return SATURN_OK;
+}
+
 saturn_status saturn_evaluate_host(saturn_plan* p, const uint8_t* h_cfg, const uint8_t* h_perm, int64_t n,
                                    int32_t* h_makespan, void* stream) {
   if (!p) return SATURN_EINVAL;

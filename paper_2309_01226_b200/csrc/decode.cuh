@@ -217,6 +217,70 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
   return ms;
 }
 
+// Node-gene variant (row f4; SURVEY.md §8c O2 -- with the node in the genome the decoder
+// space provably contains the SPASE optimum): job t runs on node nd[t], or picks greedily
+// if nd[t] == 0xFF.  Always validity-checked: a node gene naming a missing node or one with
+// fewer than g GPUs makes the genome invalid (-1), like a bad cfg / perm.
+template <int NN, int GP>
+__device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ tab, int stride,
+                                                   const uint8_t* cfg, const uint8_t* perm, const uint8_t* nd,
+                                                   int T, const Problem& pb, uint32_t* mask, int mstride) {
+  int a[NN][GP];
+#pragma unroll
+  for (int n = 0; n < NN; ++n)
+#pragma unroll
+    for (int i = 0; i < GP; ++i) a[n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
+  bool bad = false;
+  int maxt = 0;
+  uint32_t minw = 0xffffffffu;
+  for (int w = 0; w < (T + 31) / 32; ++w) mask[w * mstride] = 0u;
+  int ms = 0;
+  for (int p = 0; p < T; ++p) {
+    int t = perm[p];
+    maxt = max(maxt, t);
+    t = min(t, T - 1);
+    uint32_t* mw = mask + (t >> 5) * mstride;
+    const uint32_t bit = 1u << (t & 31);
+    const uint32_t m = *mw;
+    bad |= (m & bit) != 0;
+    *mw = m | bit;
+    const int c = min((int)cfg[t], stride - 1);
+    const uint32_t w = tab[t * stride + c];
+    minw = min(minw, w);
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    const int want = nd[t];
+    int best = INF, bn = 0;
+#pragma unroll
+    for (int n = 0; n < NN; ++n) {
+      const int st = mux<GP>(a[n], max(g - 1, 0));
+      const bool allowed = (want == 0xFF) || (want == n);
+      const bool lt = allowed && st < best;
+      best = lt ? st : best;
+      bn = lt ? n : bn;
+    }
+    bad |= (want != 0xFF) && (want >= pb.N || g > pb.gpu_n[min(want, MAX_NODES - 1)]);
+    bad |= best == INF;
+    int x[GP];
+#pragma unroll
+    for (int i = 0; i < GP; ++i) {
+      int y = a[0][i];
+#pragma unroll
+      for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
+      x[i] = y;
+    }
+    int v = place_sorted<GP>(x, max(g, 1), R);
+    if (best == INF) v = 0;
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+#pragma unroll
+      for (int i = 0; i < GP; ++i) a[n][i] = (bn == n && best != INF) ? x[i] : a[n][i];
+    ms = max(ms, v);
+  }
+  bad |= maxt >= T || minw == 0u;
+  return bad ? -1 : ms;
+}
+
 // K genomes per thread, decoded in lock-step (same T): K independent dependency chains per
 // step give the scheduler instruction-level parallelism (register-resident designs only).
 template <int NN, int GP, int CHECK, int K, class G>

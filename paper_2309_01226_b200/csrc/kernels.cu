@@ -289,6 +289,41 @@ cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* p
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ K1 with node genes (f4)
+constexpr int EVN_B = 128;
+template <int NN, int GP>
+__global__ void __launch_bounds__(EVN_B) k_evaluate_nodes(Problem pb, const uint8_t* __restrict__ gcfg,
+                                                          const uint8_t* __restrict__ gperm,
+                                                          const uint8_t* __restrict__ gnode, int64_t n,
+                                                          int32_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint8_t* s_blob = sm;
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(sm + pb.blob_bytes);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_mask + EVN_B * 8);
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const int T = pb.T;
+  for (int64_t i = (int64_t)blockIdx.x * EVN_B + threadIdx.x; i < n; i += (int64_t)gridDim.x * EVN_B)
+    out[i] = decode_sorted_nodes<NN, GP>(tab, pb.stride, gcfg + i * T, gperm + i * T, gnode + i * T, T, pb,
+                                         s_mask + threadIdx.x, EVN_B);
+}
+
+cudaError_t launch_evaluate_nodes(const Problem& pb, int NN, int GP, const uint8_t* cfg, const uint8_t* perm,
+                                  const uint8_t* node, int64_t n, int32_t* out, int sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = (size_t)pb.blob_bytes + 4 * 8 * EVN_B + 8;
+  const int64_t blocks = (n + EVN_B - 1) / EVN_B;
+#define SAT_EVN(a, b)                                                                 \
+  if (NN == a && GP == b && a >= 1) {                                                 \
+    const int g = grid_for(k_evaluate_nodes<(a >= 1 ? a : 1), b>, EVN_B, smem, sms, blocks); \
+    k_evaluate_nodes<(a >= 1 ? a : 1), b><<<g, EVN_B, smem, st>>>(pb, cfg, perm, node, n, out); \
+    return cudaGetLastError();                                                        \
+  }
+  SAT_SHAPES(SAT_EVN)
+#undef SAT_EVN
+  return cudaErrorInvalidConfiguration;
+}
+
 // ------------------------------------------------------------------ K2: enumerate
 // Genome index G -> (cfg, perm): r_cfg = G mod prod S, r_perm = G div prod S,
 // cfg[t] = (r_cfg div radix[t]) mod S_t, perm = lexicographic unrank of r_perm.

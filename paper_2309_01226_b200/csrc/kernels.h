@@ -18,6 +18,10 @@ size_t eval_smem_bytes(const Problem& pb, int NN, int GP);
 cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const uint8_t* cfg,
                             const uint8_t* perm, int64_t n, int32_t* out, int sms, cudaStream_t st);
 
+// Node-gene decode (row f4): node[n][T], 0xFF = greedy for that job.  Register shapes only.
+cudaError_t launch_evaluate_nodes(const Problem& pb, int NN, int GP, const uint8_t* cfg, const uint8_t* perm,
+                                  const uint8_t* node, int64_t n, int32_t* out, int sms, cudaStream_t st);
+
 // Trace decode (W design): placements[n][T] (32 B records, job-id order) and makespans.
 cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* perm, int64_t n,
                          void* placements, int32_t* out, int sms, cudaStream_t st);

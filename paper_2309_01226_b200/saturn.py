@@ -25,7 +25,7 @@ DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
 # Every symbol declared in include/saturn.h.
 EXPORTS = (
     "saturn_plan_create", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
-    "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
+    "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_nodes", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
     "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
@@ -113,6 +113,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_set_decoder": [h, i32],
         "saturn_evaluate": [h, vp, vp, i64, vp, vp],
         "saturn_evaluate_host": [h, P(u8), P(u8), i64, P(i32), vp],
+        "saturn_evaluate_nodes": [h, vp, vp, vp, i64, vp, vp],
         "saturn_trace": [h, vp, vp, i64, vp, vp, vp],
         "saturn_space_size": [h, P(u64)],
         "saturn_enumerate": [h, u64, vp, P(Result)],
@@ -292,6 +293,18 @@ class Plan:
                                               _dev_ptr(perm, "uint8", (n, self.n_jobs)), n,
                                               _dev_ptr(out, "int32", (n,)), self._stream(stream)),
                     "saturn_evaluate")
+        return out
+
+    def evaluate_nodes(self, cfg, perm, node, out=None, stream=None):
+        """Node-gene decode (row f4): node CUDA uint8 [n][T], 0xFF = greedy for that job."""
+        import torch
+        n = int(cfg.shape[0])
+        if out is None:
+            out = torch.empty(n, dtype=torch.int32, device=cfg.device)
+        T = self.n_jobs
+        self._check(self._lib.saturn_evaluate_nodes(self._h, _dev_ptr(cfg, "uint8", (n, T)), _dev_ptr(perm, "uint8", (n, T)),
+                                                    _dev_ptr(node, "uint8", (n, T)), n, _dev_ptr(out, "int32", (n,)),
+                                                    self._stream(stream)), "saturn_evaluate_nodes")
         return out
 
     def evaluate_host(self, cfg: np.ndarray, perm: np.ndarray, stream=None) -> np.ndarray:

@@ -405,3 +405,52 @@ print("SPLIT-OK")
     env = dict(os.environ, SATURN_GA_SPLIT="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert "SPLIT-OK" in out.stdout, out.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ f4: node genes
+def test_node_genes_match_oracle(sat, torch):
+    for inst in (synth.mix(3), synth.sweep(2, n_jobs=40), synth.sweep(4, n_jobs=30, nodes=[2, 2, 4, 8]),
+                 synth.sweep(5, n_jobs=30, nodes=[8, 4]), synth.txt(1)):
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        plan = _plan(sat, inst)
+        n = 4000
+        cfg, perm = synth.random_genomes(c.S, n, seed=13)
+        rng = np.random.default_rng(3)
+        N = len(inst.node_gpus)
+        node = rng.integers(0, N + 1, size=(n, c.n_jobs)).astype(np.uint8)
+        node[node == N] = 0xFF                              # some greedy genes
+        node[: n // 2] = np.where(rng.random((n // 2, c.n_jobs)) < 0.5, 0xFF, node[: n // 2])
+        node[0, 0] = N + 3                                  # a missing node -> invalid
+        got = plan.evaluate_nodes(torch.from_numpy(cfg).cuda(), torch.from_numpy(perm).cuda(),
+                                  torch.from_numpy(node).cuda()).cpu().numpy()
+        ref = oracle.decode_batch_nodes(c, cfg, perm, node)
+        assert got[0] == -1 and np.array_equal(got, ref)
+        greedy = np.full_like(node, 0xFF)
+        got = plan.evaluate_nodes(torch.from_numpy(cfg).cuda(), torch.from_numpy(perm).cuda(),
+                                  torch.from_numpy(greedy).cuda()).cpu().numpy()
+        assert np.array_equal(got, oracle.decode_batch(c, cfg, perm))
+
+
+def test_node_gene_space_reaches_the_exact_optimum(sat, torch):
+    """Completeness: min over all (cfg, node, perm) genomes, decoded on the
+    GPU, equals the independent time-indexed exact optimum (O4a)."""
+    import itertools
+    from oracle.exact import exact_makespan
+    for seed in range(6):
+        rng = np.random.default_rng(900 + seed)
+        inst = synth.random_tiny(rng, max_jobs=3, node_choices=([2, 2], [2, 3], [3, 1]), max_r=6)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        T, N = c.n_jobs, len(inst.node_gpus)
+        rows = []
+        for cf in itertools.product(*[range(int(s)) for s in c.S]):
+            for nd in itertools.product(range(N), repeat=T):
+                for pm in itertools.permutations(range(T)):
+                    rows.append((cf, nd, pm))
+        cfg = np.array([r[0] for r in rows], np.uint8).reshape(-1, T)
+        node = np.array([r[1] for r in rows], np.uint8).reshape(-1, T)
+        perm = np.array([r[2] for r in rows], np.uint8).reshape(-1, T)
+        plan = _plan(sat, inst)
+        ms = plan.evaluate_nodes(torch.from_numpy(cfg).cuda(), torch.from_numpy(perm).cuda(),
+                                 torch.from_numpy(node).cuda()).cpu().numpy()
+        assert np.array_equal(ms, oracle.decode_batch_nodes(c, cfg, perm, node))
+        assert ms[ms >= 0].min() == exact_makespan(c)
