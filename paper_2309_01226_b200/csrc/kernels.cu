@@ -29,7 +29,8 @@ constexpr int WARP_B = 128;
 // the multi-node path with node vectors in shared memory and a runtime node count
 // (decode_smem).  GP = GPUs per node padded to a power of two.
 #define SAT_SHAPES(X) \
-  X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(1, 32) X(2, 8) X(4, 8) X(0, 4) X(0, 8) X(0, 16) X(0, 32)
+  X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(1, 32) X(2, 2) X(2, 4) X(2, 8) X(4, 2) X(4, 4) X(4, 8) \
+  X(0, 4) X(0, 8) X(0, 16) X(0, 32)
 
 // Shared-memory bytes of the NN == 0 node states for a block of B threads.
 __host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, int NN, int GP, int B) {
