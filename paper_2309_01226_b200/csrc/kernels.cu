@@ -6,6 +6,9 @@
 // into shared memory once per persistent CTA with a 1-D TMA bulk copy (row a3).
 #include <algorithm>
 #include <climits>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <cstdlib>
 #include <cstdio>
 
@@ -240,13 +243,40 @@ __global__ void __launch_bounds__(WARP_B) k_eval_warp(Problem pb, const uint8_t*
 }
 
 // ------------------------------------------------------------------ launch helpers
+// Persistent grid = SMs x resident CTAs for (kernel, block, dynamic smem).  The attribute
+// call and occupancy query cost ~10 us of host time, so results are cached per
+// (kernel, threads, smem, device) -- a search launches two kernels per generation.
+struct GridKey {
+  const void* fn;
+  int threads;
+  size_t smem;
+  int device;
+  bool operator==(const GridKey& o) const {
+    return fn == o.fn && threads == o.threads && smem == o.smem && device == o.device;
+  }
+};
+static std::mutex g_grid_mu;
+static std::vector<std::pair<GridKey, int>> g_grid_cache;
+
 template <class K>
 static int grid_for(K kernel, int threads, size_t smem, int sms, int64_t work_blocks) {
-  static_assert(sizeof(K) > 0, "");
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
-  if (occ < 1) occ = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const GridKey key{reinterpret_cast<const void*>(kernel), threads, smem, dev};
+  int occ = -1;
+  {
+    std::lock_guard<std::mutex> lk(g_grid_mu);
+    for (const auto& e : g_grid_cache)
+      if (e.first == key) { occ = e.second; break; }
+  }
+  if (occ < 0) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+    if (occ < 1) occ = 1;
+    std::lock_guard<std::mutex> lk(g_grid_mu);
+    g_grid_cache.push_back({key, occ});
+  }
   int64_t g = (int64_t)sms * occ;
   if (work_blocks < g) g = work_blocks;
   return (int)(g < 1 ? 1 : g);
@@ -937,8 +967,7 @@ cudaError_t launch_local_search(const Problem& pb, int NN, int GP, uint8_t* gen,
   const size_t smem = ls_smem_bytes(pb, NN, GP, GS);
 #define SAT_LS(a, b)                                                                        \
   if (NN == a && GP == b) {                                                                 \
-    cudaFuncSetAttribute(k_local_search<a, b>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         (int)smem);                                                        \
+    (void)grid_for(k_local_search<a, b>, LS_B, smem, 1, 1);                                 \
     k_local_search<a, b><<<n, LS_B, smem, st>>>(pb, gen, ms, GS, iters);                    \
     return cudaGetLastError();                                                              \
   }
