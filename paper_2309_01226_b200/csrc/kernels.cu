@@ -270,7 +270,12 @@ static int grid_for(K kernel, int threads, size_t smem, int sms, int64_t work_bl
       if (e.first == key) { occ = e.second; break; }
   }
   if (occ < 0) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // The attribute is per function: always allow the opt-in maximum (227 KB on B200), so a
+    // later launch of the same kernel with a larger table never trips over a smaller value
+    // set for an earlier one.  Occupancy is still computed for this launch's smem.
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin > 0 ? optin : (int)smem);
     occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     if (occ < 1) occ = 1;
