@@ -498,8 +498,11 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
 template <int NN, int GP>
 struct GaMinBlocks {
   static constexpr int STATE = (NN == 0 ? 1 : NN) * GP;
+#ifndef SAT_GA_MINB_SMALL
+#define SAT_GA_MINB_SMALL 8
+#endif
   static constexpr int value = NN == 0 ? (GP <= 8 ? 6 : (GP <= 16 ? 4 : 2))
-                                       : (STATE <= 8 ? 8 : (STATE <= 32 ? 4 : 2));
+                                       : (STATE <= 8 ? SAT_GA_MINB_SMALL : (STATE <= 32 ? 4 : 2));
 };
 
 // Child construction follows oracle/ga.py (GA v3): every Philox
