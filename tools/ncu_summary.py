@@ -67,6 +67,7 @@ def main():
     ap.add_argument('--ga')
     ap.add_argument('--eval')
     ap.add_argument('--launches')
+    ap.add_argument('--enum')
     ap.add_argument('--workload', default='TXT')
     args = ap.parse_args()
     outdir = os.path.join(ROOT, 'profiles', args.round)
@@ -81,6 +82,8 @@ def main():
                       f, indent=1)
     if args.eval:
         summ['k_evaluate (2^24 genomes)'] = summarise(args.eval)
+    if args.enum:
+        summ['k_enumerate (TINY-shaped 7 jobs, 1.41e9 genomes)'] = summarise(args.enum)
     if args.launches:
         summ['launch_list_shares'] = launches(args.launches)
     with open(os.path.join(outdir, 'ncu_summary.json'), 'w') as f:
