@@ -454,3 +454,50 @@ def test_node_gene_space_reaches_the_exact_optimum(sat, torch):
                                  torch.from_numpy(node).cuda()).cpu().numpy()
         assert np.array_equal(ms, oracle.decode_batch_nodes(c, cfg, perm, node))
         assert ms[ms >= 0].min() == exact_makespan(c)
+
+
+# ------------------------------------------------------------------ edge cases
+def _edge_instances():
+    rng = np.random.default_rng(77)
+
+    def table(T, U, G, p=0.6, r=(1, 50)):
+        t = np.where(rng.random((T, U, G)) < p, rng.integers(r[0], r[1], size=(T, U, G)), 0).astype(np.int32)
+        t[:, 0, 0] = rng.integers(r[0], r[1], size=T)     # every job has a 1-GPU config
+        return t
+    return [
+        ("T=1", [4], table(1, 2, 4)),
+        ("T=255", [8, 8], table(255, 2, 8, r=(1, 200))),
+        ("1x32", [32], table(20, 2, 32)),
+        ("32x1", [1] * 32, table(40, 2, 1)),
+        ("16x2", [2] * 16, table(30, 3, 2)),
+        ("3x5x7", [3, 5, 7], table(25, 4, 7)),
+    ]
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_edge_shapes_evaluate_search_replay(sat, torch, idx):
+    name, nodes, tab = _edge_instances()[idx]
+    c = oracle.compact(nodes, tab)
+    plan = sat.Plan(nodes, 0).load_runtime_table(tab)
+    cfg, perm = synth.random_genomes(c.S, 700, seed=idx)
+    ref = oracle.decode_batch(c, cfg, perm)
+    for decoder in (sat.DECODER_AUTO, sat.DECODER_WARP):
+        plan.set_decoder(decoder)
+        assert np.array_equal(_ms(plan, torch, cfg, perm), ref), (name, decoder)
+    plan.set_decoder(sat.DECODER_AUTO)
+    P, E, seed = 96, 4, 3 + idx
+    g_cfg, g_perm = oga.initial_population(c.S, P, seed)
+    g_ms = oracle.decode_batch(c, g_cfg, g_perm)
+    rc, rq, _ = oga.next_generation(c.S, g_cfg, g_perm, g_ms, 1, seed, 0, E, oga.q32(0.9), oga.q32(0.5),
+                                    oga.q32(0.5))
+    plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=1, elites=E, generations_per_epoch=1,
+                                 p_xover=0.9, p_cfg_mut=0.5, p_perm_mut=0.5))
+    gc, gq, gm = plan.search_population(P)
+    assert np.array_equal(gc, rc) and np.array_equal(gq, rq), name
+    assert np.array_equal(gm, oracle.decode_batch(c, rc, rq)), name
+    best, pl, bc, bp = plan.best_plan()
+    ms, opl = oracle.decode(c, bc, bp)
+    assert ms == best and oracle.validate(c, pl, best) == [], name
+    if c.n_jobs == 1:
+        r = plan.enumerate()
+        assert (r["makespan"], r["genome_index"]) == oracle.brute_force(c)
