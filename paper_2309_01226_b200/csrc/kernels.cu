@@ -275,7 +275,12 @@ static int grid_for(K kernel, int threads, size_t smem, int sms, int64_t work_bl
     // set for an earlier one.  Occupancy is still computed for this launch's smem.
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin > 0 ? optin : (int)smem);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kernel);
+    const int max_dyn = optin - (int)fa.sharedSizeBytes;   // dynamic + static <= opt-in maximum
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_dyn > (int)smem ? max_dyn : (int)smem) != cudaSuccess)
+      cudaGetLastError();  // leave no sticky error behind; the launch reports real problems
     occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     if (occ < 1) occ = 1;
