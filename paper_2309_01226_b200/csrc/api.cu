@@ -103,6 +103,8 @@ struct saturn_plan {
   int decoder = SATURN_DECODER_AUTO;
   DevBuf<uint8_t> blob;
   int blob_bytes = 0;
+  void* pinned = nullptr;     // pinned host staging for the table upload
+  size_t pinned_bytes = 0;
   Problem pb{};
   // workspaces
   DevBuf<uint8_t> ws_cfg, ws_perm;
@@ -309,8 +311,17 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
     }
   }
   if (p->device >= 0) {
+    // upload through a pinned staging buffer owned by the handle (true DMA, no bounce)
     CU(p, p->blob.ensure(bytes));
-    CU(p, cudaMemcpy(p->blob.p, blob.data(), bytes, cudaMemcpyHostToDevice));
+    if (p->pinned_bytes < (size_t)bytes) {
+      if (p->pinned) cudaFreeHost(p->pinned);
+      p->pinned = nullptr;
+      p->pinned_bytes = 0;
+      CU(p, cudaHostAlloc(&p->pinned, bytes, cudaHostAllocDefault));
+      p->pinned_bytes = bytes;
+    }
+    memcpy(p->pinned, blob.data(), bytes);
+    CU(p, cudaMemcpy(p->blob.p, p->pinned, bytes, cudaMemcpyHostToDevice));
     p->stats.h2d_bytes += bytes;
   }
   p->T = T;
@@ -1219,6 +1230,7 @@ void saturn_plan_destroy(saturn_plan* p) {
     DeviceGuard dg(p->device);
     if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
     p->blob.release();
+    if (p->pinned) cudaFreeHost(p->pinned);
     p->ws_cfg.release();
     p->ws_perm.release();
     p->ws_ms.release();
