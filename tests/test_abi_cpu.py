@@ -152,3 +152,17 @@ def test_compaction_order_matches_spec(lib):
         for t in range(0, inst.n_jobs, 7):
             for s in range(int(S[t])):
                 assert p.config(t, s) == c.config(t, s)
+
+
+def test_c_example_compiles_and_links(lib, tmp_path):
+    """examples/saturn_demo.c uses only include/saturn.h and links against libsaturn.so."""
+    import subprocess
+    exe = tmp_path / "saturn_demo"
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "saturn_demo.c"), "-L",
+                           os.path.dirname(sat.LIB_PATH), "-lsaturn", "-Wl,-rpath," + os.path.dirname(sat.LIB_PATH),
+                           "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    import torch
+    if not torch.cuda.is_available():
+        assert r.returncode == 2 and "saturn_plan_create" in r.stderr

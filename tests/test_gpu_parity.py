@@ -501,3 +501,19 @@ def test_edge_shapes_evaluate_search_replay(sat, torch, idx):
     if c.n_jobs == 1:
         r = plan.enumerate()
         assert (r["makespan"], r["genome_index"]) == oracle.brute_force(c)
+
+
+def test_c_example_runs_on_the_gpu(sat, torch, tmp_path):
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = tmp_path / "saturn_demo"
+    libdir = os.path.dirname(sat.LIB_PATH)
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "saturn_demo.c"), "-L", libdir, "-lsaturn",
+                           "-Wl,-rpath," + libdir, "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    opt = int(out.stdout.split("exhaustive optimum")[1].split("makespan ")[1].split()[0])
+    ga = int(out.stdout.split("GA search")[1].split("makespan ")[1].split()[0])
+    assert ga >= opt
