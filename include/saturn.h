@@ -53,7 +53,7 @@ typedef enum {
 } saturn_status;
 
 /* saturn_result.flags */
-enum { SATURN_PROVEN_OPTIMAL = 1, SATURN_INCUMBENT = 2 };
+enum { SATURN_PROVEN_OPTIMAL = 1, SATURN_INCUMBENT = 2, SATURN_PREFIX_SHARED = 4 };
 
 /* saturn_set_decoder kinds (row a5: two device designs, chosen by measurement) */
 enum { SATURN_DECODER_AUTO = 0, SATURN_DECODER_THREAD = 1, SATURN_DECODER_WARP = 2 };
@@ -79,6 +79,8 @@ typedef struct {
   double seconds;         /* wall time of the call                                      */
   int32_t flags;          /* SATURN_PROVEN_OPTIMAL (enumerate) | SATURN_INCUMBENT (search) */
   int32_t generations;    /* search: generations run                                    */
+  uint64_t leaves;        /* enumerate: leaves visited (prefix-shared DFS: after the
+                             branch-and-bound cut; these are not full decodes)          */
 } saturn_result;
 
 /* Genetic search parameters (row a7).  Probabilities are q32
@@ -170,7 +172,13 @@ saturn_status saturn_space_size(const saturn_plan *p, uint64_t *size);
  * max_genomes or 2^38, or T > 20.  flags = SATURN_PROVEN_OPTIMAL.  Synchronous. */
 saturn_status saturn_enumerate(saturn_plan *p, uint64_t max_genomes, void *stream, saturn_result *out);
 
-/* Enumerate only genome indices [begin, end) on this device (no collective). */
+/* saturn_enumerate runs a depth-first enumeration with prefix sharing and a strict
+ * branch-and-bound cut (incumbent = the best paper-baseline genome) when T >= 3 and the
+ * cluster has a register decoder shape (flags |= SATURN_PREFIX_SHARED; `evaluated` = the
+ * genomes accounted for, `leaves` = leaves actually visited); the result is identical to
+ * the index-order brute force.  SATURN_ENUM_ODOMETER=1 forces full decodes in index order.
+ *
+ * Enumerate only genome indices [begin, end) on this device (no collective; full decodes). */
 saturn_status saturn_enumerate_range(saturn_plan *p, uint64_t begin, uint64_t end, void *stream,
                                      saturn_result *out);
 

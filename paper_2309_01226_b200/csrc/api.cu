@@ -544,6 +544,7 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
   if (out) {
     memset(out, 0, sizeof *out);
     out->evaluated = collective ? total : (end - begin);
+    out->leaves = out->evaluated;
     out->seconds = now_s() - t0;
     out->flags = SATURN_PROVEN_OPTIMAL;
   }
@@ -565,6 +566,79 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
 
 }  // namespace
 
+// Full-space enumeration with the DFS kernel: roots partitioned over ranks, incumbent seeded
+// with the best paper-baseline genome (any valid genome's makespan >= OPT, so the strict cut
+// keeps every optimal leaf and the smallest-index tie-break stays exact).
+static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStream_t st, saturn_result* out) {
+  const double t0 = now_s();
+  const int T = p->T;
+  sat::DfsSpace ds{};
+  ds.es.cfg_space = 1;
+  for (int t = 0; t < T; ++t) {
+    ds.es.radix[t] = ds.es.cfg_space;
+    ds.es.cfg_space *= (uint64_t)p->S[t];
+  }
+  ds.es.fact[0] = 1;
+  for (int k = 1; k <= T; ++k) ds.es.fact[k] = ds.es.fact[k - 1] * (uint64_t)k;
+  ds.pre[0] = 0;
+  for (int t = 0; t < T; ++t) ds.pre[t + 1] = ds.pre[t] + p->S[t];
+  ds.sumS = ds.pre[T];
+  // root depth: enough roots to fill the GPU (~32 per SM-thread slot), at most T - 1 levels
+  ds.D = 1;
+  ds.n_roots = (uint64_t)ds.sumS;
+  const uint64_t want = (uint64_t)p->sms * 64 * 16;
+  while (ds.D < T - 1 && ds.n_roots < want && ds.n_roots * (uint64_t)ds.sumS < (uint64_t(1) << 40)) {
+    ds.n_roots *= (uint64_t)ds.sumS;
+    ++ds.D;
+  }
+  // incumbent from the paper's baselines (row f2)
+  int32_t inc = (int32_t)((1 << 26) - 1);
+  {
+    std::vector<uint8_t> c(4 * T), q(4 * T);
+    for (int k = 0; k < 4; ++k) {
+      saturn_status sb = saturn_baseline_genome(p, k + 1, 0, &c[k * T], &q[k * T]);
+      if (sb != SATURN_OK) return sb;
+    }
+    int32_t ms[4];
+    saturn_status se = saturn_evaluate_host(p, c.data(), q.data(), 4, ms, st);
+    if (se != SATURN_OK) return se;
+    for (int k = 0; k < 4; ++k)
+      if (ms[k] > 0) inc = std::min(inc, ms[k]);
+  }
+  const unsigned long long init = ((unsigned long long)inc << 38) | ((1ull << 38) - 1ull);
+  CU(p, p->ws_key.ensure(2));
+  CU(p, cudaMemcpyAsync(p->ws_key.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
+  CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, sizeof(unsigned long long), st));
+  uint64_t rb = 0, re = ds.n_roots;
+  saturn_partition(ds.n_roots, p->rank, p->world, &rb, &re);
+  CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st));
+  p->stats.kernel_launches += 1;
+  if (p->comm && p->world > 1) {
+    NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
+    NC(p, nccl().allReduce(p->ws_key.p + 1, p->ws_key.p + 1, 1, ncclUint64, ncclSum, p->comm, st));
+  }
+  unsigned long long kl[2] = {0, 0};
+  CU(p, cudaMemcpyAsync(kl, p->ws_key.p, sizeof kl, cudaMemcpyDeviceToHost, st));
+  CU(p, cudaStreamSynchronize(st));
+  p->stats.d2h_bytes += sizeof kl;
+  const uint64_t idx = kl[0] & ((uint64_t(1) << 38) - 1);
+  if (idx == (uint64_t(1) << 38) - 1) return fail(p, SATURN_ECUDA, "enumeration found no leaf");
+  const int64_t ms = (int64_t)(kl[0] >> 38);
+  unrank_host(p, idx, p->best_cfg, p->best_perm);
+  p->best_ms = ms;
+  p->have_best = true;
+  if (out) {
+    memset(out, 0, sizeof *out);
+    out->makespan = ms;
+    out->genome_index = idx;
+    out->evaluated = total;
+    out->leaves = kl[1];
+    out->seconds = now_s() - t0;
+    out->flags = SATURN_PROVEN_OPTIMAL | SATURN_PREFIX_SHARED;
+  }
+  return SATURN_OK;
+}
+
 saturn_status saturn_enumerate(saturn_plan* p, uint64_t max_genomes, void* stream, saturn_result* out) {
   if (!p) return SATURN_EINVAL;
   if (!p->loaded) return fail(p, SATURN_ESTATE, "enumerate before load_runtime_table");
@@ -576,6 +650,12 @@ saturn_status saturn_enumerate(saturn_plan* p, uint64_t max_genomes, void* strea
     return fail(p, SATURN_ELIMIT, "genome space %llu exceeds max_genomes %llu", (unsigned long long)size,
                 (unsigned long long)max_genomes);
   DeviceGuard dg(p->device);
+  int kind;
+  saturn_status s0 = use_decoder_kind(p, &kind);
+  if (s0 != SATURN_OK) return s0;
+  const char* env = getenv("SATURN_ENUM_ODOMETER");
+  if (p->T >= 3 && p->NN >= 1 && !(env && env[0] == '1'))
+    return enumerate_dfs_impl(p, size, static_cast<cudaStream_t>(stream), out);
   uint64_t b = 0, e = size;
   saturn_partition(size, p->rank, p->world, &b, &e);
   return enumerate_impl(p, b, e, size, true, static_cast<cudaStream_t>(stream), out);

@@ -474,6 +474,220 @@ cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace&
   return cudaErrorInvalidConfiguration;
 }
 
+// ------------------------------------------------------------------ K2b: DFS enumeration
+constexpr int DFS_B = 64;
+// per-level thread-private words: state (NN*GP), ms, rperm lo/hi, rcfg lo/hi, used, t, c
+template <int NN, int GP>
+struct DfsLayout {
+  static constexpr int W = NN * GP + 8;
+};
+
+static size_t dfs_smem_bytes(const Problem& pb, int NN, int GP) {
+  return (size_t)pb.blob_bytes + (size_t)4 * pb.T * (NN * GP + 8) * DFS_B + 32 * 8 + 8;
+}
+
+template <int NN, int GP>
+__device__ __forceinline__ int start_of(const int (&a)[NN][GP], int g) {
+  int best = mux<GP>(a[0], g - 1);
+#pragma unroll
+  for (int n = 1; n < NN; ++n) best = min(best, mux<GP>(a[n], g - 1));
+  return best;
+}
+
+// place (g, R) on the cluster state a (greedy node, lowest id on ties); returns s + R
+template <int NN, int GP>
+__device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R) {
+  if constexpr (NN == 1) {
+    return place_sorted<GP>(a[0], g, R);
+  } else {
+    int best = mux<GP>(a[0], g - 1);
+    int bn = 0;
+#pragma unroll
+    for (int n = 1; n < NN; ++n) {
+      const int st = mux<GP>(a[n], g - 1);
+      const bool lt = st < best;
+      best = lt ? st : best;
+      bn = lt ? n : bn;
+    }
+    int x[GP];
+#pragma unroll
+    for (int i = 0; i < GP; ++i) {
+      int y = a[0][i];
+#pragma unroll
+      for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
+      x[i] = y;
+    }
+    const int v = place_sorted<GP>(x, g, R);
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+#pragma unroll
+      for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
+    return v;
+  }
+}
+
+template <int NN, int GP>
+__global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds, uint64_t root_begin,
+                                                         uint64_t root_end, unsigned long long* best_key,
+                                                         unsigned long long* leaves_out) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint8_t* s_blob = sm;
+  int* s_lv = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  const int T = pb.T;
+  constexpr int W = DfsLayout<NN, GP>::W;
+  uint64_t* s_red = reinterpret_cast<uint64_t*>(s_lv + (size_t)T * W * DFS_B);
+  uint64_t* bar = s_red + 32;
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  const int tid = threadIdx.x;
+  auto LV = [&](int level, int w) -> int& { return s_lv[((size_t)level * W + w) * DFS_B + tid]; };
+  const uint32_t full = (T == 32) ? 0xffffffffu : ((1u << T) - 1u);
+  const uint64_t C = ds.es.cfg_space;
+
+  uint64_t best = ~0ull, leaves = 0;
+  for (uint64_t root = root_begin + (uint64_t)blockIdx.x * DFS_B + tid; root < root_end;
+       root += (uint64_t)gridDim.x * DFS_B) {
+    const int inc = (int)(*reinterpret_cast<volatile unsigned long long*>(best_key) >> 38);
+    const int inc_ms = min(inc, (int)(best >> 38));
+    int a[NN][GP];
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+#pragma unroll
+      for (int i = 0; i < GP; ++i) a[n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
+    int ms = 0;
+    uint32_t used = 0;
+    uint64_t rperm = 0, rcfg = 0;
+    uint64_t rr = root;
+    bool ok = true;
+    for (int i = 0; i < ds.D && ok; ++i) {  // decode and place the root's prefix
+      const int pi = (int)(rr % (uint64_t)ds.sumS);
+      rr /= (uint64_t)ds.sumS;
+      int t = 0;
+      while (ds.pre[t + 1] <= pi) ++t;
+      const int c = pi - ds.pre[t];
+      if (used & (1u << t)) { ok = false; break; }
+      const uint32_t w = tab[t * pb.stride + c];
+      ms = max(ms, place_T<NN, GP>(a, (int)(w >> 24), (int)(w & R_MASK)));
+      rperm += (uint64_t)__popc(~used & full & ((1u << t) - 1u)) * ds.es.fact[T - 1 - i];
+      rcfg += (uint64_t)c * ds.es.radix[t];
+      used |= 1u << t;
+      if (ms > inc_ms) ok = false;
+    }
+    if (!ok) continue;
+    // DFS over levels D .. T-1; level L's saved state = the cluster after L placements
+    int level = ds.D;
+    int tc = -1, cc = 0;  // iterator at the current level
+    while (true) {
+      if (level == T - 1) {  // last position: closed form for every config of the last job
+        const int t = __ffs(~used & full) - 1;
+        const uint64_t base = rperm * C + rcfg;
+        for (int c = 0; c < S[t]; ++c) {
+          const uint32_t w = tab[t * pb.stride + c];
+          const int leaf = max(ms, start_of<NN, GP>(a, (int)(w >> 24)) + (int)(w & R_MASK));
+          const uint64_t key = ((uint64_t)leaf << 38) | (base + (uint64_t)c * ds.es.radix[t]);
+          best = key < best ? key : best;
+        }
+        leaves += (uint64_t)S[t];
+        if (level == ds.D) break;
+        // backtrack to the parent level
+        --level;
+        goto restore;
+      }
+      // next (job, config) candidate at this level among the unplaced jobs
+      if (tc >= 0 && cc + 1 < S[tc]) {
+        ++cc;
+      } else {
+        const uint32_t rem = ~used & full & (tc >= 0 ? ~((2u << tc) - 1u) : full);
+        if (rem == 0) {  // level exhausted
+          if (level == ds.D) break;
+          --level;
+          goto restore;
+        }
+        tc = __ffs(rem) - 1;
+        cc = 0;
+      }
+      {
+        const uint32_t w = tab[tc * pb.stride + cc];
+        int b[NN][GP];
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int i = 0; i < GP; ++i) b[n][i] = a[n][i];
+        const int ms2 = max(ms, place_T<NN, GP>(b, (int)(w >> 24), (int)(w & R_MASK)));
+        if (ms2 > inc_ms) continue;  // strict cut: no leaf below can reach the incumbent
+        // save this level and descend
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int i = 0; i < GP; ++i) LV(level, n * GP + i) = a[n][i];
+        LV(level, NN * GP + 0) = ms;
+        LV(level, NN * GP + 1) = (int)(uint32_t)rperm;
+        LV(level, NN * GP + 2) = (int)(uint32_t)(rperm >> 32);
+        LV(level, NN * GP + 3) = (int)(uint32_t)rcfg;
+        LV(level, NN * GP + 4) = (int)(uint32_t)(rcfg >> 32);
+        LV(level, NN * GP + 5) = (int)used;
+        LV(level, NN * GP + 6) = tc;
+        LV(level, NN * GP + 7) = cc;
+        rperm += (uint64_t)__popc(~used & full & ((1u << tc) - 1u)) * ds.es.fact[T - 1 - level];
+        rcfg += (uint64_t)cc * ds.es.radix[tc];
+        used |= 1u << tc;
+        ms = ms2;
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+#pragma unroll
+          for (int i = 0; i < GP; ++i) a[n][i] = b[n][i];
+        ++level;
+        tc = -1;
+        cc = 0;
+        continue;
+      }
+    restore:
+#pragma unroll
+      for (int n = 0; n < NN; ++n)
+#pragma unroll
+        for (int i = 0; i < GP; ++i) a[n][i] = LV(level, n * GP + i);
+      ms = LV(level, NN * GP + 0);
+      rperm = (uint64_t)(uint32_t)LV(level, NN * GP + 1) | ((uint64_t)(uint32_t)LV(level, NN * GP + 2) << 32);
+      rcfg = (uint64_t)(uint32_t)LV(level, NN * GP + 3) | ((uint64_t)(uint32_t)LV(level, NN * GP + 4) << 32);
+      used = (uint32_t)LV(level, NN * GP + 5);
+      tc = LV(level, NN * GP + 6);
+      cc = LV(level, NN * GP + 7);
+    }
+  }
+  best = warp_min_u64(best);
+  const int lane = tid & 31, warp = tid >> 5;
+  if (lane == 0) s_red[warp] = best;
+  for (int m = 16; m >= 1; m >>= 1) leaves += __shfl_xor_sync(0xffffffffu, leaves, m);
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t b2 = s_red[0];
+    for (int w = 1; w < DFS_B / 32; ++w) b2 = s_red[w] < b2 ? s_red[w] : b2;
+    if (b2 != ~0ull) atomicMin(best_key, (unsigned long long)b2);
+  }
+  if (lane == 0 && leaves) atomicAdd(leaves_out, (unsigned long long)leaves);
+}
+
+cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
+                                 uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,
+                                 int sms, cudaStream_t st) {
+  if (root_end <= root_begin) return cudaSuccess;
+  const size_t smem = dfs_smem_bytes(pb, NN, GP);
+  const uint64_t total = root_end - root_begin;
+#define SAT_DFS(a, b)                                                                              \
+  if (NN == a && GP == b && a >= 1) {                                                              \
+    constexpr int A_ = (a >= 1 ? a : 1);                                                           \
+    const int g0 = grid_for(k_enumerate_dfs<A_, b>, DFS_B, smem, sms, 1 << 30);                    \
+    const uint64_t need = (total + DFS_B - 1) / DFS_B;                                             \
+    const int g = (int)(need < (uint64_t)g0 ? need : (uint64_t)g0);                                \
+    k_enumerate_dfs<A_, b><<<g, DFS_B, smem, st>>>(pb, ds, root_begin, root_end, best_key, leaves); \
+    return cudaGetLastError();                                                                     \
+  }
+  SAT_SHAPES(SAT_DFS)
+#undef SAT_DFS
+  return cudaErrorInvalidConfiguration;
+}
+
 // ------------------------------------------------------------------ K3 (+K1): GA
 // Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
 // then parent B, then the OX1 slice bit set for T > 32 (8 words, interleaved per thread).

@@ -37,6 +37,24 @@ struct EnumSpace {
 cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace& es, uint64_t begin,
                              uint64_t end, unsigned long long* best_key, int sms, cudaStream_t st);
 
+// Depth-first enumeration with prefix sharing and strict branch-and-bound (a4-ii): roots
+// fix the (job, config) choices of the first D priority positions (a mixed-radix index over
+// sum_t S_t pairs per level; roots repeating a job are skipped); below a root every prefix
+// state is computed once and the last position is evaluated in closed form (g-th smallest
+// start + R), so a leaf costs a few instructions instead of a T-step decode.  Leaf indices
+// are exact, and only subtrees whose partial makespan exceeds the incumbent are cut, so the
+// result is the same (makespan, smallest index) as the index-order brute force.
+struct DfsSpace {
+  EnumSpace es;
+  int pre[ENUM_MAX_T + 1];   // prefix sums of S_t: pair index -> (job, config)
+  int sumS;
+  int D;                     // root depth
+  uint64_t n_roots;          // sumS^D
+};
+cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
+                                 uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,
+                                 int sms, cudaStream_t st);
+
 struct GaParams {
   uint64_t seed;
   uint32_t rank;

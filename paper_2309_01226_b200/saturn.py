@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libsaturn.so")
 
 OK, EINVAL, EUNSCHEDULABLE, ELIMIT, ECUDA, ENCCL, ESTATE = range(7)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EUNSCHEDULABLE", 3: "ELIMIT", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
-PROVEN_OPTIMAL, INCUMBENT = 1, 2
+PROVEN_OPTIMAL, INCUMBENT, PREFIX_SHARED = 1, 2, 4
 DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
 
 # Every symbol declared in include/saturn.h.
@@ -53,7 +53,8 @@ PLACEMENT_DTYPE = np.dtype([("node", "<i4"), ("upp", "<i4"), ("gpus", "<i4"), ("
 
 class Result(ctypes.Structure):
     _fields_ = [("makespan", ctypes.c_int64), ("genome_index", ctypes.c_uint64), ("evaluated", ctypes.c_uint64),
-                ("seconds", ctypes.c_double), ("flags", ctypes.c_int32), ("generations", ctypes.c_int32)]
+                ("seconds", ctypes.c_double), ("flags", ctypes.c_int32), ("generations", ctypes.c_int32),
+                ("leaves", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -329,7 +330,7 @@ class Plan:
                     "saturn_trace")
         return pl, ms
 
-    def enumerate(self, max_genomes: int = 1 << 34, stream=None) -> dict:
+    def enumerate(self, max_genomes: int = (1 << 38) - 1, stream=None) -> dict:
         r = Result()
         self._check(self._lib.saturn_enumerate(self._h, int(max_genomes), self._stream(stream), ctypes.byref(r)),
                     "saturn_enumerate")
@@ -465,7 +466,7 @@ def evaluate(plan: Plan, cfg, perm, out=None, stream=None):
     return plan.evaluate(cfg, perm, out, stream)
 
 
-def enumerate(plan: Plan, max_genomes: int = 1 << 34, stream=None):  # noqa: A001
+def enumerate(plan: Plan, max_genomes: int = (1 << 38) - 1, stream=None):  # noqa: A001
     return plan.enumerate(max_genomes, stream)
 
 

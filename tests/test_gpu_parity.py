@@ -164,7 +164,7 @@ def test_enumerate_tiny_matches_brute_force(sat, torch):
         c = oracle.compact(inst.node_gpus, inst.runtime)
         r = plan.enumerate()
         assert (r["makespan"], r["genome_index"]) == oracle.brute_force(c)
-        assert r["evaluated"] == 1296 and r["flags"] == sat.PROVEN_OPTIMAL
+        assert r["evaluated"] == 1296 and r["flags"] & sat.PROVEN_OPTIMAL
         best, pl, bc, bp = plan.best_plan()
         ms, opl = oracle.decode(c, bc, bp)
         assert ms == best == r["makespan"]
@@ -517,3 +517,21 @@ def test_c_example_runs_on_the_gpu(sat, torch, tmp_path):
     opt = int(out.stdout.split("exhaustive optimum")[1].split("makespan ")[1].split()[0])
     ga = int(out.stdout.split("GA search")[1].split("makespan ")[1].split()[0])
     assert ga >= opt
+
+
+
+def test_dfs_enumeration_equals_index_order_enumeration(sat, torch):
+    """The prefix-sharing branch-and-bound DFS (saturn_enumerate) returns exactly the
+    (makespan, smallest index) of the full-decode index-order kernel on the whole space."""
+    cases = [synth.tiny_variant(7, 7, (4,)), synth.tiny_variant(8, 6, (2, 2)), synth.tiny_variant(9, 5, (4,)),
+             synth.tiny_variant(3, 8, (4,))]
+    for inst in cases:
+        plan = _plan(sat, inst)
+        N = plan.space_size()
+        dfs = plan.enumerate()
+        assert dfs["flags"] & sat.PREFIX_SHARED and dfs["evaluated"] == N and 0 < dfs["leaves"] <= N
+        full = plan.enumerate_range(0, N)
+        assert (dfs["makespan"], dfs["genome_index"]) == (full["makespan"], full["genome_index"]), inst.name
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        cfg, perm = oracle.unrank(c, dfs["genome_index"])
+        assert oracle.decode(c, cfg, perm)[0] == dfs["makespan"]
