@@ -328,13 +328,18 @@ def main():
         tv = synth.tiny_variant(7, 7, (4,))
         ep = sat.Plan(tv.node_gpus, local).load_runtime_table(tv.runtime)
         ep.enumerate()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        er = ep.enumerate()
-        b.record()
-        torch.cuda.synchronize()
-        kernel_only["enumerate"] = {"genomes": er["evaluated"], "plans_per_s": er["evaluated"] / (a.elapsed_time(b) * 1e-3),
-                                    "optimum": er["makespan"], "instance": "TINY-shaped 7 jobs on 1x4 (seed 7)"}
+        t0 = time.perf_counter()
+        er = ep.enumerate()                      # DFS, prefix sharing + branch and bound
+        t_dfs = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fr = ep.enumerate_range(0, er["evaluated"])   # index order, one full decode per genome
+        t_full = time.perf_counter() - t0
+        kernel_only["enumerate"] = {
+            "instance": "TINY-shaped 7 jobs on 1x4 (seed 7)", "genomes": er["evaluated"], "optimum": er["makespan"],
+            "full_decode_plans_per_s": fr["evaluated"] / t_full,
+            "dfs_seconds": t_dfs, "dfs_leaves": er["leaves"], "dfs_leaves_per_s": er["leaves"] / t_dfs,
+            "dfs_genomes_covered_per_s": er["evaluated"] / t_dfs,
+            "same_result": (er["makespan"], er["genome_index"]) == (fr["makespan"], fr["genome_index"])}
         kernel_only["unit"] = UNIT
         kernel_only["genomes"] = n
         kernel_only["int_probe_ops_per_s"] = plan.probe_int_peak()
