@@ -118,7 +118,7 @@ saturn_status saturn_plan_create(const int32_t *node_gpus, int32_t n_nodes, int3
  * The table is compacted (row a2): job t's configs are its feasible entries with
  * g <= max_n GPU_n (single-node jobs) in UPP-major, ascending-g order
  * (SPEC.md:52); config index s in genomes and placements refers to this order.
- * EINVAL: n_jobs not in [1,255], n_upps < 1, max_gpus < 1, R >= 2^24, sum_t max_s R >= 2^26,
+ * EINVAL: n_jobs not in [1,255], n_upps not in [1,255], max_gpus < 1, R >= 2^24, sum_t max_s R >= 2^26,
  * > 255 configs for a job; EUNSCHEDULABLE: a job with no feasible config (message names it);
  * ELIMIT: packed table > 48 KB.  Replaces any previous table and search state. */
 saturn_status saturn_load_runtime_table(saturn_plan *p, const int32_t *runtime_s, int32_t n_jobs,
@@ -190,6 +190,16 @@ saturn_status saturn_enumerate_range(saturn_plan *p, uint64_t begin, uint64_t en
  * global best E.  Deterministic for fixed (params, world size).  flags = SATURN_INCUMBENT.
  * Synchronous.  EINVAL for bad params; ESTATE without a table. */
 saturn_status saturn_search(saturn_plan *p, const saturn_search_params *sp, void *stream, saturn_result *out);
+
+/* Several islands in one process (row e without NCCL): plans[0..k) -- handles with the same
+ * cluster and table, on one or several devices, no communicator -- run saturn_search in
+ * lock-step as islands 0..k-1 (the Philox rank id of island r is r) and exchange their
+ * elite records every epoch by device-to-device copies (cudaMemcpyPeer), then every island
+ * continues from the global best E -- exactly the NCCL island protocol of saturn_search with
+ * world = k.  streams: k caller streams or NULL.  out: k results (evaluated = all islands).
+ * Synchronous.  EINVAL for mismatched handles, ESTATE for host-only or attached handles. */
+saturn_status saturn_search_group(saturn_plan **plans, int32_t k, const saturn_search_params *sp, void **streams,
+                                  saturn_result *out);
 
 /* Best-so-far curve of the last search: up to n_max (seconds since the call, makespan)
  * pairs, one per epoch; *n_out = number written. */

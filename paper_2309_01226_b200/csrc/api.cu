@@ -255,7 +255,7 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   if (!p) return SATURN_EINVAL;
   if (!runtime_s) return fail(p, SATURN_EINVAL, "runtime_s is NULL");
   if (n_jobs < 1 || n_jobs > sat::MAX_JOBS) return fail(p, SATURN_EINVAL, "n_jobs=%d not in [1,255]", n_jobs);
-  if (n_upps < 1) return fail(p, SATURN_EINVAL, "n_upps=%d < 1", n_upps);
+  if (n_upps < 1 || n_upps > 255) return fail(p, SATURN_EINVAL, "n_upps=%d not in [1,255]", n_upps);
   if (max_gpus < 1) return fail(p, SATURN_EINVAL, "max_gpus=%d < 1", max_gpus);
   p->loaded = false;
   p->have_best = false;
@@ -675,116 +675,110 @@ saturn_status saturn_enumerate_range(saturn_plan* p, uint64_t begin, uint64_t en
   return enumerate_impl(p, begin, end, size, false, static_cast<cudaStream_t>(stream), out);
 }
 
-saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out) {
-  if (p && host_only(p)) return SATURN_ESTATE;
-  if (!p) return SATURN_EINVAL;
-  if (!p->loaded) return fail(p, SATURN_ESTATE, "search before load_runtime_table");
-  if (!sp) return fail(p, SATURN_EINVAL, "params is NULL");
-  const int64_t P = sp->population;
-  const int E = sp->elites;
-  if (E < 1 || E > 32) return fail(p, SATURN_EINVAL, "elites=%d not in [1,32]", E);
-  if (P < 64 || P < 2 * E || P > (int64_t(1) << 31) - 1)
-    return fail(p, SATURN_EINVAL, "population=%lld must be in [max(64, 2*elites), 2^31)", (long long)P);
-  if (sp->max_generations < 0) return fail(p, SATURN_EINVAL, "max_generations < 0");
-  if (sp->generations_per_epoch < 1) return fail(p, SATURN_EINVAL, "generations_per_epoch < 1");
-  if (sp->n_seed < 0 || (sp->n_seed > 0 && (!sp->seed_cfg || !sp->seed_perm)))
-    return fail(p, SATURN_EINVAL, "bad seed genomes");
-  if (!p->sorted_ok) return fail(p, SATURN_EINVAL, "search needs the thread decoder for this cluster shape");
-  const int T = p->T;
-  const int GS = gs_of(T);
-  for (int64_t i = 0; i < sp->n_seed; ++i) {  // seed genomes must be valid
-    std::vector<int> seen(T, 0);
-    for (int k = 0; k < T; ++k) {
-      const int t = sp->seed_perm[i * T + k];
-      if (t >= T || seen[t]++) return fail(p, SATURN_EINVAL, "seed genome %lld: perm is not a permutation", (long long)i);
-      if (sp->seed_cfg[i * T + t] >= p->S[t]) return fail(p, SATURN_EINVAL, "seed genome %lld: cfg out of range", (long long)i);
-    }
-  }
-  DeviceGuard dg(p->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const double t0 = now_s();
-  for (int b = 0; b < 2; ++b) {
-    CU(p, p->pop[b].ensure((size_t)P * GS));
-    CU(p, p->pms[b].ensure((size_t)P));
-  }
-  CU(p, p->cand.ensure((size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64));
-  CU(p, p->n_cand.ensure(1));
-  CU(p, cudaMemsetAsync(p->n_cand.p, 0, sizeof(int), st));
-  CU(p, p->rec_ms.ensure(E));
-  CU(p, p->rec_gen.ensure((size_t)E * GS));
-  CU(p, p->all_ms.ensure((size_t)E * p->world));
-  CU(p, p->all_gen.ensure((size_t)E * GS * p->world));
-  const int64_t n_seed = std::min<int64_t>(sp->n_seed, P);
-  if (n_seed > 0) {
-    std::vector<uint8_t> packed((size_t)n_seed * GS, 0);
-    for (int64_t i = 0; i < n_seed; ++i) {
-      memcpy(&packed[i * GS], sp->seed_cfg + i * T, T);
-      memcpy(&packed[i * GS + sat::perm_offset(T)], sp->seed_perm + i * T, T);
-    }
-    CU(p, p->seeds.ensure(packed.size()));
-    CU(p, cudaMemcpyAsync(p->seeds.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
-    p->stats.h2d_bytes += (int64_t)packed.size();
-  }
+namespace {
+
+// One GA island's search state (row a7 + e).  saturn_search drives one island per process
+// (exchanging elites over NCCL when a communicator is attached); saturn_search_group drives
+// several islands in lock-step in one process and exchanges by device copies -- the same
+// algorithm, so the island protocol is testable on one GPU.
+struct Island {
+  saturn_plan* p = nullptr;
+  const saturn_search_params* sp = nullptr;
+  cudaStream_t st = nullptr;
+  uint32_t island = 0;      // Philox rank id of this island
+  int world = 1;            // number of islands in the exchange
+  int64_t P = 0;
+  int E = 0, GS = 0, T = 0;
   sat::GaParams gp{};
-  gp.seed = sp->seed;
-  gp.rank = (uint32_t)p->rank;
-  gp.gen = 0;
-  gp.P = P;
-  gp.E = E;
-  gp.GS = GS;
-  gp.px = sp->p_xover_q32;
-  gp.pc = sp->p_cfg_mut_q32;
-  gp.pm = sp->p_perm_mut_q32;
-  uint64_t evaluated = (uint64_t)P;
-  CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p, p->pms[0].p,
-                            p->cand.p, p->n_cand.p, p->sms, st));
-  CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
-  p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
-  // profiling: event pairs around the GA generation kernels (first 512 per search)
-  const int64_t n_prof = p->profiling ? std::min<int64_t>(sp->max_generations, 512) : 0;
-  while ((int64_t)p->ev_pool.size() < 3 * n_prof) {
-    cudaEvent_t e;
-    CU(p, cudaEventCreate(&e));
-    p->ev_pool.push_back(e);
+  uint64_t evaluated = 0;
+  int cur = 0;
+  int64_t n_prof = 0;
+  double t0 = 0;
+
+  saturn_status validate() {
+    if (!p->loaded) return fail(p, SATURN_ESTATE, "search before load_runtime_table");
+    if (!sp) return fail(p, SATURN_EINVAL, "params is NULL");
+    P = sp->population;
+    E = sp->elites;
+    if (E < 1 || E > 32) return fail(p, SATURN_EINVAL, "elites=%d not in [1,32]", E);
+    if (P < 64 || P < 2 * E || P > (int64_t(1) << 31) - 1)
+      return fail(p, SATURN_EINVAL, "population=%lld must be in [max(64, 2*elites), 2^31)", (long long)P);
+    if (sp->max_generations < 0) return fail(p, SATURN_EINVAL, "max_generations < 0");
+    if (sp->generations_per_epoch < 1) return fail(p, SATURN_EINVAL, "generations_per_epoch < 1");
+    if (sp->n_seed < 0 || (sp->n_seed > 0 && (!sp->seed_cfg || !sp->seed_perm)))
+      return fail(p, SATURN_EINVAL, "bad seed genomes");
+    if (!p->sorted_ok) return fail(p, SATURN_EINVAL, "search needs the thread decoder for this cluster shape");
+    T = p->T;
+    GS = gs_of(T);
+    for (int64_t i = 0; i < sp->n_seed; ++i) {  // seed genomes must be valid
+      std::vector<int> seen(T, 0);
+      for (int k = 0; k < T; ++k) {
+        const int t = sp->seed_perm[i * T + k];
+        if (t >= T || seen[t]++)
+          return fail(p, SATURN_EINVAL, "seed genome %lld: perm is not a permutation", (long long)i);
+        if (sp->seed_cfg[i * T + t] >= p->S[t])
+          return fail(p, SATURN_EINVAL, "seed genome %lld: cfg out of range", (long long)i);
+      }
+    }
+    return SATURN_OK;
   }
 
-  saturn_status s0 = SATURN_OK;
-  // memetic step (row f4): improve the E elites, then re-sort them by (ms, position)
-  auto memetic = [&]() -> saturn_status {
-    if (sp->local_search_iters <= 0) return SATURN_OK;
-    CU(p, cudaMemcpyAsync(p->all_ms.p, p->rec_ms.p, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-    CU(p, cudaMemcpyAsync(p->all_gen.p, p->rec_gen.p, (size_t)E * GS, cudaMemcpyDeviceToDevice, st));
-    CU(p, sat::launch_local_search(p->pb, p->NN, p->GP, p->all_gen.p, p->all_ms.p, E, GS, sp->local_search_iters, st));
-    CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, 1, E, GS, p->rec_ms.p, p->rec_gen.p, st));
-    p->stats.kernel_launches += 2;
+  // buffers + generation 0 (seed genomes, then Philox genomes) + the first elite selection
+  saturn_status begin() {
+    DeviceGuard dg(p->device);
+    t0 = now_s();
+    for (int b = 0; b < 2; ++b) {
+      CU(p, p->pop[b].ensure((size_t)P * GS));
+      CU(p, p->pms[b].ensure((size_t)P));
+    }
+    CU(p, p->cand.ensure((size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64));
+    CU(p, p->n_cand.ensure(1));
+    CU(p, cudaMemsetAsync(p->n_cand.p, 0, sizeof(int), st));
+    CU(p, p->rec_ms.ensure(E));
+    CU(p, p->rec_gen.ensure((size_t)E * GS));
+    CU(p, p->all_ms.ensure((size_t)E * world));
+    CU(p, p->all_gen.ensure((size_t)E * GS * world));
+    const int64_t n_seed = std::min<int64_t>(sp->n_seed, P);
+    if (n_seed > 0) {
+      std::vector<uint8_t> packed((size_t)n_seed * GS, 0);
+      for (int64_t i = 0; i < n_seed; ++i) {
+        memcpy(&packed[i * GS], sp->seed_cfg + i * T, T);
+        memcpy(&packed[i * GS + sat::perm_offset(T)], sp->seed_perm + i * T, T);
+      }
+      CU(p, p->seeds.ensure(packed.size()));
+      CU(p, cudaMemcpyAsync(p->seeds.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
+      p->stats.h2d_bytes += (int64_t)packed.size();
+    }
+    gp = sat::GaParams{};
+    gp.seed = sp->seed;
+    gp.rank = island;
+    gp.gen = 0;
+    gp.P = P;
+    gp.E = E;
+    gp.GS = GS;
+    gp.px = sp->p_xover_q32;
+    gp.pc = sp->p_cfg_mut_q32;
+    gp.pm = sp->p_perm_mut_q32;
+    evaluated = (uint64_t)P;
+    cur = 0;
+    CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p,
+                              p->pms[0].p, p->cand.p, p->n_cand.p, p->sms, st));
+    CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
+    p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
+    // profiling: event triples around the GA generation kernels (first 512 per search)
+    n_prof = p->profiling ? std::min<int64_t>(sp->max_generations, 512) : 0;
+    while ((int64_t)p->ev_pool.size() < 3 * n_prof) {
+      cudaEvent_t e;
+      CU(p, cudaEventCreate(&e));
+      p->ev_pool.push_back(e);
+    }
+    p->hist_t.clear();
+    p->hist_ms.clear();
     return SATURN_OK;
-  };
-  auto exchange = [&]() -> saturn_status {
-    if ((s0 = memetic()) != SATURN_OK) return s0;
-    if (!p->comm || p->world < 2) return SATURN_OK;
-    NC(p, nccl().allGather(p->rec_ms.p, p->all_ms.p, (size_t)E, ncclInt32, p->comm, st));
-    NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
-    CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, p->world, E, GS, p->rec_ms.p, p->rec_gen.p, st));
-    p->stats.kernel_launches += 1;
-    return SATURN_OK;
-  };
-  p->hist_t.clear();
-  p->hist_ms.clear();
-  auto record = [&]() -> saturn_status {
-    int32_t best = 0;
-    CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
-    CU(p, cudaStreamSynchronize(st));
-    p->stats.d2h_bytes += sizeof best;
-    p->hist_t.push_back(now_s() - t0);
-    p->hist_ms.push_back(best);
-    return SATURN_OK;
-  };
-  saturn_status s;
-  if ((s = exchange()) != SATURN_OK) return s;
-  if ((s = record()) != SATURN_OK) return s;
-  int cur = 0;
-  int64_t gen = 1;
-  for (; gen <= sp->max_generations; ++gen) {
+  }
+
+  saturn_status generation(int64_t gen) {
+    DeviceGuard dg(p->device);
     gp.gen = (uint32_t)gen;
     const int nxt = cur ^ 1;
     const bool timed = gen <= n_prof;
@@ -797,14 +791,124 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
     evaluated += (uint64_t)(P - E);
     cur = nxt;
+    return SATURN_OK;
+  }
+
+  // memetic step (row f4): improve the E elites, then re-sort them by (ms, position)
+  saturn_status memetic() {
+    if (sp->local_search_iters <= 0) return SATURN_OK;
+    DeviceGuard dg(p->device);
+    CU(p, cudaMemcpyAsync(p->all_ms.p, p->rec_ms.p, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CU(p, cudaMemcpyAsync(p->all_gen.p, p->rec_gen.p, (size_t)E * GS, cudaMemcpyDeviceToDevice, st));
+    CU(p, sat::launch_local_search(p->pb, p->NN, p->GP, p->all_gen.p, p->all_ms.p, E, GS, sp->local_search_iters,
+                                   st));
+    CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, 1, E, GS, p->rec_ms.p, p->rec_gen.p, st));
+    p->stats.kernel_launches += 2;
+    return SATURN_OK;
+  }
+
+  // after all islands' records sit in all_ms / all_gen (W blocks of E): the global best E
+  saturn_status merge() {
+    DeviceGuard dg(p->device);
+    CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, world, E, GS, p->rec_ms.p, p->rec_gen.p, st));
+    p->stats.kernel_launches += 1;
+    return SATURN_OK;
+  }
+
+  saturn_status record() {
+    DeviceGuard dg(p->device);
+    int32_t best = 0;
+    CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
+    CU(p, cudaStreamSynchronize(st));
+    p->stats.d2h_bytes += sizeof best;
+    p->hist_t.push_back(now_s() - t0);
+    p->hist_ms.push_back(best);
+    return SATURN_OK;
+  }
+
+  saturn_status finish(int64_t gens_run, uint64_t world_evaluated, saturn_result* out) {
+    DeviceGuard dg(p->device);
+    std::vector<uint8_t> g0(GS);
+    int32_t best = 0;
+    CU(p, cudaMemcpyAsync(g0.data(), p->rec_gen.p, GS, cudaMemcpyDeviceToHost, st));
+    CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
+    CU(p, cudaStreamSynchronize(st));
+    p->stats.d2h_bytes += GS + sizeof best;
+    for (int64_t g = 1; g <= std::min<int64_t>(n_prof, gens_run); ++g) {
+      float ms = 0.f, m1 = 0.f;
+      CU(p, cudaEventElapsedTime(&ms, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 2]));
+      CU(p, cudaEventElapsedTime(&m1, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 1]));
+      p->stats.ga_kernel_ms += ms;
+      p->stats.ga_launches += 1;
+      p->stats.ga_decodes += P - E;
+      if (sat::ga_is_split()) {
+        p->stats.breed_kernel_ms += m1;
+        p->stats.decode_kernel_ms += ms - m1;
+      } else {
+        p->stats.decode_kernel_ms += ms;
+      }
+    }
+    p->best_cfg.assign(g0.begin(), g0.begin() + T);
+    p->best_perm.assign(g0.begin() + sat::perm_offset(T), g0.begin() + sat::perm_offset(T) + T);
+    p->best_ms = best;
+    p->have_best = true;
+    p->have_pop = true;
+    p->last_pop = cur;
+    p->pop_P = P;
+    p->pop_GS = GS;
+    if (out) {
+      memset(out, 0, sizeof *out);
+      out->makespan = best;
+      out->evaluated = world_evaluated;
+      out->seconds = now_s() - t0;
+      out->flags = SATURN_INCUMBENT;
+      out->generations = (int32_t)gens_run;
+    }
+    return SATURN_OK;
+  }
+};
+
+}  // namespace
+
+saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out) {
+  if (p && host_only(p)) return SATURN_ESTATE;
+  if (!p) return SATURN_EINVAL;
+  Island is;
+  is.p = p;
+  is.sp = sp;
+  is.st = static_cast<cudaStream_t>(stream);
+  is.island = (uint32_t)p->rank;
+  is.world = (p->comm && p->world > 1) ? p->world : 1;
+  saturn_status s;
+  if ((s = is.validate()) != SATURN_OK) return s;
+  if ((s = is.begin()) != SATURN_OK) return s;
+  cudaStream_t st = is.st;
+  const int E = is.E, GS = is.GS;
+  // epoch exchange: memetic step, then (multi-GPU) all-gather of every island's elites over
+  // NCCL and the device merge -- every island continues from the global best E
+  auto exchange = [&]() -> saturn_status {
+    saturn_status e;
+    if ((e = is.memetic()) != SATURN_OK) return e;
+    if (is.world < 2) return SATURN_OK;
+    DeviceGuard dg(p->device);
+    NC(p, nccl().allGather(p->rec_ms.p, p->all_ms.p, (size_t)E, ncclInt32, p->comm, st));
+    NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
+    return is.merge();
+  };
+  if ((s = exchange()) != SATURN_OK) return s;
+  if ((s = is.record()) != SATURN_OK) return s;
+  int64_t gen = 1;
+  for (; gen <= sp->max_generations; ++gen) {
+    if ((s = is.generation(gen)) != SATURN_OK) return s;
     if (gen % sp->generations_per_epoch == 0) {
       if ((s = exchange()) != SATURN_OK) return s;
-      if ((s = record()) != SATURN_OK) return s;
+      if ((s = is.record()) != SATURN_OK) return s;
       if (sp->time_budget_s > 0) {
         // The stop decision must be collective: every island runs the same number of
         // epochs, or the elite all-gathers would mismatch.  MAX-all-reduce of the flag.
-        int stop = (now_s() - t0 >= sp->time_budget_s) ? 1 : 0;
-        if (p->comm && p->world > 1) {
+        int stop = (now_s() - is.t0 >= sp->time_budget_s) ? 1 : 0;
+        if (is.world > 1) {
+          DeviceGuard dg(p->device);
           CU(p, p->flag.ensure(1));
           CU(p, cudaMemcpyAsync(p->flag.p, &stop, sizeof stop, cudaMemcpyHostToDevice, st));
           NC(p, nccl().allReduce(p->flag.p, p->flag.p, 1, ncclInt32, ncclMax, p->comm, st));
@@ -820,43 +924,90 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   }
   const int64_t gens_run = gen - 1;
   if ((s = exchange()) != SATURN_OK) return s;
-  if ((s = record()) != SATURN_OK) return s;
-  std::vector<uint8_t> g0(GS);
-  int32_t best = 0;
-  CU(p, cudaMemcpyAsync(g0.data(), p->rec_gen.p, GS, cudaMemcpyDeviceToHost, st));
-  CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
-  CU(p, cudaStreamSynchronize(st));
-  p->stats.d2h_bytes += GS + sizeof best;
-  for (int64_t g = 1; g <= std::min<int64_t>(n_prof, gens_run); ++g) {
-    float ms = 0.f, m1 = 0.f;
-    CU(p, cudaEventElapsedTime(&ms, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 2]));
-    CU(p, cudaEventElapsedTime(&m1, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 1]));
-    p->stats.ga_kernel_ms += ms;
-    p->stats.ga_launches += 1;
-    p->stats.ga_decodes += P - E;
-    if (sat::ga_is_split()) {
-      p->stats.breed_kernel_ms += m1;
-      p->stats.decode_kernel_ms += ms - m1;
-    } else {
-      p->stats.decode_kernel_ms += ms;
+  if ((s = is.record()) != SATURN_OK) return s;
+  return is.finish(gens_run, is.evaluated * (uint64_t)is.world, out);
+}
+
+saturn_status saturn_search_group(saturn_plan** plans, int32_t k, const saturn_search_params* sp, void** streams,
+                                   saturn_result* out) {
+  if (!plans || k < 1 || !sp) return SATURN_EINVAL;
+  std::vector<Island> isl(k);
+  for (int r = 0; r < k; ++r) {
+    saturn_plan* p = plans[r];
+    if (!p) return SATURN_EINVAL;
+    if (host_only(p)) return SATURN_ESTATE;
+    if (p->comm) return fail(p, SATURN_ESTATE, "search_group islands must not have an NCCL communicator");
+    for (int q = 0; q < r; ++q)
+      if (plans[q] == p) return fail(p, SATURN_EINVAL, "the same handle twice in a group");
+    isl[r].p = p;
+    isl[r].sp = sp;
+    isl[r].st = streams ? static_cast<cudaStream_t>(streams[r]) : nullptr;
+    isl[r].island = (uint32_t)r;
+    isl[r].world = k;
+    saturn_status s = isl[r].validate();
+    if (s != SATURN_OK) return s;
+    if (isl[r].T != isl[0].T || plans[r]->S != plans[0]->S || plans[r]->cfg_r != plans[0]->cfg_r ||
+        plans[r]->gpu_n != plans[0]->gpu_n)
+      return fail(p, SATURN_EINVAL, "islands of a group must load the same cluster and table");
+  }
+  saturn_status s;
+  for (auto& is : isl)
+    if ((s = is.begin()) != SATURN_OK) return s;
+  const int E = isl[0].E, GS = isl[0].GS;
+  // exchange by copies: island r's records land in block r of every island's all_* buffers
+  auto exchange = [&]() -> saturn_status {
+    saturn_status e;
+    for (auto& is : isl)
+      if ((e = is.memetic()) != SATURN_OK) return e;
+    if (k < 2) return SATURN_OK;
+    for (auto& is : isl) {  // the sources must be complete before anyone copies them
+      DeviceGuard dg(is.p->device);
+      CU(is.p, cudaStreamSynchronize(is.st));
+    }
+    for (auto& dst : isl) {
+      DeviceGuard dg(dst.p->device);
+      for (int r = 0; r < k; ++r) {
+        saturn_plan* src = isl[r].p;
+        CU(dst.p, cudaMemcpyPeerAsync(dst.p->all_ms.p + (size_t)r * E, dst.p->device, src->rec_ms.p, src->device,
+                                      E * sizeof(int32_t), dst.st));
+        CU(dst.p, cudaMemcpyPeerAsync(dst.p->all_gen.p + (size_t)r * E * GS, dst.p->device, src->rec_gen.p,
+                                      src->device, (size_t)E * GS, dst.st));
+      }
+    }
+    for (auto& dst : isl)  // all copies must read the old records before anyone merges
+      CU(dst.p, cudaStreamSynchronize(dst.st));
+    for (auto& is : isl)
+      if ((e = is.merge()) != SATURN_OK) return e;
+    return SATURN_OK;
+  };
+  auto record_all = [&]() -> saturn_status {
+    saturn_status e;
+    for (auto& is : isl)
+      if ((e = is.record()) != SATURN_OK) return e;
+    return SATURN_OK;
+  };
+  if ((s = exchange()) != SATURN_OK) return s;
+  if ((s = record_all()) != SATURN_OK) return s;
+  int64_t gen = 1;
+  for (; gen <= sp->max_generations; ++gen) {
+    for (auto& is : isl)
+      if ((s = is.generation(gen)) != SATURN_OK) return s;
+    if (gen % sp->generations_per_epoch == 0) {
+      if ((s = exchange()) != SATURN_OK) return s;
+      if ((s = record_all()) != SATURN_OK) return s;
+      if (sp->time_budget_s > 0 && now_s() - isl[0].t0 >= sp->time_budget_s) {
+        ++gen;
+        break;
+      }
     }
   }
-  p->best_cfg.assign(g0.begin(), g0.begin() + T);
-  p->best_perm.assign(g0.begin() + sat::perm_offset(T), g0.begin() + sat::perm_offset(T) + T);
-  p->best_ms = best;
-  p->have_best = true;
-  p->have_pop = true;
-  p->last_pop = cur;
-  p->pop_P = P;
-  p->pop_GS = GS;
-  if (out) {
-    memset(out, 0, sizeof *out);
-    out->makespan = best;
-    out->evaluated = evaluated * (uint64_t)p->world;
-    out->seconds = now_s() - t0;
-    out->flags = SATURN_INCUMBENT;
-    out->generations = (int32_t)gens_run;
-  }
+  const int64_t gens_run = gen - 1;
+  if ((s = exchange()) != SATURN_OK) return s;
+  if ((s = record_all()) != SATURN_OK) return s;
+  uint64_t total = 0;
+  for (auto& is : isl) total += is.evaluated;
+  for (int r = 0; r < k; ++r)
+    if ((s = isl[r].finish(gens_run, total, out ? &out[r] : nullptr)) != SATURN_OK) return s;
   return SATURN_OK;
 }
 

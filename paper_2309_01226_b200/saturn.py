@@ -26,7 +26,7 @@ DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
 EXPORTS = (
     "saturn_plan_create", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
     "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_nodes", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
-    "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_history",
+    "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_group", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
     "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_improve", "saturn_last_error",
@@ -120,6 +120,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_enumerate": [h, u64, vp, P(Result)],
         "saturn_enumerate_range": [h, u64, u64, vp, P(Result)],
         "saturn_search": [h, P(SearchParams), vp, P(Result)],
+        "saturn_search_group": [P(vp), i32, P(SearchParams), P(vp), P(Result)],
         "saturn_search_history": [h, i64, P(ctypes.c_double), P(i64), P(i64)],
         "saturn_search_population": [h, P(u8), P(u8), P(i32)],
         "saturn_best_plan": [h, P(Placement), P(u8), P(i64)],
@@ -451,6 +452,24 @@ class Plan:
         v = ctypes.c_double()
         self._check(self._lib.saturn_probe_int_peak(self._h, ctypes.byref(v)), "saturn_probe_int_peak")
         return float(v.value)
+
+
+def search_group(plans, cfg: SearchConfig | None = None, streams=None):
+    """Islands in one process (saturn_search_group): -> list of per-island result dicts."""
+    cfg = cfg or SearchConfig()
+    k = len(plans)
+    lib = load_library()
+    sp = plans[0]._search_params(cfg)
+    hs = (ctypes.c_void_p * k)(*[pl._h for pl in plans])
+    st = None
+    if streams is not None:
+        st = (ctypes.c_void_p * k)(*[s.cuda_stream if hasattr(s, "cuda_stream") else s for s in streams])
+    res = (Result * k)()
+    rc = lib.saturn_search_group(hs, k, ctypes.byref(sp), st, res)
+    if rc != OK:
+        raise SaturnError(rc, "saturn_search_group: " + " | ".join(
+            lib.saturn_last_error(pl._h).decode() for pl in plans))
+    return [r.as_dict() for r in res]
 
 
 # Names of the C ABI, for callers who prefer the flat form.

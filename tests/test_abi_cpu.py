@@ -132,6 +132,9 @@ def test_table_validation_errors(lib):
     with pytest.raises(sat.SaturnError) as e:
         p.load_runtime_table(np.ones((256, 1, 1), np.int32))   # > 255 jobs (u8 genes)
     assert e.value.status == sat.EINVAL
+    with pytest.raises(sat.SaturnError) as e:
+        p.load_runtime_table(np.ones((1, 256, 1), np.int32))   # > 255 UPPs (u8 placement field)
+    assert e.value.status == sat.EINVAL
     huge = np.ones((255, 64, 4), np.int32)       # 255 configs/job -> packed table > 48 KB
     with pytest.raises(sat.SaturnError) as e:
         p.load_runtime_table(huge)

@@ -377,6 +377,62 @@ def test_memetic_search_replays(sat, torch):
     assert oracle.decode(c, bc, bp)[0] == best == r["makespan"] <= int(ms.min())
 
 
+@pytest.mark.parametrize("k,epoch,gens,ls", [(2, 1, 2, 0), (3, 2, 5, 0), (2, 2, 3, 2)])
+def test_island_group_replays_migration(sat, torch, k, epoch, gens, ls):
+    """Row e on one GPU: k islands (saturn_search_group) = oracle replay of k ranks with
+    migrate() at every epoch boundary (PAPER.md:232-236 search over the shared plan space;
+    DESIGN.md reading A9) -- every island's population is bit-exact."""
+    from oracle.local_search import improve
+    inst = synth.txt(2)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    P, E, seed = 128, 4, 77
+    px, pc, pm = oga.q32(0.9), oga.q32(0.5), oga.q32(0.5)
+    pops = []
+    for r in range(k):
+        cfg, perm = oga.initial_population(c.S, P, seed, rank=r)
+        pops.append((cfg, perm, oracle.decode_batch(c, cfg, perm)))
+
+    def records(cfg, perm, ms):
+        recs = [(int(ms[i]), cfg[i].copy(), perm[i].copy()) for i in oga.elites(ms, E)]
+        if ls:
+            recs = [improve(c, rc, rq, ls) for _, rc, rq in recs]
+            recs = [(rm, np.asarray(rc, np.uint8), np.asarray(rq, np.uint8)) for rc, rq, rm in recs]
+            recs = [recs[j] for j in sorted(range(E), key=lambda j: (recs[j][0], j))]
+        return recs
+
+    merged = oga.migrate([records(*pp) for pp in pops])
+    for gen in range(1, gens + 1):
+        nxt = []
+        for r, (cfg, perm, ms) in enumerate(pops):
+            cfg, perm, _ = oga.next_generation(c.S, cfg, perm, ms, gen, seed, r, E, px, pc, pm, elite_records=merged)
+            nxt.append((cfg, perm, oracle.decode_batch(c, cfg, perm)))
+        pops = nxt
+        merged = oga.migrate([records(*pp) for pp in pops]) if gen % epoch == 0 else None
+    plans = [_plan(sat, inst) for _ in range(k)]
+    res = sat.search_group(plans, sat.SearchConfig(seed=seed, population=P, max_generations=gens, elites=E,
+                                                   generations_per_epoch=epoch, p_xover=0.9, p_cfg_mut=0.5,
+                                                   p_perm_mut=0.5, local_search_iters=ls))
+    final = oga.migrate([records(*pp) for pp in pops])
+    for r in range(k):
+        gc, gq, gm = plans[r].search_population(P)
+        assert np.array_equal(gc, pops[r][0]) and np.array_equal(gq, pops[r][1]), r
+        assert np.array_equal(gm, pops[r][2]), r
+        best, pl, bc, bp = plans[r].best_plan()
+        assert best == res[r]["makespan"] == final[0][0]
+        assert oracle.decode(c, bc, bp)[0] == best
+        assert res[r]["evaluated"] == k * (P + gens * (P - E))
+
+
+def test_island_group_rejects_mismatched_handles(sat, torch):
+    inst = synth.txt(2)
+    a = _plan(sat, inst)
+    b = _plan(sat, synth.txt(3))
+    with pytest.raises(sat.SaturnError):
+        sat.search_group([a, b], sat.SearchConfig(population=128, elites=4, max_generations=1))
+    with pytest.raises(sat.SaturnError):
+        sat.search_group([a, a], sat.SearchConfig(population=128, elites=4, max_generations=1))
+
+
 def test_split_generation_mode_replays(sat, torch):
     """SATURN_GA_SPLIT=1 (breed kernel + population decode kernel) reproduces the same GA
     trajectory as the oracle (run in a subprocess: the mode is read once per process)."""
