@@ -53,7 +53,7 @@ typedef enum {
 } saturn_status;
 
 /* saturn_result.flags */
-enum { SATURN_PROVEN_OPTIMAL = 1, SATURN_INCUMBENT = 2, SATURN_PREFIX_SHARED = 4 };
+enum { SATURN_PROVEN_OPTIMAL = 1, SATURN_INCUMBENT = 2, SATURN_PREFIX_SHARED = 4, SATURN_SYMMETRY_REDUCED = 8 };
 
 /* saturn_set_decoder kinds (row a5: two device designs, chosen by measurement) */
 enum { SATURN_DECODER_AUTO = 0, SATURN_DECODER_THREAD = 1, SATURN_DECODER_WARP = 2 };
@@ -178,6 +178,19 @@ saturn_status saturn_enumerate(saturn_plan *p, uint64_t max_genomes, void *strea
  * genomes accounted for, `leaves` = leaves actually visited); the result is identical to
  * the index-order brute force.  SATURN_ENUM_ODOMETER=1 forces full decodes in index order.
  *
+ * Symmetry reduction (row f4; reading A14): with
+ * SATURN_ENUM_SYMMETRY set, jobs whose compacted config lists are the same (g, R) sequence
+ * ("twins", e.g. the same model trained at several learning rates) are
+ * placed in increasing job id order only: a genome that places a job before its previous
+ * twin is skipped.  Relabelling twins maps every genome onto such a canonical genome with
+ * the same makespan, so the minimum is unchanged; the returned index is the smallest
+ * CANONICAL genome index attaining it, and the space shrinks by prod_c (k_c!) over twin
+ * classes of size k_c.  Applies to the depth-first path only (flags |= SATURN_SYMMETRY_REDUCED
+ * when a twin class exists); the odometer and range paths ignore it. */
+enum { SATURN_ENUM_SYMMETRY = 1 };
+saturn_status saturn_set_enumeration_options(saturn_plan *p, uint32_t options);
+
+/*
  * Enumerate only genome indices [begin, end) on this device (no collective; full decodes). */
 saturn_status saturn_enumerate_range(saturn_plan *p, uint64_t begin, uint64_t end, void *stream,
                                      saturn_result *out);

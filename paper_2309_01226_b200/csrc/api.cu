@@ -101,6 +101,7 @@ struct saturn_plan {
   int NN = 0, GP = 0;
   bool sorted_ok = false;
   int decoder = SATURN_DECODER_AUTO;
+  uint32_t enum_options = 0;
   DevBuf<uint8_t> blob;
   int blob_bytes = 0;
   void* pinned = nullptr;     // pinned host staging for the table upload
@@ -583,6 +584,20 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
   ds.pre[0] = 0;
   for (int t = 0; t < T; ++t) ds.pre[t + 1] = ds.pre[t] + p->S[t];
   ds.sumS = ds.pre[T];
+  // symmetry reduction: twin = same (g, R) list; each job waits for its previous twin
+  bool reduced = false;
+  for (int t = 0; t < T; ++t) {
+    ds.twin_prev[t] = 0;
+    if (!(p->enum_options & SATURN_ENUM_SYMMETRY)) continue;
+    for (int u = t - 1; u >= 0 && !ds.twin_prev[t]; --u) {
+      bool same = p->S[u] == p->S[t];
+      for (int c = 0; same && c < p->S[t]; ++c)
+        same = p->cfg_g[u * p->stride + c] == p->cfg_g[t * p->stride + c] &&
+               p->cfg_r[u * p->stride + c] == p->cfg_r[t * p->stride + c];
+      if (same) ds.twin_prev[t] = 1u << u;
+    }
+    reduced |= ds.twin_prev[t] != 0;
+  }
   // root depth: enough roots to fill the GPU (~32 per SM-thread slot), at most T - 1 levels
   ds.D = 1;
   ds.n_roots = (uint64_t)ds.sumS;
@@ -634,7 +649,7 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
     out->evaluated = total;
     out->leaves = kl[1];
     out->seconds = now_s() - t0;
-    out->flags = SATURN_PROVEN_OPTIMAL | SATURN_PREFIX_SHARED;
+    out->flags = SATURN_PROVEN_OPTIMAL | SATURN_PREFIX_SHARED | (reduced ? SATURN_SYMMETRY_REDUCED : 0);
   }
   return SATURN_OK;
 }
@@ -659,6 +674,13 @@ saturn_status saturn_enumerate(saturn_plan* p, uint64_t max_genomes, void* strea
   uint64_t b = 0, e = size;
   saturn_partition(size, p->rank, p->world, &b, &e);
   return enumerate_impl(p, b, e, size, true, static_cast<cudaStream_t>(stream), out);
+}
+
+saturn_status saturn_set_enumeration_options(saturn_plan* p, uint32_t options) {
+  if (!p) return SATURN_EINVAL;
+  if (options & ~(uint32_t)SATURN_ENUM_SYMMETRY) return fail(p, SATURN_EINVAL, "unknown option bits 0x%x", options);
+  p->enum_options = options;
+  return SATURN_OK;
 }
 
 saturn_status saturn_enumerate_range(saturn_plan* p, uint64_t begin, uint64_t end, void* stream, saturn_result* out) {

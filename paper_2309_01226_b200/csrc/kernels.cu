@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
       int t = 0;
       while (ds.pre[t + 1] <= pi) ++t;
       const int c = pi - ds.pre[t];
-      if (used & (1u << t)) { ok = false; break; }
+      if ((used & (1u << t)) || (used & ds.twin_prev[t]) != ds.twin_prev[t]) { ok = false; break; }
       const uint32_t w = tab[t * pb.stride + c];
       ms = max(ms, place_T<NN, GP>(a, (int)(w >> 24), (int)(w & R_MASK)));
       rperm += (uint64_t)__popc(~used & full & ((1u << t) - 1u)) * ds.es.fact[T - 1 - i];
@@ -606,6 +606,10 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
         }
         tc = __ffs(rem) - 1;
         cc = 0;
+        if ((used & ds.twin_prev[tc]) != ds.twin_prev[tc]) {  // a twin before its predecessor
+          cc = S[tc] - 1;
+          continue;
+        }
       }
       {
         const uint32_t w = tab[tc * pb.stride + cc];

@@ -50,6 +50,7 @@ struct DfsSpace {
   int sumS;
   int D;                     // root depth
   uint64_t n_roots;          // sumS^D
+  uint32_t twin_prev[ENUM_MAX_T];  // bit of job t's previous twin (symmetry reduction), or 0
 };
 cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
                                  uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,

@@ -19,14 +19,15 @@ LIB_PATH = os.path.join(_HERE, "libsaturn.so")
 
 OK, EINVAL, EUNSCHEDULABLE, ELIMIT, ECUDA, ENCCL, ESTATE = range(7)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EUNSCHEDULABLE", 3: "ELIMIT", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
-PROVEN_OPTIMAL, INCUMBENT, PREFIX_SHARED = 1, 2, 4
+PROVEN_OPTIMAL, INCUMBENT, PREFIX_SHARED, SYMMETRY_REDUCED = 1, 2, 4, 8
+ENUM_SYMMETRY = 1
 DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
 
 # Every symbol declared in include/saturn.h.
 EXPORTS = (
     "saturn_plan_create", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
     "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_nodes", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
-    "saturn_enumerate", "saturn_enumerate_range", "saturn_search", "saturn_search_group", "saturn_search_history",
+    "saturn_enumerate", "saturn_enumerate_range", "saturn_set_enumeration_options", "saturn_search", "saturn_search_group", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
     "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_improve", "saturn_last_error",
@@ -119,6 +120,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_space_size": [h, P(u64)],
         "saturn_enumerate": [h, u64, vp, P(Result)],
         "saturn_enumerate_range": [h, u64, u64, vp, P(Result)],
+        "saturn_set_enumeration_options": [h, ctypes.c_uint32],
         "saturn_search": [h, P(SearchParams), vp, P(Result)],
         "saturn_search_group": [P(vp), i32, P(SearchParams), P(vp), P(Result)],
         "saturn_search_history": [h, i64, P(ctypes.c_double), P(i64), P(i64)],
@@ -330,6 +332,12 @@ class Plan:
                                            _dev_ptr(pl, "uint8"), _dev_ptr(ms, "int32"), self._stream(stream)),
                     "saturn_trace")
         return pl, ms
+
+    def set_enumeration_options(self, symmetry: bool = False):
+        """saturn_set_enumeration_options: symmetry=True skips genomes that place a job before
+        its previous identical twin (row f4); the optimum is unchanged."""
+        self._check(self._lib.saturn_set_enumeration_options(self._h, ENUM_SYMMETRY if symmetry else 0),
+                    "saturn_set_enumeration_options")
 
     def enumerate(self, max_genomes: int = (1 << 38) - 1, stream=None) -> dict:
         r = Result()

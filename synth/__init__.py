@@ -8,6 +8,6 @@ side's code lives here.
 """
 from .workloads import (  # noqa: F401
     UPPS, DDP, FSDP, PIPE, SPILL, Instance,
-    tiny, txt, img, mix, sweep, tiny_variant, random_tiny, by_name, CONFIG_NAMES,
+    tiny, txt, img, mix, sweep, tiny_variant, lr_sweep, random_tiny, by_name, CONFIG_NAMES,
     random_genomes,
 )

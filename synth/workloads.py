@@ -189,6 +189,20 @@ def random_tiny(rng: np.random.Generator, max_jobs: int = 4, node_choices=None, 
                     upps=UPPS[:n_upps])
 
 
+def lr_sweep(seed: int, n_models: int, n_lrs, nodes=(4,)) -> Instance:
+    """A TINY-shaped learning-rate sweep: model m is trained at n_lrs[m] learning rates.  A
+    job's runtime does not depend on its learning rate, so the replicas of a model share one
+    runtime row exactly (no per-job noise) -- the twin structure of row f4."""
+    base = tiny(seed, n_models, nodes)
+    rows, labels = [], []
+    for m in range(n_models):
+        for k in range(n_lrs[m]):
+            rows.append(base.runtime[m])
+            labels.append(f"tiny#{m} lr={LEARNING_RATES[k % len(LEARNING_RATES)]:g}")
+    return Instance(f"LRSWEEP{sum(n_lrs)}", list(nodes), np.stack(rows).astype(np.int32), labels,
+                    upps=base.upps)
+
+
 CONFIG_NAMES = ("TINY", "TXT", "IMG", "MIX", "SWEEP")
 
 

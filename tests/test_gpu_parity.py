@@ -591,3 +591,29 @@ def test_dfs_enumeration_equals_index_order_enumeration(sat, torch):
         c = oracle.compact(inst.node_gpus, inst.runtime)
         cfg, perm = oracle.unrank(c, dfs["genome_index"])
         assert oracle.decode(c, cfg, perm)[0] == dfs["makespan"]
+
+
+@pytest.mark.parametrize("n_lrs,nodes", [((2, 2, 1), (4,)), ((3, 3), (2, 2)), ((3, 2, 1), (4,)), ((1, 1, 1, 1, 1), (4,))])
+def test_dfs_symmetry_reduction_matches_oracle(sat, torch, n_lrs, nodes):
+    """Row f4: enumeration with SATURN_ENUM_SYMMETRY = oracle brute force over canonical genomes
+    (oracle/symmetry.py), bit-exact (makespan, index); the makespan equals the unreduced one."""
+    from oracle import symmetry as sym
+    inst = synth.lr_sweep(5, len(n_lrs), n_lrs, nodes)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    plan = _plan(sat, inst)
+    full = plan.enumerate()
+    plan.set_enumeration_options(symmetry=True)
+    red = plan.enumerate()
+    want = sym.brute_force_canonical(c)
+    assert (red["makespan"], red["genome_index"]) == want
+    assert red["makespan"] == full["makespan"]
+    twins = any(p >= 0 for p in sym.twin_prev(c))
+    assert bool(red["flags"] & sat.SYMMETRY_REDUCED) == twins
+    if twins:
+        assert red["leaves"] <= full["leaves"]
+    else:
+        assert red["genome_index"] == full["genome_index"]
+    best, pl, bc, bp = plan.best_plan()
+    assert best == red["makespan"] and sym.is_canonical(c, bp)
+    plan.set_enumeration_options(symmetry=False)
+    assert plan.enumerate()["genome_index"] == full["genome_index"]
