@@ -214,8 +214,9 @@ saturn_status saturn_search(saturn_plan *p, const saturn_search_params *sp, void
 saturn_status saturn_search_group(saturn_plan **plans, int32_t k, const saturn_search_params *sp, void **streams,
                                   saturn_result *out);
 
-/* Best-so-far curve of the last search: up to n_max (seconds since the call, makespan)
- * pairs, one per epoch; *n_out = number written. */
+/* Best-so-far curve of the last search: up to n_max (seconds, makespan) pairs, one per
+ * epoch; *n_out = number written.  Seconds are device time since the search's first
+ * operation on its stream (events; the epochs are recorded without host round trips). */
 saturn_status saturn_search_history(const saturn_plan *p, int64_t n_max, double *t_s, int64_t *makespan,
                                     int64_t *n_out);
 

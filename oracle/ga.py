@@ -23,8 +23,8 @@ V(n, h) = (h * n) >> 16 and a 16-bit gate with q32 threshold p fires iff h < p >
 stream (k, g, rank << 16 | 0):
    w0, w1   tournament for parent A: i = U(P, w0), j = U(P, w1); A = smaller (ms, slot)
    w2, w3   tournament for parent B, same rule
-   w4       lo: crossover gate (p_x)          hi: OX1 cut a = V(T, hi)
-   w5       lo: OX1 cut b = V(T, lo)          hi: permutation-mutation gate (p_m)
+   w4       lo: crossover gate (p_x)          hi: LOX cut a = V(T, hi)
+   w5       lo: LOX cut b = V(T, lo)          hi: permutation-mutation gate (p_m)
    w6       lo: mutation kind = lo & 1        hi: mutation position i = V(T, hi)
    w7       lo: mutation position j = V(T, lo) hi: config-mutation gate (p_c)
    w8       lo: mutated job t* = V(T, lo)     hi: its new gene V(S_t*, hi)
@@ -32,9 +32,12 @@ stream (k, g, rank << 16 | 0):
  Steps, in order:
    1. tournaments;  2. child = copy of A;
    3. if crossover: cfg[t] = B.cfg[t] where bit t is 0;
-   4. if crossover: OX1 -- a, b swapped so a <= b; keep A.perm[a..b]; fill positions b+1,
-      b+2, ... (cyclic) with B's genes read from position b+1 (cyclic), skipping genes in
-      A's slice;
+   4. if crossover: LOX (linear order crossover, Falkenauer & Bouffouix 1991) -- a, b
+      swapped so a <= b; keep A.perm[a..b] in place; fill positions 0..a-1, then b+1..T-1,
+      with B's genes in B's order from position 0, skipping genes in A's slice.  (GA v4:
+      v3 used OX1, which treats the permutation as a cyclic tour; a priority list is
+      linear, and LOX keeps both the slice's positions and B's relative order without the
+      wrap-around.)
    5. if config mutation: cfg[t*] = new gene;
    6. if permutation mutation: kind 0 swaps positions i and j; kind 1 removes the gene at i
       and reinserts it at position j.
@@ -80,6 +83,14 @@ def elites(ms, E: int):
     return sorted(range(len(ms)), key=lambda i: (int(ms[i]), i))[:E]
 
 
+def lox(A_perm, B_perm, a: int, b: int):
+    """Linear order crossover: A's slice [a..b] stays in place; positions 0..a-1 then
+    b+1..T-1 take B's genes that are not in the slice, in B's order from position 0."""
+    kept = set(A_perm[a:b + 1])
+    fill = [x for x in B_perm if x not in kept]
+    return list(fill[:a]) + list(A_perm[a:b + 1]) + list(fill[a:])
+
+
 def make_child(S, cfg, perm, ms, slot: int, gen: int, seed: int, rank: int,
                p_x: int, p_c: int, p_m: int):
     P, T = cfg.shape
@@ -110,13 +121,7 @@ def make_child(S, cfg, perm, ms, slot: int, gen: int, seed: int, rank: int,
         a, b = V(T, hi[4]), V(T, lo[5])
         if a > b:
             a, b = b, a
-        kept = set(child_perm[a:b + 1])
-        pos = (b + 1) % T
-        for k in range(T):
-            x = B_perm[(b + 1 + k) % T]
-            if x not in kept:
-                child_perm[pos] = x
-                pos = (pos + 1) % T
+        child_perm = lox(child_perm, B_perm, a, b)
     if hi[7] < (p_c >> 16):
         t = V(T, lo[8])
         child_cfg[t] = V(int(S[t]), hi[8])

@@ -132,6 +132,12 @@ struct saturn_plan {
   int pop_GS = 0;
   std::vector<double> hist_t;
   std::vector<int64_t> hist_ms;
+  // best-so-far records in flight: async D2H copies into pinned slots + an event each, read
+  // back at the end of the search (no host round trip per epoch)
+  static constexpr int HIST_SLOTS = 256;
+  int32_t* hist_pin = nullptr;
+  std::vector<cudaEvent_t> hist_ev;   // [0] = start of the search, [1 + k] = record k
+  int hist_n = 0;
   // communicator
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -749,6 +755,15 @@ struct Island {
   saturn_status begin() {
     DeviceGuard dg(p->device);
     t0 = now_s();
+    if (!p->hist_pin) CU(p, cudaHostAlloc(reinterpret_cast<void**>(&p->hist_pin), sizeof(int32_t) * p->HIST_SLOTS,
+                                          cudaHostAllocDefault));
+    while ((int)p->hist_ev.size() < 1 + p->HIST_SLOTS) {
+      cudaEvent_t e;
+      CU(p, cudaEventCreate(&e));
+      p->hist_ev.push_back(e);
+    }
+    p->hist_n = 0;
+    CU(p, cudaEventRecord(p->hist_ev[0], st));
     for (int b = 0; b < 2; ++b) {
       CU(p, p->pop[b].ensure((size_t)P * GS));
       CU(p, p->pms[b].ensure((size_t)P));
@@ -837,14 +852,34 @@ struct Island {
     return SATURN_OK;
   }
 
+  // Best-so-far after an epoch (the anytime curve, saturn_search_history): an async copy
+  // into a pinned slot plus an event; only a time-budgeted search waits for it (its stop
+  // decision needs the host clock to match the device).
   saturn_status record() {
     DeviceGuard dg(p->device);
-    int32_t best = 0;
-    CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
+    if (p->hist_n == p->HIST_SLOTS) {
+      saturn_status s = flush_history();
+      if (s != SATURN_OK) return s;
+    }
+    const int k = p->hist_n++;
+    CU(p, cudaMemcpyAsync(p->hist_pin + k, p->rec_ms.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CU(p, cudaEventRecord(p->hist_ev[1 + k], st));
+    p->stats.d2h_bytes += sizeof(int32_t);
+    if (sp->time_budget_s > 0) return flush_history();
+    return SATURN_OK;
+  }
+
+  // Drain the in-flight records: seconds since the search started (device clock, from the
+  // event recorded before its first kernel) and the best makespan at that point.
+  saturn_status flush_history() {
     CU(p, cudaStreamSynchronize(st));
-    p->stats.d2h_bytes += sizeof best;
-    p->hist_t.push_back(now_s() - t0);
-    p->hist_ms.push_back(best);
+    for (int k = 0; k < p->hist_n; ++k) {
+      float ms = 0.f;
+      CU(p, cudaEventElapsedTime(&ms, p->hist_ev[0], p->hist_ev[1 + k]));
+      p->hist_t.push_back(1e-3 * ms);
+      p->hist_ms.push_back(p->hist_pin[k]);
+    }
+    p->hist_n = 0;
     return SATURN_OK;
   }
 
@@ -854,7 +889,8 @@ struct Island {
     int32_t best = 0;
     CU(p, cudaMemcpyAsync(g0.data(), p->rec_gen.p, GS, cudaMemcpyDeviceToHost, st));
     CU(p, cudaMemcpyAsync(&best, p->rec_ms.p, sizeof best, cudaMemcpyDeviceToHost, st));
-    CU(p, cudaStreamSynchronize(st));
+    saturn_status hs = flush_history();   // synchronises the stream
+    if (hs != SATURN_OK) return hs;
     p->stats.d2h_bytes += GS + sizeof best;
     for (int64_t g = 1; g <= std::min<int64_t>(n_prof, gens_run); ++g) {
       float ms = 0.f, m1 = 0.f;
@@ -1505,6 +1541,8 @@ void saturn_plan_destroy(saturn_plan* p) {
     p->seeds.release();
     p->sink.release();
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->hist_ev) cudaEventDestroy(e);
+    if (p->hist_pin) cudaFreeHost(p->hist_pin);
   }
   delete p;
 }

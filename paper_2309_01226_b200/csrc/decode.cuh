@@ -51,6 +51,9 @@ __device__ __forceinline__ int sel_fma(int p, int a, int b) {
 #ifndef SAT_FMA_SEL_STAGES
 #define SAT_FMA_SEL_STAGES 8   // all barrel-shift stages (measured r1: +5 % TXT, +8 % MIX evaluate)
 #endif
+#ifndef SAT_INF_SEL
+#define SAT_INF_SEL 1          // lanes that shift in +inf use an ALU select (pipe balance)
+#endif
 #ifndef SAT_FMA_MULTI
 #define SAT_FMA_MULTI 0        // multi-node gather / scatter on the FMA pipe too
 #endif
@@ -70,7 +73,12 @@ __device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R) {
     if (stage >= (int)(__builtin_ctz(GP)) - SAT_FMA_SEL_STAGES) {
       const int p = (k >> stage) & 1;
 #pragma unroll
-      for (int i = 0; i < GP; ++i) b[i] = sel_fma(p, b[i], i + sh < GP ? b[i + sh] : INF);
+      for (int i = 0; i < GP; ++i) {
+        if (SAT_INF_SEL && i + sh >= GP)
+          b[i] = on ? INF : b[i];   // shifted-in +inf: one ALU select beats two FMA-pipe ops
+        else
+          b[i] = sel_fma(p, b[i], i + sh < GP ? b[i + sh] : INF);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < GP; ++i) b[i] = on ? (i + sh < GP ? b[i + sh] : INF) : b[i];

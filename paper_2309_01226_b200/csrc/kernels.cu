@@ -694,7 +694,7 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
 
 // ------------------------------------------------------------------ K3 (+K1): GA
 // Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
-// then parent B, then the OX1 slice bit set for T > 32 (8 words, interleaved per thread).
+// then parent B, then the LOX slice bit set for T > 32 (8 words, interleaved per thread).
 static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
   return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)2 * GA_B * odd_row_stride(GS) +
          (size_t)4 * 8 * GA_B + 8 * GA_B + 8;
@@ -712,6 +712,22 @@ __device__ __forceinline__ void load_row(uint8_t* row, const uint8_t* __restrict
     d[4 * k + 3] = v.w;
   }
 }
+// Store one 16-byte chunk (index k) of a record into a smem row (4-byte stores: rows are
+// only 4-byte aligned), and copy chunks k0.. of a global record.
+__device__ __forceinline__ void put_quad(uint8_t* row, int k, const uint4 v) {
+  uint32_t* d = reinterpret_cast<uint32_t*>(row) + 4 * k;
+  d[0] = v.x;
+  d[1] = v.y;
+  d[2] = v.z;
+  d[3] = v.w;
+}
+__device__ __forceinline__ void load_row_from(uint8_t* row, const uint8_t* __restrict__ g, int k0, int GS) {
+  const uint4* src = reinterpret_cast<const uint4*>(g);
+  for (int k = k0; k < GS / 16; ++k) put_quad(row, k, src[k]);
+}
+#ifndef SAT_GA_EARLY_LOAD
+#define SAT_GA_EARLY_LOAD 0   // 1: parent records requested before the Philox blocks (A/B)
+#endif
 __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t* row, int GS) {
   uint4* dst = reinterpret_cast<uint4*>(g);
   const uint32_t* s = reinterpret_cast<const uint32_t*>(row);
@@ -728,7 +744,7 @@ struct GaMinBlocks {
                                        : (STATE <= 8 ? SAT_GA_MINB_SMALL : (STATE <= 32 ? 4 : 2));
 };
 
-// Child construction follows oracle/ga.py (GA v3): every Philox
+// Child construction follows oracle/ga.py (GA v4): every Philox
 // word has a fixed position, so all lanes draw the same blocks at the same program points
 // and the operators run as uniform loops with predicated writes (no divergent refills).
 template <int NN, int GP, bool DECODE>
@@ -755,7 +771,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   const int tid = threadIdx.x, lane = tid & 31;
   const RowG ch{s_child + RS * tid, Tp};
   const RowG gb{s_B + RS * tid, Tp};
-  uint32_t* inA = s_bits + tid;  // OX1 slice set for T > 32: word w at inA[w * GA_B]
+  uint32_t* inA = s_bits + tid;  // LOX slice set for T > 32: word w at inA[w * GA_B]
   const uint32_t P = (uint32_t)gp.P;
   const int nb = (T + 31) / 32;
   int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
@@ -809,6 +825,36 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         A = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
         B = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
       }
+#if SAT_GA_EARLY_LOAD
+      // 2. child = A (elites: the elite record).  The first 32 bytes of both parent records
+      //    are requested now and consumed after the Philox blocks, which hide their latency.
+      const uint8_t* srcA = elite ? rec_gen + slot * GS : prev_pop + (uint64_t)A * GS;
+      const uint8_t* srcB = prev_pop + (uint64_t)B * GS;
+      const int nq = GS >> 4;
+      uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
+      if (elite || child) {
+        a0 = reinterpret_cast<const uint4*>(srcA)[0];
+        if (nq > 1) a1 = reinterpret_cast<const uint4*>(srcA)[1];
+      }
+      if (child) {
+        b0 = reinterpret_cast<const uint4*>(srcB)[0];
+        if (nq > 1) b1 = reinterpret_cast<const uint4*>(srcB)[1];
+      }
+      prefetch(slot + nthr);
+      const uint4 w1 = rw.block(1), w2 = rw.block(2);
+      rw.blk = 2;
+      rw.cur = w2;
+      if (elite || child) {
+        put_quad(ch.base, 0, a0);
+        if (nq > 1) put_quad(ch.base, 1, a1);
+        load_row_from(ch.base, srcA, 2, GS);
+      }
+      if (child) {
+        put_quad(gb.base, 0, b0);
+        if (nq > 1) put_quad(gb.base, 1, b1);
+        load_row_from(gb.base, srcB, 2, GS);
+      }
+#else
       prefetch(slot + nthr);
       const uint4 w1 = rw.block(1), w2 = rw.block(2);
       rw.blk = 2;
@@ -819,6 +865,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         load_row(ch.base, prev_pop + (uint64_t)A * GS, GS);
         load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
       }
+#endif
       const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
       const bool xo = child && (w1.x & 0xffffu) < px16;
       uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
@@ -837,38 +884,42 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           cw[t >> 2] = (wa & ~m) | (wb & m);                               // pad bytes: 0 in both
         }
       }
-      // 4. OX1: keep A.perm[a..b], fill the rest with B's order from b+1 (cyclic)
-      if (T <= 32) {
-        uint32_t kept = 0;
-        for (int q = 0; q < T; ++q) {
-          const uint32_t bit = 1u << ch.q(q);
-          kept |= ((uint32_t)q - a <= b - a) ? bit : 0u;
-        }
-        int pos = ((int)b + 1 == T) ? 0 : (int)b + 1;
-        int rd = pos;
-        for (int k = 0; k < T; ++k) {
-          const int x = gb.q(rd);
-          rd = (rd + 1 == T) ? 0 : rd + 1;
-          const bool take = xo && !((kept >> x) & 1u);
-          if (take) ch.q(pos) = (uint8_t)x;
-          pos += take ? 1 : 0;
-          pos = (pos == T) ? 0 : pos;
-        }
-      } else {
-        for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
-        for (int q = (int)a; q <= (int)b; ++q) {
-          const int x = ch.q(q);
-          inA[(x >> 5) * GA_B] |= 1u << (x & 31);
-        }
-        int pos = ((int)b + 1 == T) ? 0 : (int)b + 1;
-        int rd = pos;
-        for (int k = 0; k < T; ++k) {
-          const int x = gb.q(rd);
-          rd = (rd + 1 == T) ? 0 : rd + 1;
-          const bool take = xo && !((inA[(x >> 5) * GA_B] >> (x & 31)) & 1u);
-          if (take) ch.q(pos) = (uint8_t)x;
-          pos += take ? 1 : 0;
-          pos = (pos == T) ? 0 : pos;
+      // 4. LOX (linear order crossover): keep A.perm[a..b] in place; fill positions 0..a-1,
+      //    then b+1..T-1, with B's genes in B's order from position 0, skipping the slice's
+      //    genes.  No wrap-around: the write pointer jumps over the slice once.
+      {
+        uint8_t* const p0 = &ch.q(0);
+        uint8_t* const pa = p0 + a;
+        const uint32_t gap = b - a + 1;
+        uint8_t* wp = (a == 0) ? p0 + gap : p0;
+        if (T <= 32) {
+          uint32_t kept = 0;
+          for (int q = 0; q < T; ++q) {
+            const uint32_t bit = 1u << ch.q(q);
+            kept |= ((uint32_t)q - a <= b - a) ? bit : 0u;
+          }
+          if (!xo) kept = 0xffffffffu;   // nothing is taken
+          for (int k = 0; k < T; ++k) {   // branch-free: predicated store, pointer arithmetic
+            const uint32_t x = gb.q(k);
+            const uint32_t take = (~kept >> x) & 1u;
+            if (take) *wp = (uint8_t)x;
+            wp += take;
+            wp = (wp == pa) ? wp + gap : wp;
+          }
+        } else {
+          for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
+          for (int q = (int)a; q <= (int)b; ++q) {
+            const int x = ch.q(q);
+            inA[(x >> 5) * GA_B] |= 1u << (x & 31);
+          }
+          const uint32_t xm = xo ? 1u : 0u;
+          for (int k = 0; k < T; ++k) {
+            const int x = gb.q(k);
+            const uint32_t take = (~inA[(x >> 5) * GA_B] >> (x & 31)) & xm;
+            if (take) *wp = (uint8_t)x;
+            wp += take;
+            wp = (wp == pa) ? wp + gap : wp;
+          }
         }
       }
       // 5. config mutation of one job

@@ -617,3 +617,45 @@ def test_dfs_symmetry_reduction_matches_oracle(sat, torch, n_lrs, nodes):
     assert best == red["makespan"] and sym.is_canonical(c, bp)
     plan.set_enumeration_options(symmetry=False)
     assert plan.enumerate()["genome_index"] == full["genome_index"]
+
+
+# ------------------------------------------------------------------ bench scale
+@pytest.mark.parametrize("name", ["TXT", "MIX"])
+def test_bench_scale_search_sampled_replay(sat, torch, name):
+    """The launch configuration bench.py times (P = 2^22 genomes, E = 16, epochs of 8,
+    seed 2309) at BASELINE.json's full sizes: generation 16 is checked against the oracle on
+    sampled slots -- every sampled child is rebuilt from generation 15 by oga.make_child and
+    decoded by the C oracle; the 16 elites are generation 15's best (ms, slot); every genome
+    of the final population is a valid (cfg, perm); the reported best is the population
+    minimum and its trace re-validates."""
+    inst = synth.by_name(name, 0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    P, E, seed = 1 << 22, 16, 2309
+    base = dict(seed=seed, population=P, elites=E, generations_per_epoch=8)
+    px, pc, pm = oga.q32(0.9), oga.q32(0.5), oga.q32(0.5)
+    plan = _plan(sat, inst)
+    plan.search(sat.SearchConfig(max_generations=15, **base))
+    c15, q15, m15 = plan.search_population(P)
+    r = plan.search(sat.SearchConfig(max_generations=16, **base))
+    c16, q16, m16 = plan.search_population(P)
+    T = c.n_jobs
+    # validity of every genome (vectorised): perm is a permutation, cfg < S_t
+    assert (np.sort(q16, axis=1) == np.arange(T, dtype=np.uint8)).all()
+    assert (c16 < np.asarray(c.S, np.uint8)[None, :]).all()
+    # elites: generation 15's E best by (ms, slot), carried with their makespans
+    order = np.lexsort((np.arange(P), m15))[:E]
+    assert np.array_equal(c16[:E], c15[order]) and np.array_equal(q16[:E], q15[order])
+    assert np.array_equal(m16[:E], m15[order])
+    # sampled children: operator replay + oracle decode
+    rng = np.random.default_rng(7)
+    slots = np.unique(np.concatenate([rng.integers(E, P, 1500), [E, E + 1, P - 2, P - 1]]))
+    kids = [oga.make_child(c.S, c15, q15, m15, int(k), 16, seed, 0, px, pc, pm) for k in slots]
+    kc = np.array([k[0] for k in kids], np.uint8)
+    kq = np.array([k[1] for k in kids], np.uint8)
+    assert np.array_equal(c16[slots], kc) and np.array_equal(q16[slots], kq)
+    assert np.array_equal(m16[slots], oracle.decode_batch(c, kc, kq))
+    # the reported best = population minimum; its plan re-validates
+    assert r["makespan"] == int(m16.min()) == int(m16[0])
+    best, pl, bc, bp = plan.best_plan()
+    ms, _ = oracle.decode(c, bc, bp)
+    assert ms == best == r["makespan"] and oracle.validate(c, pl, best) == []

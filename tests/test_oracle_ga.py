@@ -1,7 +1,7 @@
 """GA operator replay (oracle/ga.py) invariants.  The GA is a heuristic, so its trajectory
 is unpinned by the paper; what is pinned:
-operators emit valid genomes, elitism keeps the best, OX1 keeps A's slice and B's
-relative order, and everything is a pure function of (seed, counters)."""
+operators emit valid genomes, elitism keeps the best, LOX keeps A's slice in place and
+B's relative order (plus a hand-worked LOX example), and everything is a pure function of (seed, counters)."""
 import numpy as np
 
 import oracle
@@ -44,7 +44,18 @@ def test_children_valid_and_elites_kept():
         cfg, perm, ms = ncfg, nperm, nms
 
 
-def test_ox1_keeps_slice_and_order():
+def test_lox_hand_example():
+    # A = 0..7, B = 7..0, slice [2..4] = (2 3 4) stays; B without {2,3,4} in B's order is
+    # 7 6 5 1 0: positions 0..1 <- 7 6, positions 5..7 <- 5 1 0.
+    assert ga.lox(list(range(8)), list(range(7, -1, -1)), 2, 4) == [7, 6, 2, 3, 4, 5, 1, 0]
+    # slice at the front / back and the whole permutation
+    assert ga.lox([0, 1, 2, 3], [3, 2, 1, 0], 0, 1) == [0, 1, 3, 2]
+    assert ga.lox([0, 1, 2, 3], [3, 2, 1, 0], 2, 3) == [1, 0, 2, 3]
+    assert ga.lox([0, 1, 2, 3], [3, 2, 1, 0], 0, 3) == [0, 1, 2, 3]
+    assert ga.lox([2, 0, 1], [1, 2, 0], 1, 1) == [1, 0, 2]
+
+
+def test_lox_keeps_slice_and_order():
     from oracle.philox import Stream
     c, cfg, perm, ms = _setup(P=16)
     T = c.n_jobs
@@ -60,8 +71,8 @@ def test_ox1_keeps_slice_and_order():
         B = i if (ms[i], i) < (ms[j], j) else j
         a, b = sorted((((w[4] >> 16) * T) >> 16, ((w[5] & 0xFFFF) * T) >> 16))
         assert list(child_perm[a:b + 1]) == list(perm[A][a:b + 1])
-        rest = [x for x in np.roll(perm[B], -(b + 1)) if x not in set(perm[A][a:b + 1])]
-        filled = [child_perm[(b + 1 + k) % T] for k in range(T - (b - a + 1))]
+        rest = [x for x in perm[B] if x not in set(perm[A][a:b + 1])]
+        filled = list(child_perm[:a]) + list(child_perm[b + 1:])
         assert filled == rest
         for t in range(T):
             assert child_cfg[t] == (cfg[A][t] if (w[9] >> t) & 1 else cfg[B][t])

@@ -15,7 +15,7 @@ name = sys.argv[2] if len(sys.argv) > 2 else "TXT"
 S.load_library(lib)
 inst = synth.by_name(name, 0)
 plan = S.Plan(inst.node_gpus, 0).load_runtime_table(inst.runtime)
-n = 1 << 24
+n = (1 << 24) if name != "SWEEP" else (1 << 21)
 c, p = synth.random_genomes(plan.num_configs(), n, seed=5)
 c, p = torch.from_numpy(c).cuda(), torch.from_numpy(p).cuda()
 out = torch.empty(n, dtype=torch.int32, device="cuda")
