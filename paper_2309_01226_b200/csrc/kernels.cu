@@ -712,22 +712,6 @@ __device__ __forceinline__ void load_row(uint8_t* row, const uint8_t* __restrict
     d[4 * k + 3] = v.w;
   }
 }
-// Store one 16-byte chunk (index k) of a record into a smem row (4-byte stores: rows are
-// only 4-byte aligned), and copy chunks k0.. of a global record.
-__device__ __forceinline__ void put_quad(uint8_t* row, int k, const uint4 v) {
-  uint32_t* d = reinterpret_cast<uint32_t*>(row) + 4 * k;
-  d[0] = v.x;
-  d[1] = v.y;
-  d[2] = v.z;
-  d[3] = v.w;
-}
-__device__ __forceinline__ void load_row_from(uint8_t* row, const uint8_t* __restrict__ g, int k0, int GS) {
-  const uint4* src = reinterpret_cast<const uint4*>(g);
-  for (int k = k0; k < GS / 16; ++k) put_quad(row, k, src[k]);
-}
-#ifndef SAT_GA_EARLY_LOAD
-#define SAT_GA_EARLY_LOAD 0   // 1: parent records requested before the Philox blocks (A/B)
-#endif
 __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t* row, int GS) {
   uint4* dst = reinterpret_cast<uint4*>(g);
   const uint32_t* s = reinterpret_cast<const uint32_t*>(row);
@@ -825,36 +809,6 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         A = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
         B = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
       }
-#if SAT_GA_EARLY_LOAD
-      // 2. child = A (elites: the elite record).  The first 32 bytes of both parent records
-      //    are requested now and consumed after the Philox blocks, which hide their latency.
-      const uint8_t* srcA = elite ? rec_gen + slot * GS : prev_pop + (uint64_t)A * GS;
-      const uint8_t* srcB = prev_pop + (uint64_t)B * GS;
-      const int nq = GS >> 4;
-      uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
-      if (elite || child) {
-        a0 = reinterpret_cast<const uint4*>(srcA)[0];
-        if (nq > 1) a1 = reinterpret_cast<const uint4*>(srcA)[1];
-      }
-      if (child) {
-        b0 = reinterpret_cast<const uint4*>(srcB)[0];
-        if (nq > 1) b1 = reinterpret_cast<const uint4*>(srcB)[1];
-      }
-      prefetch(slot + nthr);
-      const uint4 w1 = rw.block(1), w2 = rw.block(2);
-      rw.blk = 2;
-      rw.cur = w2;
-      if (elite || child) {
-        put_quad(ch.base, 0, a0);
-        if (nq > 1) put_quad(ch.base, 1, a1);
-        load_row_from(ch.base, srcA, 2, GS);
-      }
-      if (child) {
-        put_quad(gb.base, 0, b0);
-        if (nq > 1) put_quad(gb.base, 1, b1);
-        load_row_from(gb.base, srcB, 2, GS);
-      }
-#else
       prefetch(slot + nthr);
       const uint4 w1 = rw.block(1), w2 = rw.block(2);
       rw.blk = 2;
@@ -865,7 +819,6 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         load_row(ch.base, prev_pop + (uint64_t)A * GS, GS);
         load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
       }
-#endif
       const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
       const bool xo = child && (w1.x & 0xffffu) < px16;
       uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
