@@ -724,8 +724,15 @@ struct GaMinBlocks {
 #ifndef SAT_GA_MINB_SMALL
 #define SAT_GA_MINB_SMALL 8
 #endif
+#ifndef SAT_GA_MINB_16
+#define SAT_GA_MINB_16 6   // measured r1: MIX k_ga 0.811 -> 0.780 ms (5: 0.784, 8: 0.780 with spills)
+#endif
+#ifndef SAT_GA_MINB_32
+#define SAT_GA_MINB_32 4   // measured r1: 5 and 6 lose on SWEEP (its shared memory caps it at 3 CTAs anyway)
+#endif
   static constexpr int value = NN == 0 ? (GP <= 8 ? 6 : (GP <= 16 ? 4 : 2))
-                                       : (STATE <= 8 ? SAT_GA_MINB_SMALL : (STATE <= 32 ? 4 : 2));
+                                       : (STATE <= 8 ? SAT_GA_MINB_SMALL
+                                                     : (STATE <= 16 ? SAT_GA_MINB_16 : (STATE <= 32 ? SAT_GA_MINB_32 : 2)));
 };
 
 // Child construction follows oracle/ga.py (GA v4): every Philox
