@@ -339,7 +339,8 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   p->Gmax = max_gpus;
   Problem pb{};
   pb.blob = p->blob.p;
-  pb.blob_bytes = bytes;
+  pb.blob_bytes = std::min(bytes, (4 * T * stride + T + 15) & ~15);   // tab + S (staged by the decoders)
+  pb.full_bytes = bytes;
   pb.T = T;
   pb.stride = stride;
   pb.N = (int)p->gpu_n.size();

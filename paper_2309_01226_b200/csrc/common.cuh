@@ -19,11 +19,13 @@ constexpr uint32_t R_MASK = 0x00ffffffu; // config word = (g << 24) | R, R < 2^2
 
 // Problem description passed by value to every kernel.  The packed config table
 // (u32 words, job-major, `stride` words per job) is followed in the same allocation by
-// S[t] (u8, configs per job); `blob_bytes` (multiple of 16) covers both so one bulk copy
-// stages everything into shared memory.
+// S[t] (u8, configs per job) and the UPP id of every config; `blob_bytes` (multiple of 16)
+// covers the table and S so one bulk copy stages what the decoders read into shared memory
+// (the UPP ids only matter to the trace decoder, which stages `full_bytes`).
 struct Problem {
-  const uint8_t* blob;     // device: tab[T*stride] u32, then S[T] u8, zero padded
-  int blob_bytes;
+  const uint8_t* blob;     // device: tab[T*stride] u32, then S[T] u8, then upp[T*stride] u8, zero padded
+  int blob_bytes;          // staged prefix: tab + S, rounded up to 16 (all the decoders read)
+  int full_bytes;          // the whole blob incl. the UPP ids (the trace decoder only)
   int T;                   // jobs
   int stride;              // words per job row = max_t S_t
   int N;                   // nodes

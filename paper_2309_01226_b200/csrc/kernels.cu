@@ -309,24 +309,28 @@ cudaError_t launch_evaluate(const Problem& pb, int NN, int GP, int kind, const u
 #undef SAT_EVAL
     return cudaErrorInvalidConfiguration;
   }
-  const size_t smem = warp_smem_bytes(pb);
+  Problem pw = pb;               // the warp decoder stages the UPP ids too
+  pw.blob_bytes = pb.full_bytes;
+  const size_t smem = warp_smem_bytes(pw);
   int seg = 1;
   while (seg < pb.sumG) seg <<= 1;
   const int64_t per_block = (int64_t)(WARP_B / 32) * (32 / seg);
   const int g = grid_for(k_eval_warp<false>, WARP_B, smem, sms, (n + per_block - 1) / per_block);
-  k_eval_warp<false><<<g, WARP_B, smem, st>>>(pb, cfg, perm, n, out, nullptr);
+  k_eval_warp<false><<<g, WARP_B, smem, st>>>(pw, cfg, perm, n, out, nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_trace(const Problem& pb, const uint8_t* cfg, const uint8_t* perm, int64_t n, void* placements,
                          int32_t* out, int sms, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  const size_t smem = warp_smem_bytes(pb);
+  Problem pw = pb;               // the trace reads the UPP ids
+  pw.blob_bytes = pb.full_bytes;
+  const size_t smem = warp_smem_bytes(pw);
   int seg = 1;
   while (seg < pb.sumG) seg <<= 1;
   const int64_t per_block = (int64_t)(WARP_B / 32) * (32 / seg);
   const int g = grid_for(k_eval_warp<true>, WARP_B, smem, sms, (n + per_block - 1) / per_block);
-  k_eval_warp<true><<<g, WARP_B, smem, st>>>(pb, cfg, perm, n, out, static_cast<Placement*>(placements));
+  k_eval_warp<true><<<g, WARP_B, smem, st>>>(pw, cfg, perm, n, out, static_cast<Placement*>(placements));
   return cudaGetLastError();
 }
 
@@ -694,10 +698,10 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
 
 // ------------------------------------------------------------------ K3 (+K1): GA
 // Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
-// then parent B, then the LOX slice bit set for T > 32 (8 words, interleaved per thread).
+// then parent B, then the LOX slice bit set for T > 32 (ceil(T/32) words, interleaved per thread).
 static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
   return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)2 * GA_B * odd_row_stride(GS) +
-         (size_t)4 * 8 * GA_B + 8 * GA_B + 8;
+         (size_t)4 * ((pb.T + 31) / 32) * GA_B + 8 * GA_B + 8;
 }
 
 // Copy a GS-byte global record into a smem row (4-byte stores) and back.
@@ -754,7 +758,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   uint8_t* s_child = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
   uint8_t* s_B = s_child + GA_B * RS;
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + GA_B * RS);
-  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + 8 * GA_B);   // [GA_B / 32][32]
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);   // [GA_B / 32][32]
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
