@@ -48,6 +48,22 @@ __device__ __forceinline__ int sel_fma(int p, int a, int b) {
   asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(p), "r"(d), "r"(a));
   return r;
 }
+// mux on the FMA pipe: a[k] via the same binary tree, each level a sel_fma on one bit of k.
+template <int GP>
+__device__ __forceinline__ int mux_fma(const int (&a)[GP], int k) {
+  if constexpr (GP == 1) {
+    return a[0];
+  } else {
+    int v[GP / 2];
+    const int p = k & 1;
+#pragma unroll
+    for (int i = 0; i < GP / 2; ++i) v[i] = sel_fma(p, a[2 * i], a[2 * i + 1]);
+    return mux_fma<GP / 2>(v, k >> 1);
+  }
+}
+#ifndef SAT_FMA_MUX
+#define SAT_FMA_MUX 0          // 1: multi-node starts by a mux tree on the FMA pipe (A/B)
+#endif
 #ifndef SAT_FMA_SEL_STAGES
 #define SAT_FMA_SEL_STAGES 8   // all barrel-shift stages (measured r1: +5 % TXT, +8 % MIX evaluate)
 #endif
@@ -174,11 +190,11 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
       v = place_sorted<GP>(a[0], g, R);
     } else {
       // start of every node: its g-th smallest free time (+inf if it has fewer GPUs)
-      int best = mux<GP>(a[0], g - 1);
+      int best = SAT_FMA_MUX ? mux_fma<GP>(a[0], g - 1) : mux<GP>(a[0], g - 1);
       int bn = 0;
 #pragma unroll
       for (int n = 1; n < NN; ++n) {
-        const int st = mux<GP>(a[n], g - 1);
+        const int st = SAT_FMA_MUX ? mux_fma<GP>(a[n], g - 1) : mux<GP>(a[n], g - 1);
         const bool lt = st < best;   // strict: ties keep the lowest node id
         best = lt ? st : best;
         bn = lt ? n : bn;

@@ -88,8 +88,15 @@ __device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E, 
 }
 
 // ------------------------------------------------------------------ K1: evaluate (T design)
+// Genome tiles are double-buffered (TMA of tile i+1 behind the decode of tile i) while two
+// buffers stay small; long genomes (SWEEP, T = 100: 51 KB) use one buffer, so that more CTAs
+// fit per SM (the decode needs warps more than it needs the copy overlap).
+#ifndef SAT_EVAL_DB_LIMIT
+#define SAT_EVAL_DB_LIMIT 16384
+#endif
+__host__ __device__ __forceinline__ int eval_nbuf(int T) { return 4 * EVAL_TILE * T <= SAT_EVAL_DB_LIMIT ? 2 : 1; }
 size_t eval_smem_bytes(const Problem& pb, int NN, int GP) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B) + 4u * EVAL_TILE * pb.T +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B) + 2u * eval_nbuf(pb.T) * EVAL_TILE * pb.T +
          4u * EVAL_B * ((pb.T + 31) / 32) + 3 * 8;
 }
 
@@ -102,8 +109,9 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
   const int tileB = EVAL_TILE * T;  // bytes per array per tile (multiple of 16)
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B);   // [2 buffers][cfg | perm]
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 4 * tileB);
+  const int nbuf = eval_nbuf(T);
+  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B);   // [nbuf buffers][cfg | perm]
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 2 * nbuf * tileB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_mask + EVAL_B * ((T + 31) / 32));
   const int64_t ntiles = (n + EVAL_TILE - 1) / EVAL_TILE;
   const int tid = threadIdx.x;
@@ -129,13 +137,13 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
 
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
+    const int buf = (nbuf == 2) ? (it & 1) : 0;
     uint8_t* bc = s_g + buf * 2 * tileB;
     uint8_t* bp = bc + tileB;
     const int64_t first = tile * EVAL_TILE;
     const bool full = use_bulk && first + EVAL_TILE <= n;
     if (full) {
-      mbar_wait(&bars[buf], (it >> 1) & 1);
+      mbar_wait(&bars[buf], (nbuf == 2 ? (it >> 1) : it) & 1);
     } else {  // ragged last tile (or unaligned caller buffers): plain cooperative loads
       const int cnt = (int)min((int64_t)EVAL_TILE, n - first) * T;
       for (int k = tid; k < cnt; k += EVAL_B) {
@@ -144,7 +152,7 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
       }
       __syncthreads();
     }
-    if (tid == 0) {  // prefetch the next tile into the other buffer
+    if (nbuf == 2 && tid == 0) {  // prefetch the next tile into the other buffer
       const int64_t nt = tile + gridDim.x;
       if (use_bulk && nt < ntiles && (nt + 1) * EVAL_TILE <= n) {
         uint8_t* nc = s_g + (buf ^ 1) * 2 * tileB;
@@ -182,6 +190,15 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
       }
     }
     __syncthreads();
+    if (nbuf == 1 && tid == 0) {  // one buffer: the next tile's copy starts once it is free
+      const int64_t nt = tile + gridDim.x;
+      if (use_bulk && nt < ntiles && (nt + 1) * EVAL_TILE <= n) {
+        fence_proxy_async();
+        mbar_expect_tx(&bars[0], 2 * tileB);
+        bulk_g2s(s_g, gcfg + nt * tileB, tileB, &bars[0]);
+        bulk_g2s(s_g + tileB, gperm + nt * tileB, tileB, &bars[0]);
+      }
+    }
   }
 }
 
@@ -871,15 +888,17 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
             wp = (wp == pa) ? wp + gap : wp;
           }
         } else {
+          // Rows of lanes without a child (elites, past the population) hold stale bytes: the
+          // word index is clamped so those lanes stay inside this thread's ceil(T/32) words.
           for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
           for (int q = (int)a; q <= (int)b; ++q) {
             const int x = ch.q(q);
-            inA[(x >> 5) * GA_B] |= 1u << (x & 31);
+            inA[min(x >> 5, nb - 1) * GA_B] |= 1u << (x & 31);
           }
           const uint32_t xm = xo ? 1u : 0u;
           for (int k = 0; k < T; ++k) {
             const int x = gb.q(k);
-            const uint32_t take = (~inA[(x >> 5) * GA_B] >> (x & 31)) & xm;
+            const uint32_t take = (~inA[min(x >> 5, nb - 1) * GA_B] >> (x & 31)) & xm;
             if (take) *wp = (uint8_t)x;
             wp += take;
             wp = (wp == pa) ? wp + gap : wp;

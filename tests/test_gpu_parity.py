@@ -659,3 +659,25 @@ def test_bench_scale_search_sampled_replay(sat, torch, name):
     best, pl, bc, bp = plan.best_plan()
     ms, _ = oracle.decode(c, bc, bp)
     assert ms == best == r["makespan"] and oracle.validate(c, pl, best) == []
+
+
+def test_empty_inputs(sat, torch):
+    """Degenerate sizes: evaluating zero genomes is a no-op (output untouched), an empty
+    enumeration range reports nothing found, and the first/last single-genome ranges equal
+    the oracle's decode of those indices."""
+    inst = synth.tiny(0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    plan = _plan(sat, inst)
+    T = c.n_jobs
+    out = torch.full((4,), -7, dtype=torch.int32, device="cuda")
+    plan.evaluate(torch.zeros((0, T), dtype=torch.uint8, device="cuda"),
+                  torch.zeros((0, T), dtype=torch.uint8, device="cuda"), out[:0])
+    assert (out.cpu().numpy() == -7).all()
+    r = plan.enumerate_range(5, 5)
+    assert r["evaluated"] == 0
+    size = plan.space_size()
+    for i in (0, size - 1):
+        r = plan.enumerate_range(i, i + 1)
+        assert r["evaluated"] == 1 and r["genome_index"] == i
+        cfg, perm = oracle.unrank(c, i)
+        assert r["makespan"] == oracle.decode(c, cfg, perm)[0]
