@@ -716,8 +716,14 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
 // ------------------------------------------------------------------ K3 (+K1): GA
 // Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
 // then parent B, then the LOX slice bit set for T > 32 (ceil(T/32) words, interleaved per thread).
+// Long genomes (T > 32) read parent B straight from the population in global memory (L1)
+// instead of staging it: one row per thread instead of two lets more CTAs fit per SM.
+#ifndef SAT_GA_B_GLOBAL
+#define SAT_GA_B_GLOBAL 1
+#endif
+__host__ __device__ __forceinline__ int ga_rows(int T) { return (SAT_GA_B_GLOBAL && T > 32) ? 1 : 2; }
 static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)2 * GA_B * odd_row_stride(GS) +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)ga_rows(pb.T) * GA_B * odd_row_stride(GS) +
          (size_t)4 * ((pb.T + 31) / 32) * GA_B + 8 * GA_B + 8;
 }
 
@@ -773,8 +779,8 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   uint8_t* s_child = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
-  uint8_t* s_B = s_child + GA_B * RS;
-  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_B + GA_B * RS);
+  uint8_t* s_B = s_child + GA_B * RS;   // (T <= 32 only)
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_child + ga_rows(T) * GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);   // [GA_B / 32][32]
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
@@ -845,7 +851,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       if (elite) load_row(ch.base, rec_gen + slot * GS, GS);
       if (child) {
         load_row(ch.base, prev_pop + (uint64_t)A * GS, GS);
-        load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
+        if (ga_rows(T) == 2) load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
       }
       const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
       const bool xo = child && (w1.x & 0xffffu) < px16;
@@ -854,15 +860,26 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       // 3. uniform crossover of the config genes (bits from words 9 .. 9+nb-1), 4 genes per step
       {
         const uint32_t* ca = reinterpret_cast<const uint32_t*>(ch.base);
-        const uint32_t* cb = reinterpret_cast<const uint32_t*>(gb.base);
         uint32_t* cw = reinterpret_cast<uint32_t*>(ch.base);
         uint32_t bits = 0;
-        for (int t = 0; t < T; t += 4) {
-          if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
-          const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;     // 1 -> take B's gene
-          const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;  // nibble -> byte mask
-          const uint32_t wa = ca[t >> 2], wb = cb[t >> 2];
-          cw[t >> 2] = (wa & ~m) | (wb & m);                               // pad bytes: 0 in both
+        if (ga_rows(T) == 2) {
+          const uint32_t* cb = reinterpret_cast<const uint32_t*>(gb.base);
+          for (int t = 0; t < T; t += 4) {
+            if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
+            const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;     // 1 -> take B's gene
+            const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;  // nibble -> byte mask
+            const uint32_t wa = ca[t >> 2], wb = cb[t >> 2];
+            cw[t >> 2] = (wa & ~m) | (wb & m);                               // pad bytes: 0 in both
+          }
+        } else {   // B's config words from the population (global, L1-cached)
+          const uint32_t* cb = reinterpret_cast<const uint32_t*>(prev_pop + (uint64_t)B * GS);
+          for (int t = 0; t < T; t += 4) {
+            if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
+            const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;
+            const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
+            const uint32_t wa = ca[t >> 2], wb = cb[t >> 2];
+            cw[t >> 2] = (wa & ~m) | (wb & m);
+          }
         }
       }
       // 4. LOX (linear order crossover): keep A.perm[a..b] in place; fill positions 0..a-1,
@@ -896,8 +913,9 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
             inA[min(x >> 5, nb - 1) * GA_B] |= 1u << (x & 31);
           }
           const uint32_t xm = xo ? 1u : 0u;
+          const uint8_t* Bq = (ga_rows(T) == 2) ? gb.base + Tp : prev_pop + (uint64_t)B * GS + Tp;
           for (int k = 0; k < T; ++k) {
-            const int x = gb.q(k);
+            const int x = Bq[k];
             const uint32_t take = (~inA[min(x >> 5, nb - 1) * GA_B] >> (x & 31)) & xm;
             if (take) *wp = (uint8_t)x;
             wp += take;
