@@ -280,6 +280,22 @@ saturn_status saturn_introspect(saturn_plan *p, const saturn_introspect_params *
 saturn_status saturn_get_unique_id(uint8_t *id128);
 saturn_status saturn_plan_attach_comm(saturn_plan *p, const uint8_t *id128, int32_t rank, int32_t world);
 
+/* Multi-GPU without NCCL (row e; SURVEY.md §8e "B200-native alternative"): the `world`
+ * ranks of one node (one process per GPU) pass the same fresh POSIX shared-memory name
+ * ("/saturn_<nonce>", created by rank 0, removed once every rank is attached).  Each rank
+ * exports a device exchange buffer with CUDA IPC and maps every peer's; the elite exchange
+ * of saturn_search then PUSHES this island's E records into block `rank` of every rank's
+ * buffer (device-to-device over NVLink, or within one device), passes a shared-memory
+ * barrier and merges its own buffer -- the blocks an NCCL all-gather would produce, so the
+ * island protocol and its results are those of saturn_plan_attach_comm / search_group.
+ * saturn_enumerate reduces (MIN key, SUM leaves) the same way.  Collective and blocking;
+ * a rank that does not arrive within SATURN_PEER_TIMEOUT_S (default 120 s) fails the others
+ * with ECUDA instead of hanging.  Host-only handles attach the barrier alone (tests).
+ * world <= 8.  ESTATE if the handle already has an NCCL communicator (and vice versa). */
+saturn_status saturn_plan_attach_peers(saturn_plan *p, const char *name, int32_t rank, int32_t world);
+/* Barrier over the ranks of the peer link (ESTATE without one). */
+saturn_status saturn_plan_barrier(saturn_plan *p);
+
 /* Contiguous slice [begin, end) of [0, total) owned by `rank` of `world` (pure host). */
 saturn_status saturn_partition(uint64_t total, int32_t rank, int32_t world, uint64_t *begin, uint64_t *end);
 

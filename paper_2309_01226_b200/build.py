@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsaturn.so")
-SOURCES = ["kernels.cu", "api.cu"]
-HEADERS = ["common.cuh", "decode.cuh", "kernels.h"]
+SOURCES = ["kernels.cu", "api.cu", "peers.cu"]
+HEADERS = ["common.cuh", "decode.cuh", "kernels.h", "peers.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -40,7 +40,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = True) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -48,10 +48,15 @@ def build(force: bool = False, verbose: bool = True) -> str:
                "-I" + _nccl_include(), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    procs = [subprocess.Popen(c) for c in cmds]          # the sources compile in parallel
+    codes = [pr.wait() for pr in procs]
+    for c, rc in zip(cmds, codes):
+        if rc:
+            raise subprocess.CalledProcessError(rc, c)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-o", LIB] + objs + [
-        "-ldl"]
+        "-ldl", "-lrt"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

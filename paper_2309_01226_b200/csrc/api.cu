@@ -1,6 +1,6 @@
 // libsaturn host runtime: the C ABI of include/saturn.h (row b), table validation and
-// compaction (rows a1/a2), workspace management, the search epoch loop and the NCCL
-// island exchange (row e).
+// compaction (rows a1/a2), workspace management, the search epoch loop and the island
+// exchange (row e) over NCCL or over peer memory (peers.h).
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -17,6 +17,7 @@
 #include "../../include/saturn.h"
 #include "kernels.h"
 #include "decode.cuh"
+#include "peers.h"
 
 using sat::Problem;
 
@@ -138,8 +139,9 @@ struct saturn_plan {
   int32_t* hist_pin = nullptr;
   std::vector<cudaEvent_t> hist_ev;   // [0] = start of the search, [1 + k] = record k
   int hist_n = 0;
-  // communicator
+  // communicator: NCCL, or the peer-memory link (one of the two)
   ncclComm_t comm = nullptr;
+  std::unique_ptr<sat::PeerLink> peers;
   int rank = 0, world = 1;
   // measurement
   bool profiling = false;
@@ -522,6 +524,31 @@ void unrank_host(const saturn_plan* p, uint64_t G, std::vector<uint8_t>& cfg, st
   }
 }
 
+// ---- peer-memory exchange helpers (row e without NCCL; peers.h)
+bool distributed(const saturn_plan* p) { return p->world > 1 && (p->comm || p->peers); }
+
+// MIN of key[0] and SUM of key[1] over the ranks: push this rank's pair into slot `rank` of
+// every rank's exchange buffer, barrier, reduce the own buffer's slots on the host, barrier
+// (so the next call's pushes cannot overtake a slow reader).  `key` is device memory [2].
+saturn_status peer_reduce_keys(saturn_plan* p, unsigned long long* key, cudaStream_t st,
+                               unsigned long long out[2]) {
+  sat::PeerLink& L = *p->peers;
+  for (int q = 0; q < L.world; ++q)
+    CU(p, cudaMemcpyAsync(L.peer[q] + sat::PeerLayout::keys + 16 * L.rank, key, 16, cudaMemcpyDeviceToDevice, st));
+  CU(p, cudaStreamSynchronize(st));
+  if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
+  unsigned long long all[2 * sat::PEER_MAX];
+  CU(p, cudaMemcpy(all, L.local + sat::PeerLayout::keys, 16 * L.world, cudaMemcpyDeviceToHost));
+  out[0] = ~0ull;
+  out[1] = 0;
+  for (int q = 0; q < L.world; ++q) {
+    out[0] = std::min(out[0], all[2 * q]);
+    out[1] += all[2 * q + 1];
+  }
+  if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
+  return SATURN_OK;
+}
+
 saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint64_t total, bool collective,
                              cudaStream_t st, saturn_result* out) {
   const double t0 = now_s();
@@ -543,12 +570,21 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
   CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, p->ws_key.p, p->sms, st));
   p->stats.kernel_launches += 1;
   p->stats.d2h_bytes += 8;
+  unsigned long long key = 0;
   if (collective && p->comm) {
     NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
   }
-  unsigned long long key = 0;
-  CU(p, cudaMemcpyAsync(&key, p->ws_key.p, sizeof key, cudaMemcpyDeviceToHost, st));
-  CU(p, cudaStreamSynchronize(st));
+  if (collective && p->peers && p->world > 1) {
+    CU(p, p->ws_key.ensure(2));
+    CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, sizeof(unsigned long long), st));
+    unsigned long long r[2];
+    saturn_status sr = peer_reduce_keys(p, p->ws_key.p, st, r);
+    if (sr != SATURN_OK) return sr;
+    key = r[0];
+  } else {
+    CU(p, cudaMemcpyAsync(&key, p->ws_key.p, sizeof key, cudaMemcpyDeviceToHost, st));
+    CU(p, cudaStreamSynchronize(st));
+  }
   if (out) {
     memset(out, 0, sizeof *out);
     out->evaluated = collective ? total : (end - begin);
@@ -640,8 +676,13 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
     NC(p, nccl().allReduce(p->ws_key.p + 1, p->ws_key.p + 1, 1, ncclUint64, ncclSum, p->comm, st));
   }
   unsigned long long kl[2] = {0, 0};
-  CU(p, cudaMemcpyAsync(kl, p->ws_key.p, sizeof kl, cudaMemcpyDeviceToHost, st));
-  CU(p, cudaStreamSynchronize(st));
+  if (p->peers && p->world > 1) {
+    saturn_status sr = peer_reduce_keys(p, p->ws_key.p, st, kl);
+    if (sr != SATURN_OK) return sr;
+  } else {
+    CU(p, cudaMemcpyAsync(kl, p->ws_key.p, sizeof kl, cudaMemcpyDeviceToHost, st));
+    CU(p, cudaStreamSynchronize(st));
+  }
   p->stats.d2h_bytes += sizeof kl;
   const uint64_t idx = kl[0] & ((uint64_t(1) << 38) - 1);
   if (idx == (uint64_t(1) << 38) - 1) return fail(p, SATURN_ECUDA, "enumeration found no leaf");
@@ -937,7 +978,7 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   is.sp = sp;
   is.st = static_cast<cudaStream_t>(stream);
   is.island = (uint32_t)p->rank;
-  is.world = (p->comm && p->world > 1) ? p->world : 1;
+  is.world = distributed(p) ? p->world : 1;
   saturn_status s;
   if ((s = is.validate()) != SATURN_OK) return s;
   if ((s = is.begin()) != SATURN_OK) return s;
@@ -950,6 +991,28 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     if ((e = is.memetic()) != SATURN_OK) return e;
     if (is.world < 2) return SATURN_OK;
     DeviceGuard dg(p->device);
+    if (p->peers) {
+      // push this island's E records into block `rank` of every rank's exchange buffer
+      // (epoch-parity half), barrier, merge the own buffer: the same blocks the NCCL
+      // all-gather would have produced
+      sat::PeerLink& L = *p->peers;
+      if (E > sat::PEER_EMAX || GS > sat::PEER_GSMAX) return fail(p, SATURN_EINVAL, "peer exchange: E or genome too large");
+      const int par = (int)(L.exchanges++ & 1);
+      const size_t ms_off = sat::PeerLayout::ms0 + par * sat::PeerLayout::ms_bytes;
+      const size_t gen_off = sat::PeerLayout::gen0 + par * sat::PeerLayout::gen_bytes;
+      for (int q = 0; q < L.world; ++q) {
+        CU(p, cudaMemcpyAsync(L.peer[q] + ms_off + (size_t)4 * E * L.rank, p->rec_ms.p, (size_t)4 * E,
+                              cudaMemcpyDeviceToDevice, st));
+        CU(p, cudaMemcpyAsync(L.peer[q] + gen_off + (size_t)E * GS * L.rank, p->rec_gen.p, (size_t)E * GS,
+                              cudaMemcpyDeviceToDevice, st));
+      }
+      CU(p, cudaStreamSynchronize(st));
+      if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
+      CU(p, sat::launch_merge_elites(reinterpret_cast<const int32_t*>(L.local + ms_off), L.local + gen_off, L.world,
+                                     E, GS, p->rec_ms.p, p->rec_gen.p, st));
+      p->stats.kernel_launches += 1;
+      return SATURN_OK;
+    }
     NC(p, nccl().allGather(p->rec_ms.p, p->all_ms.p, (size_t)E, ncclInt32, p->comm, st));
     NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
     return is.merge();
@@ -966,7 +1029,16 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
         // The stop decision must be collective: every island runs the same number of
         // epochs, or the elite all-gathers would mismatch.  MAX-all-reduce of the flag.
         int stop = (now_s() - is.t0 >= sp->time_budget_s) ? 1 : 0;
-        if (is.world > 1) {
+        if (is.world > 1 && p->peers) {   // any rank's flag: SUM of the flags > 0
+          DeviceGuard dg(p->device);
+          CU(p, p->ws_key.ensure(2));
+          const unsigned long long kf[2] = {~0ull, (unsigned long long)stop};
+          CU(p, cudaMemcpyAsync(p->ws_key.p, kf, sizeof kf, cudaMemcpyHostToDevice, st));
+          unsigned long long r[2];
+          saturn_status sr = peer_reduce_keys(p, p->ws_key.p, st, r);
+          if (sr != SATURN_OK) return sr;
+          stop = r[1] > 0 ? 1 : 0;
+        } else if (is.world > 1) {
           DeviceGuard dg(p->device);
           CU(p, p->flag.ensure(1));
           CU(p, cudaMemcpyAsync(p->flag.p, &stop, sizeof stop, cudaMemcpyHostToDevice, st));
@@ -995,7 +1067,8 @@ saturn_status saturn_search_group(saturn_plan** plans, int32_t k, const saturn_s
     saturn_plan* p = plans[r];
     if (!p) return SATURN_EINVAL;
     if (host_only(p)) return SATURN_ESTATE;
-    if (p->comm) return fail(p, SATURN_ESTATE, "search_group islands must not have an NCCL communicator");
+    if (p->comm || p->peers)
+      return fail(p, SATURN_ESTATE, "search_group islands must not have an NCCL communicator or a peer link");
     for (int q = 0; q < r; ++q)
       if (plans[q] == p) return fail(p, SATURN_EINVAL, "the same handle twice in a group");
     isl[r].p = p;
@@ -1442,6 +1515,7 @@ saturn_status saturn_plan_attach_comm(saturn_plan* p, const uint8_t* id128, int3
   if (!p) return SATURN_EINVAL;
   if (!id128 || world < 1 || rank < 0 || rank >= world) return fail(p, SATURN_EINVAL, "bad rank/world");
   if (!nccl().ok) return fail(p, SATURN_ENCCL, "%s", nccl().why.c_str());
+  if (p->peers) return fail(p, SATURN_ESTATE, "attach_comm: the handle already has a peer link");
   DeviceGuard dg(p->device);
   if (p->comm) {
     nccl().commDestroy(p->comm);
@@ -1452,6 +1526,33 @@ saturn_status saturn_plan_attach_comm(saturn_plan* p, const uint8_t* id128, int3
   NC(p, nccl().commInitRank(&p->comm, world, id, rank));
   p->rank = rank;
   p->world = world;
+  return SATURN_OK;
+}
+
+saturn_status saturn_plan_attach_peers(saturn_plan* p, const char* name, int32_t rank, int32_t world) {
+  if (!p) return SATURN_EINVAL;
+  if (!name || name[0] != '/' || world < 1 || world > sat::PEER_MAX || rank < 0 || rank >= world)
+    return fail(p, SATURN_EINVAL, "attach_peers: need a '/name', 1 <= world <= 8 and 0 <= rank < world");
+  if (p->comm) return fail(p, SATURN_ESTATE, "attach_peers: the handle already has an NCCL communicator");
+  std::unique_ptr<sat::PeerLink> L(new sat::PeerLink());
+  const char* to = getenv("SATURN_PEER_TIMEOUT_S");
+  const double timeout = to ? atof(to) : 120.0;
+  if (host_only(p)) {
+    if (!L->attach(name, rank, world, -1, timeout)) return fail(p, SATURN_ECUDA, "%s", L->err.c_str());
+  } else {
+    DeviceGuard dg(p->device);
+    if (!L->attach(name, rank, world, p->device, timeout)) return fail(p, SATURN_ECUDA, "%s", L->err.c_str());
+  }
+  p->peers = std::move(L);
+  p->rank = rank;
+  p->world = world;
+  return SATURN_OK;
+}
+
+saturn_status saturn_plan_barrier(saturn_plan* p) {
+  if (!p) return SATURN_EINVAL;
+  if (!p->peers) return fail(p, SATURN_ESTATE, "barrier: no peer link (saturn_plan_attach_peers)");
+  if (!p->peers->barrier()) return fail(p, SATURN_ECUDA, "%s", p->peers->err.c_str());
   return SATURN_OK;
 }
 
@@ -1519,6 +1620,7 @@ void saturn_plan_destroy(saturn_plan* p) {
   {
     DeviceGuard dg(p->device);
     if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
+    p->peers.reset();
     p->blob.release();
     if (p->pinned) cudaFreeHost(p->pinned);
     p->ws_cfg.release();

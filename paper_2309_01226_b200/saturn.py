@@ -29,6 +29,7 @@ EXPORTS = (
     "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_nodes", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
     "saturn_enumerate", "saturn_enumerate_range", "saturn_set_enumeration_options", "saturn_search", "saturn_search_group", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
+    "saturn_plan_attach_peers", "saturn_plan_barrier",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
     "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_improve", "saturn_last_error",
     "saturn_plan_destroy",
@@ -128,6 +129,8 @@ def load_library(path: str = LIB_PATH):
         "saturn_best_plan": [h, P(Placement), P(u8), P(i64)],
         "saturn_get_unique_id": [P(u8)],
         "saturn_plan_attach_comm": [h, P(u8), i32, i32],
+        "saturn_plan_attach_peers": [h, ctypes.c_char_p, i32, i32],
+        "saturn_plan_barrier": [h],
         "saturn_partition": [u64, i32, i32, P(u64), P(u64)],
         "saturn_probe_int_peak": [h, P(ctypes.c_double)],
         "saturn_set_profiling": [h, i32],
@@ -436,6 +439,15 @@ class Plan:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         self._check(self._lib.saturn_plan_attach_comm(self._h, buf, rank, world), "saturn_plan_attach_comm")
 
+    def attach_peers(self, name: str, rank: int, world: int):
+        """Peer-memory transport (saturn_plan_attach_peers): `name` is a fresh '/...' shm name
+        shared by the `world` ranks of one node."""
+        self._check(self._lib.saturn_plan_attach_peers(self._h, name.encode(), rank, world),
+                    "saturn_plan_attach_peers")
+
+    def barrier(self):
+        self._check(self._lib.saturn_plan_barrier(self._h), "saturn_plan_barrier")
+
     def baseline_genome(self, kind: str, seed: int = 0):
         """The paper's baselines as genomes (row f2): kind in max | min | optimus | random."""
         T = self.n_jobs
@@ -517,6 +529,23 @@ def broadcast_unique_id(group=None) -> bytes:
         buf = buf.cuda()
     dist.broadcast(buf, src=0, group=group)
     return bytes(buf.cpu().tolist())
+
+
+def peer_name() -> str:
+    """A fresh POSIX shared-memory name for saturn_plan_attach_peers."""
+    import uuid
+    return f"/saturn_{os.getpid()}_{uuid.uuid4().hex[:16]}"
+
+
+def attach_peers(plan: Plan, group=None) -> str:
+    """Peer-memory transport over the ranks of a torch.distributed group on one node (row e
+    without NCCL): rank 0 draws the shared-memory name, the group broadcasts it."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    obj = [peer_name() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    plan.attach_peers(obj[0], rank, dist.get_world_size(group))
+    return obj[0]
 
 
 def attach_distributed(plan: Plan, group=None):
