@@ -175,7 +175,10 @@ class ClockSampler:
 def _config(args, extra):
     cfg = {"workload": WORKLOADS[args.workload], "table_seed": 0, "population_per_gpu": args.population,
            "generations_per_step": args.generations, "elites": args.elites,
-           "parallelism": f"islands x{args.gpus} (one GA population per GPU, NCCL elite exchange)",
+           "parallelism": f"islands x{args.gpus} (one GA population per GPU, elite exchange over "
+                          f"{os.environ.get('SATURN_TRANSPORT', 'nccl')})"
+                          + (" -- all ranks on ONE GPU (SATURN_SHARE_GPU=1, functional check only)"
+                             if os.environ.get("SATURN_SHARE_GPU") == "1" else ""),
            "l2": "inputs larger than L2: two population buffers of P genomes x genome stride "
                  "(>= 2 x 128 MB at the default P) > 126 MB L2"}
     if extra:
@@ -220,15 +223,31 @@ def main():
     import synth
     import paper_2309_01226_b200 as sat
 
+    # The library's island exchange runs over NCCL (default) or over peer memory
+    # (SATURN_TRANSPORT=peers: CUDA IPC + a shared-memory barrier); torch.distributed only
+    # carries the host plumbing (barriers, max over ranks) -- over gloo with the peer
+    # transport.  SATURN_SHARE_GPU=1 puts every rank on cuda:0 (a functional check of the
+    # multi-rank path on a one-GPU box; its numbers are not a scaling measurement).
+    transport = os.environ.get("SATURN_TRANSPORT", "nccl")
+    share = os.environ.get("SATURN_SHARE_GPU") == "1"
+    if share and transport != "peers":
+        raise SystemExit("SATURN_SHARE_GPU=1 needs SATURN_TRANSPORT=peers (NCCL refuses two ranks on one GPU)")
+    local = 0 if share else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if transport == "peers":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     inst = synth.by_name(args.workload, 0)
     plan = sat.Plan(inst.node_gpus, local).load_runtime_table(inst.runtime)
     if world > 1:
-        sat.attach_distributed(plan)
+        if transport == "peers":
+            sat.attach_peers(plan)
+        else:
+            sat.attach_distributed(plan)
     T = inst.n_jobs
     P, G, E = args.population, args.generations, args.elites
     scfg = sat.SearchConfig(seed=2309, population=P, max_generations=G, elites=E,
@@ -244,7 +263,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if transport == "peers" else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
