@@ -96,3 +96,25 @@ def test_two_process_islands_and_enumeration_over_peer_memory():
         assert (er["makespan"], er["genome_index"]) == (one["makespan"], one["genome_index"])
         assert (er["makespan"], er["genome_index"]) == oracle.brute_force(ct)
         assert er["leaves"] > 0   # per-rank pruning differs from one process: leaves are not compared
+
+
+def test_bench_two_ranks_over_peer_memory_on_one_gpu():
+    """bench.py's multi-rank path end to end (torchrun, barriers, max-over-ranks device time,
+    the island exchange) with both ranks on this pool's one GPU over the peer transport."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ, SATURN_TRANSPORT="peers", SATURN_SHARE_GPU="1", SATURN_PEER_TIMEOUT_S="60")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--population", "65536", "--generations", "4",
+           "--no-cpu-baseline", "--kernel-only-n", "0"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and "peers" in line["config"]["parallelism"]
+    # 2 ranks x (P + 4 (P - E)) full decodes per step
+    assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
