@@ -549,6 +549,33 @@ saturn_status peer_reduce_keys(saturn_plan* p, unsigned long long* key, cudaStre
   return SATURN_OK;
 }
 
+// Fused enumeration collective over peer memory: the enumeration kernel of every rank folds
+// its best (makespan << 38 | index) key with atomicMin -- and its leaf count with atomicAdd
+// -- straight into ONE slot pair in rank 0's exchange buffer (a remote atomic over NVLink
+// for the other GPUs), and the DFS reads that slot as its live branch-and-bound incumbent,
+// so every rank prunes with every rank's best.  begin: rank 0 initialises the pair, barrier;
+// end: barrier after all kernels, read the pair, barrier (before the next call re-inits).
+unsigned long long* peer_shared_slot(saturn_plan* p) {
+  return reinterpret_cast<unsigned long long*>(p->peers->peer[0] + sat::PeerLayout::shared);
+}
+saturn_status peer_shared_begin(saturn_plan* p, const unsigned long long init[2], cudaStream_t st) {
+  sat::PeerLink& L = *p->peers;
+  if (L.rank == 0) {
+    CU(p, cudaMemcpyAsync(peer_shared_slot(p), init, 16, cudaMemcpyHostToDevice, st));
+    CU(p, cudaStreamSynchronize(st));
+  }
+  if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
+  return SATURN_OK;
+}
+saturn_status peer_shared_end(saturn_plan* p, cudaStream_t st, unsigned long long out[2]) {
+  sat::PeerLink& L = *p->peers;
+  CU(p, cudaStreamSynchronize(st));
+  if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
+  CU(p, cudaMemcpy(out, peer_shared_slot(p), 16, cudaMemcpyDeviceToHost));
+  if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
+  return SATURN_OK;
+}
+
 saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint64_t total, bool collective,
                              cudaStream_t st, saturn_result* out) {
   const double t0 = now_s();
@@ -565,23 +592,26 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
   if (s != SATURN_OK) return s;
   if (kind != SATURN_DECODER_THREAD)
     return fail(p, SATURN_EINVAL, "enumerate needs the thread decoder for this cluster shape");
-  CU(p, p->ws_key.ensure(1));
-  CU(p, cudaMemsetAsync(p->ws_key.p, 0xff, sizeof(unsigned long long), st));
-  CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, p->ws_key.p, p->sms, st));
-  p->stats.kernel_launches += 1;
-  p->stats.d2h_bytes += 8;
   unsigned long long key = 0;
-  if (collective && p->comm) {
-    NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
-  }
-  if (collective && p->peers && p->world > 1) {
-    CU(p, p->ws_key.ensure(2));
-    CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, sizeof(unsigned long long), st));
+  p->stats.d2h_bytes += 8;
+  if (collective && p->peers && p->world > 1) {   // fused: the kernel reduces into rank 0's slot
+    const unsigned long long init[2] = {~0ull, 0ull};
+    saturn_status sr = peer_shared_begin(p, init, st);
+    if (sr != SATURN_OK) return sr;
+    CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, peer_shared_slot(p), p->sms, st));
+    p->stats.kernel_launches += 1;
     unsigned long long r[2];
-    saturn_status sr = peer_reduce_keys(p, p->ws_key.p, st, r);
+    sr = peer_shared_end(p, st, r);
     if (sr != SATURN_OK) return sr;
     key = r[0];
   } else {
+    CU(p, p->ws_key.ensure(1));
+    CU(p, cudaMemsetAsync(p->ws_key.p, 0xff, sizeof(unsigned long long), st));
+    CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, p->ws_key.p, p->sms, st));
+    p->stats.kernel_launches += 1;
+    if (collective && p->comm) {
+      NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
+    }
     CU(p, cudaMemcpyAsync(&key, p->ws_key.p, sizeof key, cudaMemcpyDeviceToHost, st));
     CU(p, cudaStreamSynchronize(st));
   }
@@ -664,22 +694,28 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
       if (ms[k] > 0) inc = std::min(inc, ms[k]);
   }
   const unsigned long long init = ((unsigned long long)inc << 38) | ((1ull << 38) - 1ull);
-  CU(p, p->ws_key.ensure(2));
-  CU(p, cudaMemcpyAsync(p->ws_key.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
-  CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, sizeof(unsigned long long), st));
   uint64_t rb = 0, re = ds.n_roots;
   saturn_partition(ds.n_roots, p->rank, p->world, &rb, &re);
-  CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st));
-  p->stats.kernel_launches += 1;
-  if (p->comm && p->world > 1) {
-    NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
-    NC(p, nccl().allReduce(p->ws_key.p + 1, p->ws_key.p + 1, 1, ncclUint64, ncclSum, p->comm, st));
-  }
   unsigned long long kl[2] = {0, 0};
-  if (p->peers && p->world > 1) {
-    saturn_status sr = peer_reduce_keys(p, p->ws_key.p, st, kl);
+  if (p->peers && p->world > 1) {   // fused: live shared incumbent + reduction in rank 0's slot
+    const unsigned long long iv[2] = {init, 0ull};
+    saturn_status sr = peer_shared_begin(p, iv, st);
+    if (sr != SATURN_OK) return sr;
+    unsigned long long* g = peer_shared_slot(p);
+    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, g, g + 1, p->sms, st));
+    p->stats.kernel_launches += 1;
+    sr = peer_shared_end(p, st, kl);
     if (sr != SATURN_OK) return sr;
   } else {
+    CU(p, p->ws_key.ensure(2));
+    CU(p, cudaMemcpyAsync(p->ws_key.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
+    CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, sizeof(unsigned long long), st));
+    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st));
+    p->stats.kernel_launches += 1;
+    if (p->comm && p->world > 1) {
+      NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
+      NC(p, nccl().allReduce(p->ws_key.p + 1, p->ws_key.p + 1, 1, ncclUint64, ncclSum, p->comm, st));
+    }
     CU(p, cudaMemcpyAsync(kl, p->ws_key.p, sizeof kl, cudaMemcpyDeviceToHost, st));
     CU(p, cudaStreamSynchronize(st));
   }

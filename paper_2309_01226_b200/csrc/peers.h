@@ -25,6 +25,8 @@ constexpr int PEER_GSMAX = 528;    // genome record bytes for T <= 255
 struct PeerLayout {
   static constexpr size_t keys = 0;                                   // u64 [PEER_MAX][2]
   static constexpr size_t flags = keys + 16 * PEER_MAX;               // i32 [PEER_MAX]
+  static constexpr size_t shared = 192;                               // u64 [2]: the fused enumeration's
+                                                                      // (key, leaves), used in rank 0's buffer
   static constexpr size_t ms0 = 256;                                  // i32 [2][PEER_MAX * E]
   static constexpr size_t ms_bytes = 4 * PEER_MAX * PEER_EMAX;
   static constexpr size_t gen0 = ms0 + 2 * ms_bytes;                  // u8 [2][PEER_MAX * E * GS]
