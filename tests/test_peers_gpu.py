@@ -47,7 +47,11 @@ def _worker(rank, world, port, q):
         ep = sat.Plan(tv.node_gpus, 0).load_runtime_table(tv.runtime)
         sat.attach_peers(ep)
         er = ep.enumerate()
-        q.put((rank, r, pop, best[0], best[2], best[3], rt, er, None))
+        tb = synth.tiny_variant(7, 7, (4,))          # the bench's instance: 6.8e10 genomes, DFS
+        bp = sat.Plan(tb.node_gpus, 0).load_runtime_table(tb.runtime)
+        sat.attach_peers(bp)
+        er7 = bp.enumerate()
+        q.put((rank, r, pop, best[0], best[2], best[3], rt, (er, er7), None))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, None, None, None, None, None, None, None, repr(e)))
     dist.destroy_process_group()
@@ -91,11 +95,14 @@ def test_two_process_islands_and_enumeration_over_peer_memory():
     tv = synth.tiny_variant(45, 5, (2, 2))
     one = sat.Plan(tv.node_gpus, 0).load_runtime_table(tv.runtime).enumerate()
     ct = oracle.compact(tv.node_gpus, tv.runtime)
+    tb = synth.tiny_variant(7, 7, (4,))
+    one7 = sat.Plan(tb.node_gpus, 0).load_runtime_table(tb.runtime).enumerate()
     for rank in range(2):
-        er = res[rank][7]
+        er, er7 = res[rank][7]
         assert (er["makespan"], er["genome_index"]) == (one["makespan"], one["genome_index"])
         assert (er["makespan"], er["genome_index"]) == oracle.brute_force(ct)
         assert er["leaves"] > 0   # per-rank pruning differs from one process: leaves are not compared
+        assert (er7["makespan"], er7["genome_index"]) == (one7["makespan"], one7["genome_index"])
 
 
 def test_bench_two_ranks_over_peer_memory_on_one_gpu():
