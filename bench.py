@@ -362,6 +362,11 @@ def main():
             "same_result": (er["makespan"], er["genome_index"]) == (fr["makespan"], fr["genome_index"])}
         kernel_only["unit"] = UNIT
         kernel_only["genomes"] = n
+        # the decode kernel alone against the same ALU roofline (algorithmic ops per plan)
+        kernel_only["roofline_thread"] = {"bound": "alu", "achieved": ops * kernel_only["thread"] / 1e12,
+                                          "peak": ALU_PEAK_OPS / 1e12, "unit": "TOP/s",
+                                          "frac": ops * kernel_only["thread"] / ALU_PEAK_OPS,
+                                          "kernel": "k_evaluate (T design, validity-checked decode)"}
         kernel_only["int_probe_ops_per_s"] = plan.probe_int_peak()
 
     if rank != 0:
