@@ -902,7 +902,8 @@ struct Island {
                                     p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st,
                                     timed ? p->ev_pool[3 * (gen - 1) + 1] : nullptr));
     if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * (gen - 1) + 2], st));
-    CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st));
+    CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st,
+                             /*few=*/true));   // generations >= 1 append only keys beating the E-th elite
     p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
     evaluated += (uint64_t)(P - E);
     cur = nxt;

@@ -1294,9 +1294,38 @@ __global__ void __launch_bounds__(1024) k_select(const unsigned long long* __res
   }
 }
 
+// One warp: after generation 0 only the children that beat the current E-th elite are
+// appended (typically tens), so a single warp walks them without the block-wide merge.
+__global__ void __launch_bounds__(32) k_select_warp(const unsigned long long* __restrict__ cand,
+                                                    int* __restrict__ n_cand, int E, int GS,
+                                                    const uint8_t* __restrict__ pop, int32_t* __restrict__ rec_ms,
+                                                    uint8_t* __restrict__ rec_gen) {
+  const int lane = threadIdx.x;
+  const int n = *n_cand;
+  uint64_t lst = ~0ull;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    topE_insert(lst, (i < n) ? cand[i] : ~0ull, E);
+  }
+  if (lane < E) {
+    const uint32_t slot = (uint32_t)(lst & 0xffffffffu);
+    rec_ms[lane] = (int32_t)(lst >> 32);
+    const uint4* src = reinterpret_cast<const uint4*>(pop + (uint64_t)slot * GS);
+    uint4* dst = reinterpret_cast<uint4*>(rec_gen + (uint64_t)lane * GS);
+    for (int k2 = 0; k2 < GS / 16; ++k2) dst[k2] = src[k2];
+  }
+  if (lane == 0) *n_cand = 0;
+}
+#ifndef SAT_SELECT_WARP
+#define SAT_SELECT_WARP 1
+#endif
+
 cudaError_t launch_select(const unsigned long long* cand, int* n_cand, int E, int GS, const uint8_t* pop,
-                          int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st) {
-  k_select<<<1, 1024, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);
+                          int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st, bool few) {
+  if (SAT_SELECT_WARP && few)
+    k_select_warp<<<1, 32, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);
+  else
+    k_select<<<1, 1024, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);
   return cudaGetLastError();
 }
 

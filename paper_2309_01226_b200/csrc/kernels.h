@@ -83,7 +83,7 @@ bool ga_is_split();
 int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms);
 // Top-E of the *d_n_cand candidate keys -> elite records (ms, genome) copied from `pop`.
 cudaError_t launch_select(const unsigned long long* cand, int* d_n_cand, int E, int GS, const uint8_t* pop,
-                          int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st);
+                          int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st, bool few = false);
 // Island migration: the E best of W ranks' gathered records by (ms, rank, position).
 cudaError_t launch_merge_elites(const int32_t* all_ms, const uint8_t* all_gen, int W, int E, int GS,
                                 int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st);

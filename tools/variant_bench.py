@@ -36,7 +36,14 @@ plan.set_profiling(True)
 for _ in range(10):
     r = plan.search(cfg)
 st = plan.stats()
-print(json.dumps({"lib": os.path.basename(lib), "workload": name, "evaluate_plans_per_s": ev,
+plan.set_profiling(False)
+a.record()
+for _ in range(10):
+    plan.search(cfg)
+b.record()
+torch.cuda.synchronize()
+step_ms = a.elapsed_time(b) / 10
+print(json.dumps({"lib": lib, "workload": name, "evaluate_plans_per_s": ev, "step_ms": step_ms,
                   "ga_kernel_ms": st["ga_kernel_ms"] / st["ga_launches"],
                   "ga_children_per_s": st["ga_decodes"] / (st["ga_kernel_ms"] * 1e-3), "best": r["makespan"],
                   "breed_ms": st.get("breed_kernel_ms", 0) / st["ga_launches"],
