@@ -317,6 +317,9 @@ typedef struct {
   double breed_kernel_ms;   /* of which the GA-operator (breed) kernel, split mode   */
   double decode_kernel_ms;  /* and the population decode kernel (fused: everything) */
 } saturn_stats;
+/* on = 0: off; on = n >= 1: time every n-th GA generation kernel of saturn_search with CUDA
+ * events on the launching stream (1 = all; an event record between two kernels costs a few
+ * microseconds, so bench.py samples every 4th). */
 saturn_status saturn_set_profiling(saturn_plan *p, int32_t on);
 saturn_status saturn_get_stats(const saturn_plan *p, saturn_stats *out);
 saturn_status saturn_reset_stats(saturn_plan *p);

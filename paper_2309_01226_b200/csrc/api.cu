@@ -144,7 +144,7 @@ struct saturn_plan {
   std::unique_ptr<sat::PeerLink> peers;
   int rank = 0, world = 1;
   // measurement
-  bool profiling = false;
+  int profiling = 0;          // 0: off; n >= 1: time every n-th GA generation with CUDA events
   saturn_stats stats{};
   std::vector<cudaEvent_t> ev_pool;
   std::string err;
@@ -798,7 +798,7 @@ struct Island {
   sat::GaParams gp{};
   uint64_t evaluated = 0;
   int cur = 0;
-  int64_t n_prof = 0;
+  int64_t n_prof = 0, n_timed = 0;
   double t0 = 0;
 
   saturn_status validate() {
@@ -880,8 +880,11 @@ struct Island {
                               p->pms[0].p, p->cand.p, p->n_cand.p, p->sms, st));
     CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
     p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
-    // profiling: event triples around the GA generation kernels (first 512 per search)
-    n_prof = p->profiling ? std::min<int64_t>(sp->max_generations, 512) : 0;
+    // profiling: event triples around every `profiling`-th GA generation kernel (at most 512
+    // per search).  An event record between kernels costs a few microseconds of drain, so
+    // sampling keeps the instrumented step within ~1 % of the uninstrumented one.
+    n_prof = p->profiling ? std::min<int64_t>(sp->max_generations / p->profiling + 1, 512) : 0;
+    n_timed = 0;
     while ((int64_t)p->ev_pool.size() < 3 * n_prof) {
       cudaEvent_t e;
       CU(p, cudaEventCreate(&e));
@@ -896,12 +899,17 @@ struct Island {
     DeviceGuard dg(p->device);
     gp.gen = (uint32_t)gen;
     const int nxt = cur ^ 1;
-    const bool timed = gen <= n_prof;
-    if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * (gen - 1)], st));
+    const int per = p->profiling;
+    const bool timed = per > 0 && n_timed < n_prof && (gen % per) == (per / 2) % per;
+    const int64_t ti = n_timed;
+    if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * ti], st));
     CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
                                     p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st,
-                                    timed ? p->ev_pool[3 * (gen - 1) + 1] : nullptr));
-    if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * (gen - 1) + 2], st));
+                                    timed ? p->ev_pool[3 * ti + 1] : nullptr));
+    if (timed) {
+      CU(p, cudaEventRecord(p->ev_pool[3 * ti + 2], st));
+      ++n_timed;
+    }
     CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st,
                              /*few=*/true));   // generations >= 1 append only keys beating the E-th elite
     p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
@@ -971,7 +979,7 @@ struct Island {
     saturn_status hs = flush_history();   // synchronises the stream
     if (hs != SATURN_OK) return hs;
     p->stats.d2h_bytes += GS + sizeof best;
-    for (int64_t g = 1; g <= std::min<int64_t>(n_prof, gens_run); ++g) {
+    for (int64_t g = 1; g <= n_timed; ++g) {
       float ms = 0.f, m1 = 0.f;
       CU(p, cudaEventElapsedTime(&ms, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 2]));
       CU(p, cudaEventElapsedTime(&m1, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 1]));
@@ -1630,7 +1638,7 @@ saturn_status saturn_probe_int_peak(saturn_plan* p, double* int_ops_per_s) {
 
 saturn_status saturn_set_profiling(saturn_plan* p, int32_t on) {
   if (!p) return SATURN_EINVAL;
-  p->profiling = on != 0;
+  p->profiling = on < 0 ? 0 : on;
   return SATURN_OK;
 }
 

@@ -457,8 +457,9 @@ class Plan:
                                                      _np_ptr(q, ctypes.c_uint8)), "saturn_baseline_genome")
         return c, q
 
-    def set_profiling(self, on: bool = True):
-        self._check(self._lib.saturn_set_profiling(self._h, int(bool(on))), "saturn_set_profiling")
+    def set_profiling(self, on=True):
+        """False/0: off; True/1: time every GA generation; n >= 2: every n-th."""
+        self._check(self._lib.saturn_set_profiling(self._h, int(on)), "saturn_set_profiling")
 
     def stats(self) -> dict:
         st = Stats()

@@ -681,3 +681,18 @@ def test_empty_inputs(sat, torch):
         assert r["evaluated"] == 1 and r["genome_index"] == i
         cfg, perm = oracle.unrank(c, i)
         assert r["makespan"] == oracle.decode(c, cfg, perm)[0]
+
+
+def test_profiling_samples_generations(sat, torch):
+    """saturn_set_profiling(n): CUDA events around every n-th GA generation kernel."""
+    inst = synth.txt(0)
+    plan = _plan(sat, inst)
+    cfg = sat.SearchConfig(seed=1, population=4096, max_generations=16, elites=8, generations_per_epoch=4)
+    for per, want in ((0, 0), (1, 16), (4, 4), (16, 1)):
+        plan.set_profiling(per)
+        plan.reset_stats()
+        plan.search(cfg)
+        st = plan.stats()
+        assert st["ga_launches"] == want, (per, st)
+        assert (st["ga_kernel_ms"] > 0) == (want > 0)
+        assert st["ga_decodes"] == want * (4096 - 8)
