@@ -822,9 +822,15 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           load_row(ch.base, seeds + slot * GS, GS);
         } else {  // cfg[t] = U(S_t), then Fisher-Yates on the identity
           Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
-          for (int t = 0; t < GS; ++t) ch.base[t] = 0;
+          uint32_t* rw32 = reinterpret_cast<uint32_t*>(ch.base);   // zero the record (pads), 4 bytes a store
+          for (int k = 0; k < GS / 4; ++k) rw32[k] = 0u;
           for (int t = 0; t < T; ++t) ch.c(t) = (uint8_t)rng.below(S[t]);
-          for (int t = 0; t < T; ++t) ch.q(t) = (uint8_t)t;
+          uint32_t* pq = reinterpret_cast<uint32_t*>(ch.base + Tp);  // identity permutation, 4 genes a store
+          for (int k = 0; 4 * k < T; ++k) {
+            const int nb = T - 4 * k;
+            const uint32_t m = nb >= 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
+            pq[k] = (0x03020100u + 0x04040404u * (uint32_t)k) & m;
+          }
           for (int i = T - 1; i > 0; --i) {
             const int j = (int)rng.below(i + 1);
             const uint8_t a = ch.q(i);

@@ -620,7 +620,7 @@ def test_dfs_symmetry_reduction_matches_oracle(sat, torch, n_lrs, nodes):
 
 
 # ------------------------------------------------------------------ bench scale
-@pytest.mark.parametrize("name", ["TXT", "MIX"])
+@pytest.mark.parametrize("name", ["TXT", "MIX", "SWEEP"])
 def test_bench_scale_search_sampled_replay(sat, torch, name):
     """The launch configuration bench.py times (P = 2^22 genomes, E = 16, epochs of 8,
     seed 2309) at BASELINE.json's full sizes: generation 16 is checked against the oracle on
@@ -630,7 +630,9 @@ def test_bench_scale_search_sampled_replay(sat, torch, name):
     minimum and its trace re-validates."""
     inst = synth.by_name(name, 0)
     c = oracle.compact(inst.node_gpus, inst.runtime)
-    P, E, seed = 1 << 22, 16, 2309
+    # SWEEP (T = 100: parent B read from global memory, the LOX bit set in shared memory) at
+    # 2^20 genomes to bound the host copies (2 x 200 MB) and the Python replay
+    P, E, seed = (1 << 22) if name != "SWEEP" else (1 << 20), 16, 2309
     base = dict(seed=seed, population=P, elites=E, generations_per_epoch=8)
     px, pc, pm = oga.q32(0.9), oga.q32(0.5), oga.q32(0.5)
     plan = _plan(sat, inst)
@@ -648,7 +650,7 @@ def test_bench_scale_search_sampled_replay(sat, torch, name):
     assert np.array_equal(m16[:E], m15[order])
     # sampled children: operator replay + oracle decode
     rng = np.random.default_rng(7)
-    slots = np.unique(np.concatenate([rng.integers(E, P, 1500), [E, E + 1, P - 2, P - 1]]))
+    slots = np.unique(np.concatenate([rng.integers(E, P, 1500 if name != "SWEEP" else 400), [E, E + 1, P - 2, P - 1]]))
     kids = [oga.make_child(c.S, c15, q15, m15, int(k), 16, seed, 0, px, pc, pm) for k in slots]
     kc = np.array([k[0] for k in kids], np.uint8)
     kq = np.array([k[1] for k in kids], np.uint8)
