@@ -31,6 +31,7 @@ struct Problem {
   int N;                   // nodes
   int sumG;                // sum_n GPU_n
   int8_t gpu_n[MAX_NODES]; // GPU_n
+  int full_nodes;          // 1: one node with exactly GP GPUs (decode reads the makespan off the state)
 };
 
 __device__ __forceinline__ const uint32_t* tab_of(const uint8_t* blob) {

@@ -145,10 +145,27 @@ __host__ __device__ __forceinline__ int odd_row_stride(int bytes) {
 // CHECK = 0: genome trusted.  CHECK = 1 (T <= 32) / 2 (any T): invalid genomes (perm not a
 // permutation of 0..T-1, cfg[t] >= S_t) return -1; mode 1 keeps the seen-set in a register,
 // mode 2 in `mask` (this thread's ceil(T/32) scratch words, `mstride` words apart).
+// TRACK_MS = false (every node has exactly GP GPUs): the makespan is read off the final
+// state instead of a running max -- a GPU's free time is the end of its last job, every job
+// holds >= 1 GPU and a later job on a GPU ends later, so max_t (s_t + R_t) = max over the
+// GPUs of their final free time = max over nodes of the sorted vector's last slot.
+template <int NN, int GP, int CHECK, bool TRACK_MS, class G>
+__device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
+                                                  int stride, const G& gen, int T, const Problem& pb,
+                                                  uint32_t* mask, int mstride);
+
 template <int NN, int GP, int CHECK, class G>
 __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
                                              int stride, const G& gen, int T, const Problem& pb,
                                              uint32_t* mask = nullptr, int mstride = 0) {
+  if (pb.full_nodes) return decode_sorted_impl<NN, GP, CHECK, false>(tab, S, stride, gen, T, pb, mask, mstride);
+  return decode_sorted_impl<NN, GP, CHECK, true>(tab, S, stride, gen, T, pb, mask, mstride);
+}
+
+template <int NN, int GP, int CHECK, bool TRACK_MS, class G>
+__device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
+                                                  int stride, const G& gen, int T, const Problem& pb,
+                                                  uint32_t* mask, int mstride) {
   int a[NN][GP];
 #pragma unroll
   for (int n = 0; n < NN; ++n)
@@ -231,7 +248,11 @@ __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, c
           for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
       }
     }
-    ms = max(ms, v);
+    if constexpr (TRACK_MS) ms = max(ms, v);
+  }
+  if constexpr (!TRACK_MS) {
+#pragma unroll
+    for (int n = 0; n < NN; ++n) ms = max(ms, a[n][GP - 1]);
   }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;
   if constexpr (CHECK != 0) {
