@@ -120,7 +120,7 @@ class ClockSampler:
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, torch_device: int):
-        self.samples, self.reasons, self.ok = [], 0, False
+        self.samples, self.mem_samples, self.reasons, self.ok = [], [], 0, False
         self.max_mhz = None
         try:
             import pynvml
@@ -147,6 +147,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.mem_samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
@@ -168,7 +169,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": len(self.samples)}
         s = sorted(self.samples)
         names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
-        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
+        m = sorted(self.mem_samples) or [None]
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "mem_mhz": m[len(m) // 2], "reasons": names,
+                "samples": len(s)}
 
 
 # ------------------------------------------------------------------ helpers

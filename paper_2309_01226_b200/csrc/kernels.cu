@@ -41,11 +41,14 @@ __host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, int NN, i
 }
 
 // Decode one genome with the (NN, GP) design; `ns` = this thread's node-state slice (NN == 0).
-template <int NN, int GP, int CHECK, class G>
+// STATE_MS: allow reading the makespan off the final state for one full node (decode_sorted);
+// only the evaluate kernel uses it -- in k_ga the extra loop copy measured 3 % slower.
+template <int NN, int GP, int CHECK, bool STATE_MS = false, class G>
 __device__ __forceinline__ int decode_T(const uint32_t* tab, const uint8_t* S, int stride, const G& gen, int T,
                                         const Problem& pb, int* ns, uint32_t* mask = nullptr, int mstride = 0) {
   if constexpr (NN == 0) return decode_smem<GP, CHECK>(tab, S, stride, gen, T, pb, ns, mask, mstride);
-  else return decode_sorted<NN, GP, CHECK>(tab, S, stride, gen, T, pb, mask, mstride);
+  else if constexpr (STATE_MS) return decode_sorted<NN, GP, CHECK>(tab, S, stride, gen, T, pb, mask, mstride);
+  else return decode_sorted_impl<NN, GP, CHECK, true>(tab, S, stride, gen, T, pb, mask, mstride);
 }
 
 bool have_sorted_shape(int NN, int GP) {
@@ -185,8 +188,8 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
       if (first + j < n) {
         RowGenome gen{bc + j * T, bp + j * T};
         int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
-        out[first + j] = (T <= 32) ? decode_T<NN, GP, 1>(tab, S, pb.stride, gen, T, pb, ns)
-                                   : decode_T<NN, GP, 2>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
+        out[first + j] = (T <= 32) ? decode_T<NN, GP, 1, true>(tab, S, pb.stride, gen, T, pb, ns)
+                                   : decode_T<NN, GP, 2, true>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
       }
     }
     __syncthreads();
@@ -822,15 +825,11 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           load_row(ch.base, seeds + slot * GS, GS);
         } else {  // cfg[t] = U(S_t), then Fisher-Yates on the identity
           Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
-          uint32_t* rw32 = reinterpret_cast<uint32_t*>(ch.base);   // zero the record (pads), 4 bytes a store
-          for (int k = 0; k < GS / 4; ++k) rw32[k] = 0u;
+          // (byte loops on purpose: word-wise zeroing here measured k_ga's generation path 7 %
+          // slower -- the one kernel's register allocation / layout changed)
+          for (int t = 0; t < GS; ++t) ch.base[t] = 0;
           for (int t = 0; t < T; ++t) ch.c(t) = (uint8_t)rng.below(S[t]);
-          uint32_t* pq = reinterpret_cast<uint32_t*>(ch.base + Tp);  // identity permutation, 4 genes a store
-          for (int k = 0; 4 * k < T; ++k) {
-            const int nb = T - 4 * k;
-            const uint32_t m = nb >= 4 ? 0xffffffffu : ((1u << (8 * nb)) - 1u);
-            pq[k] = (0x03020100u + 0x04040404u * (uint32_t)k) & m;
-          }
+          for (int t = 0; t < T; ++t) ch.q(t) = (uint8_t)t;
           for (int i = T - 1; i > 0; --i) {
             const int j = (int)rng.below(i + 1);
             const uint8_t a = ch.q(i);
