@@ -261,8 +261,12 @@ def test_search_best_is_valid_and_monotone(sat, torch):
     ms, opl = oracle.decode(c, bc, bp)
     assert ms == best and oracle.validate(c, pl, best) == []
     assert best >= oracle.lower_bound(c)
-    _, hist = plan.search_history()
+    ts, hist = plan.search_history()
+    # one record per epoch (after generation 0, every 4 generations, and the final exchange),
+    # device seconds since the search's first operation: non-decreasing, best non-increasing
+    assert len(hist) == 1 + 40 // 4 + 1 and hist[-1] == best
     assert all(a >= b for a, b in zip(hist, hist[1:]))
+    assert ts[0] > 0 and all(a <= b for a, b in zip(ts, ts[1:])) and ts[-1] <= r["seconds"]
     assert r["evaluated"] == (1 << 14) + 40 * ((1 << 14) - 16)
     # determinism
     r2 = plan.search(sat.SearchConfig(seed=1, population=1 << 14, max_generations=40, elites=16,
