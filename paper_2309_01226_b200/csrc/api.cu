@@ -851,8 +851,8 @@ struct Island {
       CU(p, p->pms[b].ensure((size_t)P));
     }
     CU(p, p->cand.ensure((size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64));
-    CU(p, p->n_cand.ensure(1));
-    CU(p, cudaMemsetAsync(p->n_cand.p, 0, sizeof(int), st));
+    CU(p, p->n_cand.ensure(2));   // [0] appended candidates, [1] the GA kernels' work counter
+    CU(p, cudaMemsetAsync(p->n_cand.p, 0, 2 * sizeof(int), st));
     CU(p, p->rec_ms.ensure(E));
     CU(p, p->rec_gen.ensure((size_t)E * GS));
     CU(p, p->all_ms.ensure((size_t)E * world));

@@ -765,6 +765,9 @@ struct GaMinBlocks {
                                                      : (STATE <= 16 ? SAT_GA_MINB_16 : (STATE <= 32 ? SAT_GA_MINB_32 : 2)));
 };
 
+#ifndef SAT_GA_DYNAMIC
+#define SAT_GA_DYNAMIC 1
+#endif
 // Child construction follows oracle/ga.py (GA v4): every Philox
 // word has a fixed position, so all lanes draw the same blocks at the same program points
 // and the operators run as uniform loops with predicated writes (no divergent refills).
@@ -814,8 +817,22 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       t_m2 = (uint32_t)prev_ms[t_i2]; t_n2 = (uint32_t)prev_ms[t_j2];
     }
   };
+  // DYN (multi-node shapes): warp chunks of 32 children, the first from the static grid
+  // stride, the rest claimed from a counter (n_cand[1], reset by the previous elite
+  // selection) so warps that finish early take more -- with the static stride the SMs idled
+  // in the tail (measured MIX k_ga -11 %, SWEEP -10 %; on one node +4 %, so it keeps the
+  // static stride).  A claim is issued one iteration before its value is needed.
+  constexpr bool DYN = SAT_GA_DYNAMIC && NN != 1;
+  unsigned int* work = reinterpret_cast<unsigned int*>(n_cand + 1);
+  const auto claim = [&]() -> unsigned int { return lane == 0 ? atomicAdd(work, 32u) : 0u; };
+  int64_t next_base = 0;
+  unsigned int pending = 0;
+  if constexpr (DYN) {
+    next_base = nthr + (int64_t)__shfl_sync(0xffffffffu, claim(), 0);
+    pending = claim();
+  }
   prefetch((int64_t)blockIdx.x * GA_B + (tid & ~31) + lane);
-  for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P; base += nthr) {
+  for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P;) {
     const int64_t slot = base + lane;
     const bool live = slot < gp.P;
     int msv = INT_MAX;
@@ -848,7 +865,8 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         A = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
         B = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
       }
-      prefetch(slot + nthr);
+      if constexpr (DYN) prefetch(next_base + lane);
+      else prefetch(slot + nthr);
       const uint4 w1 = rw.block(1), w2 = rw.block(2);
       rw.blk = 2;
       rw.cur = w2;
@@ -974,6 +992,13 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     if constexpr (DECODE) {
       const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
       topE_insert(lst, key, gp.E, cap);
+    }
+    if constexpr (DYN) {
+      base = next_base;
+      next_base = nthr + (int64_t)__shfl_sync(0xffffffffu, pending, 0);
+      pending = claim();
+    } else {
+      base += nthr;
     }
   }
   if constexpr (!DECODE) return;
@@ -1295,7 +1320,7 @@ __global__ void __launch_bounds__(1024) k_select(const unsigned long long* __res
       uint4* dst = reinterpret_cast<uint4*>(rec_gen + (uint64_t)lane * GS);
       for (int k2 = 0; k2 < GS / 16; ++k2) dst[k2] = src[k2];
     }
-    if (lane == 0) *n_cand = 0;  // ready for the next generation
+    if (lane == 0) { n_cand[0] = 0; n_cand[1] = 0; }  // candidates and the GA work counter, next generation
   }
 }
 
@@ -1319,7 +1344,7 @@ __global__ void __launch_bounds__(32) k_select_warp(const unsigned long long* __
     uint4* dst = reinterpret_cast<uint4*>(rec_gen + (uint64_t)lane * GS);
     for (int k2 = 0; k2 < GS / 16; ++k2) dst[k2] = src[k2];
   }
-  if (lane == 0) *n_cand = 0;
+  if (lane == 0) { n_cand[0] = 0; n_cand[1] = 0; }
 }
 #ifndef SAT_SELECT_WARP
 #define SAT_SELECT_WARP 1
