@@ -368,7 +368,7 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   // makespan read off the final state (decode_sorted) for one full node: measured r1 TXT
   // evaluate +2.7 %, k_ga -0.8 %; on 2x8 (MIX) the second loop copy cost k_ga 1 %, so
   // multi-node shapes keep the running max
-  p->pb.full_nodes = (p->NN == 1 && p->gpu_n.size() == 1 && p->gpu_n[0] == p->GP) ? 1 : 0;
+  p->pb.full_nodes = (p->NN == 1 && p->gpu_n.size() == 1 && p->gpu_n[0] == p->GP && p->GP >= 8) ? 1 : 0;
   if (sat::eval_smem_bytes(pb, p->NN, p->GP) > 227 * 1024)
     return fail(p, SATURN_ELIMIT, "evaluate tile exceeds shared memory");
   p->loaded = true;
@@ -559,6 +559,15 @@ saturn_status peer_reduce_keys(saturn_plan* p, unsigned long long* key, cudaStre
 // for the other GPUs), and the DFS reads that slot as its live branch-and-bound incumbent,
 // so every rank prunes with every rank's best.  begin: rank 0 initialises the pair, barrier;
 // end: barrier after all kernels, read the pair, barrier (before the next call re-inits).
+// Dynamic DFS root scheduling (the counter in ws_key[2]); SATURN_DFS_STATIC=1: static stride.
+unsigned long long* dfs_work(saturn_plan* p) {
+  static const bool stat = [] {
+    const char* e = getenv("SATURN_DFS_STATIC");
+    return e && e[0] == '1';
+  }();
+  return stat ? nullptr : p->ws_key.p + 2;
+}
+
 unsigned long long* peer_shared_slot(saturn_plan* p) {
   return reinterpret_cast<unsigned long long*>(p->peers->peer[0] + sat::PeerLayout::shared);
 }
@@ -706,15 +715,18 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
     saturn_status sr = peer_shared_begin(p, iv, st);
     if (sr != SATURN_OK) return sr;
     unsigned long long* g = peer_shared_slot(p);
-    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, g, g + 1, p->sms, st));
+    CU(p, p->ws_key.ensure(3));
+    CU(p, cudaMemsetAsync(p->ws_key.p + 2, 0, sizeof(unsigned long long), st));   // this rank's root counter
+    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, g, g + 1, p->sms, st, dfs_work(p)));
     p->stats.kernel_launches += 1;
     sr = peer_shared_end(p, st, kl);
     if (sr != SATURN_OK) return sr;
   } else {
-    CU(p, p->ws_key.ensure(2));
+    CU(p, p->ws_key.ensure(3));
     CU(p, cudaMemcpyAsync(p->ws_key.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
-    CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, sizeof(unsigned long long), st));
-    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st));
+    CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, 2 * sizeof(unsigned long long), st));   // leaves, root counter
+    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st,
+                                    dfs_work(p)));
     p->stats.kernel_launches += 1;
     if (p->comm && p->world > 1) {
       NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));

@@ -500,6 +500,7 @@ cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace&
 
 // ------------------------------------------------------------------ K2b: DFS enumeration
 constexpr int DFS_B = 64;
+constexpr uint64_t DFS_BATCH = 4;   // roots per claim (dynamic root scheduling)
 // per-level thread-private words: state (NN*GP), ms, rperm lo/hi, rcfg lo/hi, used, t, c
 template <int NN, int GP>
 struct DfsLayout {
@@ -553,7 +554,8 @@ __device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R) {
 template <int NN, int GP>
 __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds, uint64_t root_begin,
                                                          uint64_t root_end, unsigned long long* best_key,
-                                                         unsigned long long* leaves_out) {
+                                                         unsigned long long* leaves_out,
+                                                         unsigned long long* work) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint8_t* s_blob = sm;
   int* s_lv = reinterpret_cast<int*>(sm + pb.blob_bytes);
@@ -570,8 +572,23 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
   const uint64_t C = ds.es.cfg_space;
 
   uint64_t best = ~0ull, leaves = 0;
-  for (uint64_t root = root_begin + (uint64_t)blockIdx.x * DFS_B + tid; root < root_end;
-       root += (uint64_t)gridDim.x * DFS_B) {
+  // Roots: pruning makes subtree sizes very uneven, so with `work` each thread takes a first
+  // batch of DFS_BATCH roots by its position and then claims further batches from the
+  // counter as it finishes (dynamic); without it, the static grid stride.
+  const uint64_t nthr = (uint64_t)gridDim.x * DFS_B;
+  const uint64_t gtid = (uint64_t)blockIdx.x * DFS_B + tid;
+  uint64_t batch_end = work ? min(root_begin + (gtid + 1) * DFS_BATCH, root_end) : root_begin + gtid + 1;
+  for (uint64_t root = work ? root_begin + gtid * DFS_BATCH : root_begin + gtid;; ++root) {
+    if (root >= batch_end) {
+      if (work) {
+        root = root_begin + nthr * DFS_BATCH + atomicAdd(work, (unsigned long long)DFS_BATCH);
+        batch_end = min(root + DFS_BATCH, root_end);
+      } else {
+        root = batch_end - 1 + nthr;
+        batch_end = root + 1;
+      }
+    }
+    if (root >= root_end) break;
     const int inc = (int)(*reinterpret_cast<volatile unsigned long long*>(best_key) >> 38);
     const int inc_ms = min(inc, (int)(best >> 38));
     int a[NN][GP];
@@ -698,7 +715,7 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
 
 cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
                                  uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,
-                                 int sms, cudaStream_t st) {
+                                 int sms, cudaStream_t st, unsigned long long* work) {
   if (root_end <= root_begin) return cudaSuccess;
   const size_t smem = dfs_smem_bytes(pb, NN, GP);
   const uint64_t total = root_end - root_begin;
@@ -708,7 +725,7 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
     const int g0 = grid_for(k_enumerate_dfs<A_, b>, DFS_B, smem, sms, 1 << 30);                    \
     const uint64_t need = (total + DFS_B - 1) / DFS_B;                                             \
     const int g = (int)(need < (uint64_t)g0 ? need : (uint64_t)g0);                                \
-    k_enumerate_dfs<A_, b><<<g, DFS_B, smem, st>>>(pb, ds, root_begin, root_end, best_key, leaves); \
+    k_enumerate_dfs<A_, b><<<g, DFS_B, smem, st>>>(pb, ds, root_begin, root_end, best_key, leaves, work); \
     return cudaGetLastError();                                                                     \
   }
   SAT_SHAPES(SAT_DFS)
@@ -752,7 +769,7 @@ template <int NN, int GP>
 struct GaMinBlocks {
   static constexpr int STATE = (NN == 0 ? 1 : NN) * GP;
 #ifndef SAT_GA_MINB_SMALL
-#define SAT_GA_MINB_SMALL 8
+#define SAT_GA_MINB_SMALL 7   // with dynamic chunks (SAT_GA_DYNAMIC_ONE); 8 without
 #endif
 #ifndef SAT_GA_MINB_16
 #define SAT_GA_MINB_16 6   // measured r1: MIX k_ga 0.811 -> 0.780 ms (5: 0.784, 8: 0.780 with spills)
@@ -761,13 +778,16 @@ struct GaMinBlocks {
 #define SAT_GA_MINB_32 4   // measured r1: 5 and 6 lose on SWEEP (its shared memory caps it at 3 CTAs anyway)
 #endif
   static constexpr int value = NN == 0 ? (GP <= 8 ? 6 : (GP <= 16 ? 4 : 2))
-                                       : (STATE <= 8 ? SAT_GA_MINB_SMALL
+                                       : (STATE < 8 ? 8 : STATE == 8 ? SAT_GA_MINB_SMALL
                                                      : (STATE <= 16 ? SAT_GA_MINB_16 : (STATE <= 32 ? SAT_GA_MINB_32 : 2)));
 };
 
 #ifndef SAT_GA_DYNAMIC
 #define SAT_GA_DYNAMIC 1
 #endif
+#ifndef SAT_GA_DYNAMIC_ONE
+#define SAT_GA_DYNAMIC_ONE 1   // one-node shapes too: with 7 CTAs/SM (72 registers) TXT k_ga
+#endif                         // 0.3374 -> 0.3286 ms; at 8 CTAs (64 registers) it lost 4 %
 // Child construction follows oracle/ga.py (GA v4): every Philox
 // word has a fixed position, so all lanes draw the same blocks at the same program points
 // and the operators run as uniform loops with predicated writes (no divergent refills).
@@ -817,12 +837,12 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       t_m2 = (uint32_t)prev_ms[t_i2]; t_n2 = (uint32_t)prev_ms[t_j2];
     }
   };
-  // DYN (multi-node shapes): warp chunks of 32 children, the first from the static grid
-  // stride, the rest claimed from a counter (n_cand[1], reset by the previous elite
-  // selection) so warps that finish early take more -- with the static stride the SMs idled
-  // in the tail (measured MIX k_ga -11 %, SWEEP -10 %; on one node +4 %, so it keeps the
-  // static stride).  A claim is issued one iteration before its value is needed.
-  constexpr bool DYN = SAT_GA_DYNAMIC && NN != 1;
+  // DYN: warp chunks of 32 children, the first from the static grid stride, the rest
+  // claimed from a counter (n_cand[1], reset by the previous elite selection) so warps that
+  // finish early take more -- with the static stride the SMs idled in the tail (measured
+  // MIX k_ga -11 %, SWEEP -10 %, TXT -2.6 % with 7 CTAs/SM).  A claim is issued one
+  // iteration before its value is needed.
+  constexpr bool DYN = SAT_GA_DYNAMIC && (NN != 1 || (SAT_GA_DYNAMIC_ONE && GP >= 8));   // (TINY 1x4: +13 %)
   unsigned int* work = reinterpret_cast<unsigned int*>(n_cand + 1);
   const auto claim = [&]() -> unsigned int { return lane == 0 ? atomicAdd(work, 32u) : 0u; };
   int64_t next_base = 0;

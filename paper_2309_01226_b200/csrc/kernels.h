@@ -54,7 +54,8 @@ struct DfsSpace {
 };
 cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
                                  uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,
-                                 int sms, cudaStream_t st);
+                                 int sms, cudaStream_t st,
+                                 unsigned long long* work = nullptr);
 
 struct GaParams {
   uint64_t seed;
