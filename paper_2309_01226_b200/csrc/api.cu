@@ -559,13 +559,16 @@ saturn_status peer_reduce_keys(saturn_plan* p, unsigned long long* key, cudaStre
 // for the other GPUs), and the DFS reads that slot as its live branch-and-bound incumbent,
 // so every rank prunes with every rank's best.  begin: rank 0 initialises the pair, barrier;
 // end: barrier after all kernels, read the pair, barrier (before the next call re-inits).
-// Dynamic DFS root scheduling (the counter in ws_key[2]); SATURN_DFS_STATIC=1: static stride.
+// DFS root scheduling: the static grid stride by default; SATURN_DFS_DYNAMIC=1 claims batches
+// of roots from a counter (ws_key[2]).  Measured r1: dynamic is slower (7 jobs on 1x4: 4.7 vs
+// 3.7 ms; 9 on 2x2: 0.83 vs 0.77 s) -- batches of consecutive roots find the good leaves
+// later, the shared incumbent tightens later and 30 % more leaves are visited.
 unsigned long long* dfs_work(saturn_plan* p) {
-  static const bool stat = [] {
-    const char* e = getenv("SATURN_DFS_STATIC");
+  static const bool dyn = [] {
+    const char* e = getenv("SATURN_DFS_DYNAMIC");
     return e && e[0] == '1';
   }();
-  return stat ? nullptr : p->ws_key.p + 2;
+  return dyn ? p->ws_key.p + 2 : nullptr;
 }
 
 unsigned long long* peer_shared_slot(saturn_plan* p) {
