@@ -772,7 +772,7 @@ struct GaMinBlocks {
 #define SAT_GA_MINB_SMALL 7   // with dynamic chunks (SAT_GA_DYNAMIC_ONE); 8 without
 #endif
 #ifndef SAT_GA_MINB_16
-#define SAT_GA_MINB_16 6   // measured r1: MIX k_ga 0.811 -> 0.780 ms (5: 0.784, 8: 0.780 with spills)
+#define SAT_GA_MINB_16 7   // measured r1 with dynamic chunks: MIX k_ga 0.690 (6) -> 0.680 ms (7); 5: 0.702
 #endif
 #ifndef SAT_GA_MINB_32
 #define SAT_GA_MINB_32 4   // measured r1: 5 and 6 lose on SWEEP (its shared memory caps it at 3 CTAs anyway)
