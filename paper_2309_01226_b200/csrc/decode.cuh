@@ -158,7 +158,9 @@ template <int NN, int GP, int CHECK, class G>
 __device__ __forceinline__ int decode_sorted(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
                                              int stride, const G& gen, int T, const Problem& pb,
                                              uint32_t* mask = nullptr, int mstride = 0) {
-  if (pb.full_nodes) return decode_sorted_impl<NN, GP, CHECK, false>(tab, S, stride, gen, T, pb, mask, mstride);
+  if constexpr (NN == 1 && GP >= 8) {   // (the only shapes the host flags; smaller ones keep one loop copy)
+    if (pb.full_nodes) return decode_sorted_impl<NN, GP, CHECK, false>(tab, S, stride, gen, T, pb, mask, mstride);
+  }
   return decode_sorted_impl<NN, GP, CHECK, true>(tab, S, stride, gen, T, pb, mask, mstride);
 }
 
