@@ -197,6 +197,25 @@ struct DeviceGuard {
 
 int gs_of(int T) { return sat::record_bytes(T); }  // cfg | pad | perm | pad
 
+// Decoder shape for the evaluate kernel: 4-node register states (SWEEP 4x8) are ALU-bound on
+// their gather/scatter selects, and there the shared-memory node-state decoder (dynamic
+// indexing on the LSU pipe) measured faster: evaluate 1.15e9 -> 1.37e9 plans/s (its GA
+// kernel is slower, so k_ga keeps the register states).  MIX 2x8: equal -> registers.
+// SATURN_EVAL_REGISTERS=1 keeps the register shape.
+void eval_shape(const saturn_plan* p, int* nn, int* gp) {
+  static const bool regs = [] {
+    const char* e = getenv("SATURN_EVAL_REGISTERS");
+    return e && e[0] == '1';
+  }();
+  *nn = p->NN;
+  *gp = p->GP;
+  if (!regs && p->NN >= 4 && sat::have_sorted_shape(0, std::max(4, p->GP)) &&
+      sat::eval_smem_bytes(p->pb, 0, std::max(4, p->GP)) <= 227 * 1024) {
+    *nn = 0;
+    *gp = std::max(4, p->GP);
+  }
+}
+
 bool host_only(saturn_plan* p) {
   if (p->device < 0) {
     fail(p, SATURN_ESTATE, "host-only handle (created with cuda_device = -1)");
@@ -414,7 +433,9 @@ saturn_status saturn_evaluate(saturn_plan* p, const uint8_t* d_cfg, const uint8_
   saturn_status s = use_decoder_kind(p, &kind);
   if (s != SATURN_OK) return s;
   DeviceGuard dg(p->device);
-  CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, kind, d_cfg, d_perm, n, d_makespan, p->sms,
+  int enn, egp;
+  eval_shape(p, &enn, &egp);
+  CU(p, sat::launch_evaluate(p->pb, enn, egp, kind, d_cfg, d_perm, n, d_makespan, p->sms,
                              static_cast<cudaStream_t>(stream)));
   p->stats.kernel_launches += 1;
   return SATURN_OK;
@@ -460,7 +481,9 @@ saturn_status saturn_evaluate_host(saturn_plan* p, const uint8_t* h_cfg, const u
     const int64_t m = std::min(chunk, n - off);
     CU(p, cudaMemcpyAsync(p->ws_cfg.p, h_cfg + off * p->T, m * p->T, cudaMemcpyHostToDevice, st));
     CU(p, cudaMemcpyAsync(p->ws_perm.p, h_perm + off * p->T, m * p->T, cudaMemcpyHostToDevice, st));
-    CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, kind, p->ws_cfg.p, p->ws_perm.p, m, p->ws_ms.p, p->sms, st));
+    int enn, egp;
+    eval_shape(p, &enn, &egp);
+    CU(p, sat::launch_evaluate(p->pb, enn, egp, kind, p->ws_cfg.p, p->ws_perm.p, m, p->ws_ms.p, p->sms, st));
     CU(p, cudaMemcpyAsync(h_makespan + off, p->ws_ms.p, m * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     p->stats.kernel_launches += 1;
     p->stats.h2d_bytes += 2 * m * p->T;
