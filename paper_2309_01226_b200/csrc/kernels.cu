@@ -17,7 +17,10 @@
 
 namespace sat {
 
-constexpr int EVAL_B = 128;  // threads of the evaluate kernel
+#ifndef SAT_EVAL_B
+#define SAT_EVAL_B 128
+#endif
+constexpr int EVAL_B = SAT_EVAL_B;  // threads of the evaluate kernel
 #ifndef SAT_EVAL_X
 #define SAT_EVAL_X 1          // genomes per thread in k_evaluate (register designs, T <= 32)
 #endif
