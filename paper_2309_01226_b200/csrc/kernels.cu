@@ -794,7 +794,12 @@ struct GaMinBlocks {
 // Child construction follows oracle/ga.py (GA v4): every Philox
 // word has a fixed position, so all lanes draw the same blocks at the same program points
 // and the operators run as uniform loops with predicated writes (no divergent refills).
-template <int NN, int GP, bool DECODE>
+// INIT: the generation-0 kernel (Philox genomes / seeds) is compiled separately from the
+// generation kernel, so each gets its own register allocation and code layout.
+#ifndef SAT_GA_INIT_KERNEL
+#define SAT_GA_INIT_KERNEL 1
+#endif
+template <int NN, int GP, bool DECODE, bool INIT = false>
 __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
          const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
@@ -859,7 +864,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     const int64_t slot = base + lane;
     const bool live = slot < gp.P;
     int msv = INT_MAX;
-    if (gp.gen == 0) {  // ---------------- initial population
+    if (SAT_GA_INIT_KERNEL ? INIT : gp.gen == 0) {  // ---------------- initial population
       if (live) {
         if (slot < n_seed) {
           load_row(ch.base, seeds + slot * GS, GS);
@@ -1123,9 +1128,15 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
   if (ga_split()) {
     {
       const size_t smem = ga_smem_bytes(pb, 1, 2, gp.GS);
-      const int g = grid_for(k_ga<1, 2, false>, GA_B, smem, sms, blocks);
-      k_ga<1, 2, false><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
-                                               cand, d_n_cand);
+      if (gp.gen == 0) {
+        const int g = grid_for(k_ga<1, 2, false, true>, GA_B, smem, sms, blocks);
+        k_ga<1, 2, false, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop,
+                                                       ms, cand, d_n_cand);
+      } else {
+        const int g = grid_for(k_ga<1, 2, false>, GA_B, smem, sms, blocks);
+        k_ga<1, 2, false><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
+                                                 cand, d_n_cand);
+      }
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
@@ -1145,9 +1156,15 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
   const size_t smem = ga_smem_bytes(pb, NN, GP, gp.GS);
 #define SAT_GA(a, b)                                                                                        \
   if (NN == a && GP == b) {                                                                                 \
-    const int g = grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks);                                      \
-    k_ga<a, b, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, \
-                                            ms, cand, d_n_cand);                                            \
+    if (gp.gen == 0) {                                                                                      \
+      const int g = grid_for(k_ga<a, b, true, true>, GA_B, smem, sms, blocks);                              \
+      k_ga<a, b, true, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms,       \
+                                                    rec_gen, pop, ms, cand, d_n_cand);                      \
+    } else {                                                                                                \
+      const int g = grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks);                                    \
+      k_ga<a, b, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen,    \
+                                              pop, ms, cand, d_n_cand);                                     \
+    }                                                                                                       \
     if (mid) cudaEventRecord(mid, st);                                                                      \
     return cudaGetLastError();                                                                              \
   }
@@ -1169,8 +1186,10 @@ int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t 
   }
   {
     const size_t smem = ga_smem_bytes(pb, NN, GP, GS);
-#define SAT_GAC(a, b) \
-    if (NN == a && GP == b) g2 = grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks);
+#define SAT_GAC(a, b)                                                                       \
+    if (NN == a && GP == b)                                                                   \
+      g2 = std::max(grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks),                      \
+                    grid_for(k_ga<a, b, true, true>, GA_B, smem, sms, blocks));
     SAT_SHAPES(SAT_GAC)
 #undef SAT_GAC
   }
