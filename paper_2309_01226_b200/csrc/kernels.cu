@@ -799,7 +799,12 @@ struct GaMinBlocks {
 #ifndef SAT_GA_INIT_KERNEL
 #define SAT_GA_INIT_KERNEL 1
 #endif
-template <int NN, int GP, bool DECODE, bool INIT = false>
+// LONGT (T > 32: the shared-memory LOX bit set, parent B from global memory) is a template
+// parameter too, so the short-genome kernel carries no long-genome code (and vice versa).
+#ifndef SAT_GA_LONGT_KERNEL
+#define SAT_GA_LONGT_KERNEL 1
+#endif
+template <int NN, int GP, bool DECODE, bool INIT = false, bool LONGT = false>
 __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
          const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
@@ -813,8 +818,11 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   uint8_t* s_child = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
+  // short: T <= 32 (compile-time when SAT_GA_LONGT_KERNEL; LONGT == (T > 32) at launch)
+  const bool short_t = SAT_GA_LONGT_KERNEL ? !LONGT : (T <= 32);
+  const int rows = (SAT_GA_B_GLOBAL && !short_t) ? 1 : 2;   // == ga_rows(T)
   uint8_t* s_B = s_child + GA_B * RS;   // (T <= 32 only)
-  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_child + ga_rows(T) * GA_B * RS);
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_child + rows * GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);   // [GA_B / 32][32]
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
@@ -902,7 +910,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       if (elite) load_row(ch.base, rec_gen + slot * GS, GS);
       if (child) {
         load_row(ch.base, prev_pop + (uint64_t)A * GS, GS);
-        if (ga_rows(T) == 2) load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
+        if (rows == 2) load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
       }
       const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
       const bool xo = child && (w1.x & 0xffffu) < px16;
@@ -913,7 +921,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         const uint32_t* ca = reinterpret_cast<const uint32_t*>(ch.base);
         uint32_t* cw = reinterpret_cast<uint32_t*>(ch.base);
         uint32_t bits = 0;
-        if (ga_rows(T) == 2) {
+        if (rows == 2) {
           const uint32_t* cb = reinterpret_cast<const uint32_t*>(gb.base);
           for (int t = 0; t < T; t += 4) {
             if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
@@ -941,7 +949,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         uint8_t* const pa = p0 + a;
         const uint32_t gap = b - a + 1;
         uint8_t* wp = (a == 0) ? p0 + gap : p0;
-        if (T <= 32) {
+        if (short_t) {
           uint32_t kept = 0;
           for (int q = 0; q < T; ++q) {
             const uint32_t bit = 1u << ch.q(q);
@@ -964,7 +972,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
             inA[min(x >> 5, nb - 1) * GA_B] |= 1u << (x & 31);
           }
           const uint32_t xm = xo ? 1u : 0u;
-          const uint8_t* Bq = (ga_rows(T) == 2) ? gb.base + Tp : prev_pop + (uint64_t)B * GS + Tp;
+          const uint8_t* Bq = (rows == 2) ? gb.base + Tp : prev_pop + (uint64_t)B * GS + Tp;
           for (int k = 0; k < T; ++k) {
             const int x = Bq[k];
             const uint32_t take = (~inA[min(x >> 5, nb - 1) * GA_B] >> (x & 31)) & xm;
@@ -1120,6 +1128,40 @@ static bool ga_split() {
   return v == 1;
 }
 
+// One GA launch of shape (A, B): the kernel variant is picked by generation 0 (INIT) and
+// by T > 32 (LONGT).
+template <int A, int B, bool DEC, bool I, bool L>
+static cudaError_t ga_go(const Problem& pb, const GaParams& gp, const uint8_t* seeds, int64_t n_seed,
+                         const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen,
+                         uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, size_t smem, int sms,
+                         int64_t blocks, cudaStream_t st) {
+  const int g = grid_for(k_ga<A, B, DEC, I, L>, GA_B, smem, sms, blocks);
+  k_ga<A, B, DEC, I, L><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
+                                                cand, d_n_cand);
+  return cudaGetLastError();
+}
+template <int A, int B, bool DEC>
+static cudaError_t ga_shape(const Problem& pb, const GaParams& gp, const uint8_t* seeds, int64_t n_seed,
+                            const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
+                            const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand,
+                            size_t smem, int sms, int64_t blocks, cudaStream_t st) {
+  const bool init = gp.gen == 0, longt = pb.T > 32;
+#define SAT_GO(I, L) \
+  ga_go<A, B, DEC, I, L>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, smem, sms, \
+                         blocks, st)
+  if (init) return longt ? SAT_GO(true, true) : SAT_GO(true, false);
+  return longt ? SAT_GO(false, true) : SAT_GO(false, false);
+#undef SAT_GO
+}
+// grid size the largest variant of a shape can take (candidate buffer sizing)
+template <int A, int B>
+static int ga_grid_max(size_t smem, int sms, int64_t blocks) {
+  return std::max(std::max(grid_for(k_ga<A, B, true, false, false>, GA_B, smem, sms, blocks),
+                           grid_for(k_ga<A, B, true, true, false>, GA_B, smem, sms, blocks)),
+                  std::max(grid_for(k_ga<A, B, true, false, true>, GA_B, smem, sms, blocks),
+                           grid_for(k_ga<A, B, true, true, true>, GA_B, smem, sms, blocks)));
+}
+
 static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
                              int64_t n_seed, const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
                              const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand,
@@ -1128,16 +1170,8 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
   if (ga_split()) {
     {
       const size_t smem = ga_smem_bytes(pb, 1, 2, gp.GS);
-      if (gp.gen == 0) {
-        const int g = grid_for(k_ga<1, 2, false, true>, GA_B, smem, sms, blocks);
-        k_ga<1, 2, false, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop,
-                                                       ms, cand, d_n_cand);
-      } else {
-        const int g = grid_for(k_ga<1, 2, false>, GA_B, smem, sms, blocks);
-        k_ga<1, 2, false><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
-                                                 cand, d_n_cand);
-      }
-      const cudaError_t e = cudaGetLastError();
+      const cudaError_t e = ga_shape<1, 2, false>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
+                                                  cand, d_n_cand, smem, sms, blocks, st);
       if (e != cudaSuccess) return e;
     }
     if (mid) cudaEventRecord(mid, st);
@@ -1156,17 +1190,10 @@ static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& 
   const size_t smem = ga_smem_bytes(pb, NN, GP, gp.GS);
 #define SAT_GA(a, b)                                                                                        \
   if (NN == a && GP == b) {                                                                                 \
-    if (gp.gen == 0) {                                                                                      \
-      const int g = grid_for(k_ga<a, b, true, true>, GA_B, smem, sms, blocks);                              \
-      k_ga<a, b, true, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms,       \
-                                                    rec_gen, pop, ms, cand, d_n_cand);                      \
-    } else {                                                                                                \
-      const int g = grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks);                                    \
-      k_ga<a, b, true><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen,    \
-                                              pop, ms, cand, d_n_cand);                                     \
-    }                                                                                                       \
+    const cudaError_t e = ga_shape<a, b, true>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen,   \
+                                               pop, ms, cand, d_n_cand, smem, sms, blocks, st);             \
     if (mid) cudaEventRecord(mid, st);                                                                      \
-    return cudaGetLastError();                                                                              \
+    return e;                                                                                               \
   }
   SAT_SHAPES(SAT_GA)
 #undef SAT_GA
@@ -1186,10 +1213,8 @@ int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t 
   }
   {
     const size_t smem = ga_smem_bytes(pb, NN, GP, GS);
-#define SAT_GAC(a, b)                                                                       \
-    if (NN == a && GP == b)                                                                   \
-      g2 = std::max(grid_for(k_ga<a, b, true>, GA_B, smem, sms, blocks),                      \
-                    grid_for(k_ga<a, b, true, true>, GA_B, smem, sms, blocks));
+#define SAT_GAC(a, b) \
+    if (NN == a && GP == b) g2 = ga_grid_max<a, b>(smem, sms, blocks);
     SAT_SHAPES(SAT_GAC)
 #undef SAT_GAC
   }
