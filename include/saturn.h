@@ -195,13 +195,14 @@ saturn_status saturn_set_enumeration_options(saturn_plan *p, uint32_t options);
 saturn_status saturn_enumerate_range(saturn_plan *p, uint64_t begin, uint64_t end, void *stream,
                                      saturn_result *out);
 
-/* Genetic search (rows a4-iii, a5, a6, a7): an initial
- * population, then max_generations generations of Philox tournament selection, uniform /
- * OX1 crossover and mutation, every child decoded on the device, the elites carried over.
- * With an attached communicator each GPU runs an island and every generations_per_epoch
- * generations the elites of all islands are all-gathered and every island continues from the
- * global best E.  Deterministic for fixed (params, world size).  flags = SATURN_INCUMBENT.
- * Synchronous.  EINVAL for bad params; ESTATE without a table. */
+/* Genetic search (rows a4-iii, a5, a6, a7, oracle/ga.py GA v4):
+ * an initial population, then max_generations generations of Philox tournament selection,
+ * uniform (configs) / LOX (priority permutation) crossover and mutation, every child decoded
+ * on the device, the elites carried over.  With an attached communicator or peer link each
+ * GPU runs an island and every generations_per_epoch generations the elites of all islands
+ * are exchanged and every island continues from the global best E.  Deterministic for fixed
+ * (params, world size).  flags = SATURN_INCUMBENT.  Synchronous.  EINVAL for bad params;
+ * ESTATE without a table. */
 saturn_status saturn_search(saturn_plan *p, const saturn_search_params *sp, void *stream, saturn_result *out);
 
 /* Several islands in one process (row e without NCCL): plans[0..k) -- handles with the same
