@@ -1,8 +1,10 @@
 """Mutation check for the oracle pins (run by hand: python tests/oracle_mutation_check.py).
 
-Each mutation plants one plausible mistake in oracle/saturn_oracle.c (a wrong GPU rule, a
-wrong tie-break, an off-by-one, a dropped max, a transposed radix) and confirms that the
-`-m "not gpu"` oracle pins in tests/test_oracle_pins.py fail.  The original source is
+Each mutation plants one plausible mistake in an oracle source (a wrong GPU rule, a wrong
+tie-break, an off-by-one, a dropped max, a transposed radix in oracle/saturn_oracle.c; a
+non-strict acceptance, a wrong tie-break or a dropped move family in oracle/local_search.py;
+Sattolo's shuffle, a skipped swap or a short config range in oracle/ga.py:initial_genome)
+and confirms that the `-m "not gpu"` pins of that source fail.  The original source is
 restored afterwards.  Result for this round is recorded in DESIGN.md ("Oracle pins").
 """
 import os
@@ -11,42 +13,60 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "oracle", "saturn_oracle.c")
 LIB = os.path.join(ROOT, "oracle", "liboracle.so")
+C_SRC = "oracle/saturn_oracle.c"
+LS_SRC = "oracle/local_search.py"
+GA_SRC = "oracle/ga.py"
+PINS = "tests/test_oracle_pins.py"
+SEARCH_PINS = "tests/test_oracle_search_pins.py"
 
 MUTATIONS = [
-    ("gpu rule smallest-free", "f > free_t[first[best_n] + pick]", "f < free_t[first[best_n] + pick]"),
-    ("node tie -> highest id", "start_n < best_s", "start_n <= best_s"),
-    ("free test strict", "f > s) continue", "f >= s) continue"),
-    ("k-th smallest off by one", "sorted_free[g - 1]", "sorted_free[g > 1 ? g - 2 : 0]"),
-    ("gpu tie -> higher id", "if (pick < 0 || f > free_t", "if (pick < 0 || f >= free_t"),
-    ("makespan = last end", "if (s + r > makespan) makespan = s + r;", "makespan = s + r;"),
-    ("radix reversed", "cfg[t] = (uint8_t)(r_cfg % (uint64_t)n_cfg[t]);",
+    (C_SRC, PINS, "gpu rule smallest-free", "f > free_t[first[best_n] + pick]", "f < free_t[first[best_n] + pick]"),
+    (C_SRC, PINS, "node tie -> highest id", "start_n < best_s", "start_n <= best_s"),
+    (C_SRC, PINS, "free test strict", "f > s) continue", "f >= s) continue"),
+    (C_SRC, PINS, "k-th smallest off by one", "sorted_free[g - 1]", "sorted_free[g > 1 ? g - 2 : 0]"),
+    (C_SRC, PINS, "gpu tie -> higher id", "if (pick < 0 || f > free_t", "if (pick < 0 || f >= free_t"),
+    (C_SRC, PINS, "makespan = last end", "if (s + r > makespan) makespan = s + r;", "makespan = s + r;"),
+    (C_SRC, PINS, "radix reversed", "cfg[t] = (uint8_t)(r_cfg % (uint64_t)n_cfg[t]);",
      "cfg[n_jobs-1-t] = (uint8_t)(r_cfg % (uint64_t)n_cfg[n_jobs-1-t]);"),
-    ("brute force keeps last tie", "if (best < 0 || ms < best)", "if (best < 0 || ms <= best)"),
+    (C_SRC, PINS, "brute force keeps last tie", "if (best < 0 || ms < best)", "if (best < 0 || ms <= best)"),
+    (LS_SRC, SEARCH_PINS, "local search accepts equal makespan", "if m[best] >= ms:", "if m[best] > ms:"),
+    (LS_SRC, SEARCH_PINS, "local search tie -> largest move", "np.lexsort((np.arange(len(m)), m))",
+     "np.lexsort((-np.arange(len(m)), m))"),
+    (LS_SRC, SEARCH_PINS, "config moves dropped", "    for t in range(T):\n        for v in range(int(c.S[t])):",
+     "    for t in range(0):\n        for v in range(int(c.S[t])):"),
+    (LS_SRC, SEARCH_PINS, "insertion target off by one", "j = jj if jj < i else jj + 1\n        p = list(perm)",
+     "j = jj + 1 if jj < i else jj\n        p = list(perm)"),
+    (GA_SRC, SEARCH_PINS, "Sattolo shuffle", "j = st.below(i + 1)", "j = st.below(i)"),
+    (GA_SRC, SEARCH_PINS, "last swap skipped", "for i in range(T - 1, 0, -1):", "for i in range(T - 1, 1, -1):"),
+    (GA_SRC, SEARCH_PINS, "config range short by one", "cfg = [st.below(int(S[t])) for t in range(T)]",
+     "cfg = [st.below(max(int(S[t]) - 1, 1)) for t in range(T)]"),
 ]
 
 
 def main():
-    backup = SRC + ".orig"
-    shutil.copy(SRC, backup)
     ok = True
-    try:
-        src = open(backup).read()
-        for name, old, new in MUTATIONS:
-            assert old in src, old
-            open(SRC, "w").write(src.replace(old, new, 1))
+    for src_rel, tests, name, old, new in MUTATIONS:
+        src = os.path.join(ROOT, src_rel)
+        backup = src + ".orig"
+        shutil.copy(src, backup)
+        try:
+            text = open(backup).read()
+            assert old in text, (src_rel, old)
+            open(src, "w").write(text.replace(old, new, 1))
             if os.path.exists(LIB):
                 os.remove(LIB)
-            r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "tests/test_oracle_pins.py"],
+            shutil.rmtree(os.path.join(ROOT, "oracle", "__pycache__"), ignore_errors=True)   # same-size edits
+            r = subprocess.run([sys.executable, "-B", "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", tests],
                                cwd=ROOT, capture_output=True, text=True)
             caught = r.returncode != 0
             ok &= caught
-            print(f"{'CAUGHT ' if caught else 'MISSED '} {name}: {r.stdout.strip().splitlines()[-1]}")
-    finally:
-        shutil.move(backup, SRC)
-        if os.path.exists(LIB):
-            os.remove(LIB)
+            print(f"{'CAUGHT ' if caught else 'MISSED '} {src_rel}: {name}: {r.stdout.strip().splitlines()[-1]}",
+                  flush=True)
+        finally:
+            shutil.move(backup, src)
+            if os.path.exists(LIB):
+                os.remove(LIB)
     sys.exit(0 if ok else 1)
 
 
