@@ -313,7 +313,8 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
     return fail(p, SATURN_EINVAL, "sum of per-job max runtimes %lld >= 2^26 s", (long long)sum_max);
   int stride = 0;  // max_t S_t plus one zero sentinel column (invalid genes decode to it)
   for (int t = 0; t < T; ++t) stride = std::max(stride, (int)gs[t].size() + 1);
-  const int raw = 4 * T * stride + T + T * stride;
+  const int NG = (int)p->gpu_n.size();
+  const int raw = 4 * T * stride + T + NG + T * stride;   // tab | S | GPU_n | upp
   const int bytes = (raw + 15) & ~15;
   if (bytes > 48 * 1024) return fail(p, SATURN_ELIMIT, "packed table %d B > 48 KB", bytes);
   std::unique_ptr<DeviceGuard> dg;
@@ -322,7 +323,9 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   std::vector<uint8_t> blob(bytes, 0);
   uint32_t* tab = reinterpret_cast<uint32_t*>(blob.data());
   uint8_t* Sb = blob.data() + 4 * T * stride;
-  uint8_t* upp = Sb + T;
+  uint8_t* Gb = Sb + T;     // GPU_n per node (decoders index it with a runtime node id)
+  uint8_t* upp = Gb + NG;
+  for (int n = 0; n < NG; ++n) Gb[n] = (uint8_t)p->gpu_n[n];
   p->S.assign(T, 0);
   p->cfg_g.assign(T * stride, 0);
   p->cfg_r.assign(T * stride, 0);
@@ -360,7 +363,7 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   p->Gmax = max_gpus;
   Problem pb{};
   pb.blob = p->blob.p;
-  pb.blob_bytes = std::min(bytes, (4 * T * stride + T + 15) & ~15);   // tab + S (staged by the decoders)
+  pb.blob_bytes = std::min(bytes, (4 * T * stride + T + NG + 15) & ~15);   // tab + S + GPU_n (staged by the decoders)
   pb.full_bytes = bytes;
   pb.T = T;
   pb.stride = stride;

@@ -23,8 +23,8 @@ constexpr uint32_t R_MASK = 0x00ffffffu; // config word = (g << 24) | R, R < 2^2
 // covers the table and S so one bulk copy stages what the decoders read into shared memory
 // (the UPP ids only matter to the trace decoder, which stages `full_bytes`).
 struct Problem {
-  const uint8_t* blob;     // device: tab[T*stride] u32, then S[T] u8, then upp[T*stride] u8, zero padded
-  int blob_bytes;          // staged prefix: tab + S, rounded up to 16 (all the decoders read)
+  const uint8_t* blob;     // device: tab[T*stride] u32, S[T] u8, GPU_n[N] u8, upp[T*stride] u8, zero padded
+  int blob_bytes;          // staged prefix: tab + S + GPU_n, rounded up to 16 (all the decoders read)
   int full_bytes;          // the whole blob incl. the UPP ids (the trace decoder only)
   int T;                   // jobs
   int stride;              // words per job row = max_t S_t
@@ -40,6 +40,9 @@ __device__ __forceinline__ const uint32_t* tab_of(const uint8_t* blob) {
 __device__ __forceinline__ const uint8_t* S_of(const uint8_t* blob, const Problem& pb) {
   return blob + 4 * pb.T * pb.stride;
 }
+// GPU_n of every node, right after S in the staged blob: indexing the kernel parameter
+// pb.gpu_n with a runtime node id would copy the whole Problem to local memory.
+__device__ __forceinline__ const uint8_t* G_of(const uint8_t* S, const Problem& pb) { return S + pb.T; }
 
 // ------------------------------------------------------------------ TMA bulk staging
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

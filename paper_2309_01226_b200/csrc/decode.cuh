@@ -168,20 +168,14 @@ template <int NN, int GP, int CHECK, bool TRACK_MS, class G>
 __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
                                                   int stride, const G& gen, int T, const Problem& pb,
                                                   uint32_t* mask, int mstride) {
-  int a[NN][GP];
-#pragma unroll
-  for (int n = 0; n < NN; ++n)
-#pragma unroll
-    for (int i = 0; i < GP; ++i) a[n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
-
   bool bad = false;
   int maxt = 0;
   uint32_t seen = 0u, minw = 0xffffffffu;
   if constexpr (CHECK == 2) {
     for (int w = 0; w < (T + 31) / 32; ++w) mask[w * mstride] = 0u;
   }
-  int ms = 0;
-  for (int p = 0; p < T; ++p) {
+  // config word (g << 24 | R) of the job at priority position p (+ the validity bookkeeping)
+  const auto fetch = [&](int p) -> uint32_t {
     int t = gen.perm(p);
     int c;
     if constexpr (CHECK != 0) {
@@ -202,6 +196,31 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
     }
     const uint32_t w = tab[t * stride + c];
     if constexpr (CHECK != 0) minw = min(minw, w);
+    return w;
+  };
+  // Position 0 in closed form: every GPU is free at 0, so the first job starts at 0 on the
+  // lowest node with >= g GPUs and (latest-free-first = all equal, lower ids first ... in the
+  // multiset view: the g top slots of that node's GPU_n free ones) ends at R.
+  int a[NN][GP];
+  int ms;
+  {
+    const uint32_t w = fetch(0);
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    int bn = NN;
+#pragma unroll
+    for (int n = NN - 1; n >= 0; --n) bn = (n < pb.N && g <= pb.gpu_n[n]) ? n : bn;
+#pragma unroll
+    for (int n = 0; n < NN; ++n) {
+      const int gn = n < pb.N ? pb.gpu_n[n] : 0;
+#pragma unroll
+      for (int i = 0; i < GP; ++i) a[n][i] = (i < gn) ? ((n == bn && i >= gn - g) ? R : 0) : INF;
+    }
+    ms = R;
+  }
+  // Positions 1 .. T-2: the full update.
+  for (int p = 1; p < T - 1; ++p) {
+    const uint32_t w = fetch(p);
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
     int v;
@@ -209,52 +228,45 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
       v = place_sorted<GP>(a[0], g, R);
     } else {
       // start of every node: its g-th smallest free time (+inf if it has fewer GPUs)
-      int best = SAT_FMA_MUX ? mux_fma<GP>(a[0], g - 1) : mux<GP>(a[0], g - 1);
+      int best = mux<GP>(a[0], g - 1);
       int bn = 0;
 #pragma unroll
       for (int n = 1; n < NN; ++n) {
-        const int st = SAT_FMA_MUX ? mux_fma<GP>(a[n], g - 1) : mux<GP>(a[n], g - 1);
+        const int st = mux<GP>(a[n], g - 1);
         const bool lt = st < best;   // strict: ties keep the lowest node id
         best = lt ? st : best;
         bn = lt ? n : bn;
       }
       int x[GP];
-      if constexpr (SAT_FMA_MULTI) {
-        int on[NN];
 #pragma unroll
-        for (int n = 0; n < NN; ++n) on[n] = (bn == n) ? 1 : 0;
+      for (int i = 0; i < GP; ++i) {
+        int y = a[0][i];
 #pragma unroll
-        for (int i = 0; i < GP; ++i) {
-          int y = a[0][i];
-#pragma unroll
-          for (int n = 1; n < NN; ++n) y = sel_fma(on[n], y, a[n][i]);
-          x[i] = y;
-        }
-        v = place_sorted<GP>(x, g, R);
-#pragma unroll
-        for (int n = 0; n < NN; ++n)
-#pragma unroll
-          for (int i = 0; i < GP; ++i) a[n][i] = sel_fma(on[n], a[n][i], x[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < GP; ++i) {
-          int y = a[0][i];
-#pragma unroll
-          for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
-          x[i] = y;
-        }
-        v = place_sorted<GP>(x, g, R);
-#pragma unroll
-        for (int n = 0; n < NN; ++n)
-#pragma unroll
-          for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
+        for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
+        x[i] = y;
       }
+      v = place_sorted<GP>(x, g, R);
+#pragma unroll
+      for (int n = 0; n < NN; ++n)
+#pragma unroll
+        for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
     }
     if constexpr (TRACK_MS) ms = max(ms, v);
   }
   if constexpr (!TRACK_MS) {
+    ms = 0;
 #pragma unroll
     for (int n = 0; n < NN; ++n) ms = max(ms, a[n][GP - 1]);
+  }
+  // Position T-1: only its end matters (no later job reads the state): earliest start + R.
+  if (T > 1) {
+    const uint32_t w = fetch(T - 1);
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    int best = mux<GP>(a[0], g - 1);
+#pragma unroll
+    for (int n = 1; n < NN; ++n) best = min(best, mux<GP>(a[n], g - 1));
+    ms = max(ms, best + R);
   }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;
   if constexpr (CHECK != 0) {
@@ -269,7 +281,7 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
 // if nd[t] == 0xFF.  Always validity-checked: a node gene naming a missing node or one with
 // fewer than g GPUs makes the genome invalid (-1), like a bad cfg / perm.
 template <int NN, int GP>
-__device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ tab, int stride,
+__device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ tab, const uint8_t* G, int stride,
                                                    const uint8_t* cfg, const uint8_t* perm, const uint8_t* nd,
                                                    int T, const Problem& pb, uint32_t* mask, int mstride) {
   int a[NN][GP];
@@ -306,7 +318,7 @@ __device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ 
       best = lt ? st : best;
       bn = lt ? n : bn;
     }
-    bad |= (want != 0xFF) && (want >= pb.N || g > pb.gpu_n[min(want, MAX_NODES - 1)]);
+    bad |= (want != 0xFF) && (want >= pb.N || g > G[min(want, pb.N - 1)]);
     bad |= best == INF;
     int x[GP];
 #pragma unroll
@@ -420,23 +432,13 @@ __device__ __forceinline__ int decode_smem(const uint32_t* __restrict__ tab, con
                                            uint32_t* mask = nullptr, int mstride = 0) {
   static_assert(GP % 4 == 0, "vector node rows");
   const int N = pb.N;
-  for (int n = 0; n < N; ++n) {
-    int4* row = reinterpret_cast<int4*>(ns + n * GP);
-#pragma unroll
-    for (int j = 0; j < GP / 4; ++j) {
-      const int i = 4 * j;
-      const int gn = pb.gpu_n[n];
-      row[j] = make_int4(i < gn ? 0 : INF, i + 1 < gn ? 0 : INF, i + 2 < gn ? 0 : INF, i + 3 < gn ? 0 : INF);
-    }
-  }
   bool bad = false;
   int maxt = 0;
   uint32_t seen = 0u, minw = 0xffffffffu;
   if constexpr (CHECK == 2) {
     for (int w = 0; w < (T + 31) / 32; ++w) mask[w * mstride] = 0u;
   }
-  int ms = 0;
-  for (int p = 0; p < T; ++p) {
+  const auto fetch = [&](int p) -> uint32_t {
     int t = gen.perm(p);
     int c;
     if constexpr (CHECK != 0) {
@@ -457,6 +459,34 @@ __device__ __forceinline__ int decode_smem(const uint32_t* __restrict__ tab, con
     }
     const uint32_t w = tab[t * stride + c];
     if constexpr (CHECK != 0) minw = min(minw, w);
+    return w;
+  };
+  // Position 0 in closed form (every GPU free at 0): the lowest node with >= g GPUs gets
+  // R in its top g free slots.
+  int ms;
+  {
+    const uint32_t w = fetch(0);
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    const uint8_t* G = G_of(S, pb);
+    int bn = N;
+    for (int n = N - 1; n >= 0; --n) bn = (g <= G[n]) ? n : bn;
+    for (int n = 0; n < N; ++n) {
+      int4* row = reinterpret_cast<int4*>(ns + n * GP);
+      const int gn = G[n];
+      const int lo = (n == bn) ? gn - g : gn;
+#pragma unroll
+      for (int j = 0; j < GP / 4; ++j) {
+        int q[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) q[e] = (4 * j + e < gn) ? ((4 * j + e >= lo) ? R : 0) : INF;
+        row[j] = make_int4(q[0], q[1], q[2], q[3]);
+      }
+    }
+    ms = R;
+  }
+  for (int p = 1; p < T - 1; ++p) {
+    const uint32_t w = fetch(p);
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
     // start of every node (its g-th smallest free time; +inf padding if it has fewer GPUs)
@@ -480,6 +510,15 @@ __device__ __forceinline__ int decode_smem(const uint32_t* __restrict__ tab, con
     for (int j = 0; j < GP / 4; ++j) row[j] = make_int4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
     ms = max(ms, v);
   }
+  // Position T-1: earliest start + R, no state update.
+  if (T > 1) {
+    const uint32_t w = fetch(T - 1);
+    const int g = (int)(w >> 24);
+    const int R = (int)(w & R_MASK);
+    int best = ns[g - 1];
+    for (int n = 1; n < N; ++n) best = min(best, ns[n * GP + g - 1]);
+    ms = max(ms, best + R);
+  }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;
   if constexpr (CHECK != 0) {
     bad |= maxt >= T || minw == 0u;
@@ -502,7 +541,7 @@ struct WarpLane {
   int maxg;       // max_n GPU_n
 };
 
-__device__ __forceinline__ WarpLane warp_lane(const Problem& pb) {
+__device__ __forceinline__ WarpLane warp_lane(const Problem& pb, const uint8_t* G) {
   WarpLane L;
   int seg = 1;
   while (seg < pb.sumG) seg <<= 1;
@@ -517,7 +556,7 @@ __device__ __forceinline__ WarpLane warp_lane(const Problem& pb) {
   L.maxg = 0;
   int acc = 0;
   for (int n = 0; n < pb.N; ++n) {
-    const int gn = pb.gpu_n[n];
+    const int gn = G[n];
     if (L.q >= acc && L.q < acc + gn) { L.node = n; L.first = acc; L.local = L.q - acc; L.size = gn; }
     acc += gn;
     L.maxg = max(L.maxg, (int)gn);

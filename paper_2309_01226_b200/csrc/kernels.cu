@@ -222,16 +222,18 @@ __global__ void __launch_bounds__(WARP_B) k_eval_warp(Problem pb, const uint8_t*
   int* s_first = reinterpret_cast<int*>(sm + pb.blob_bytes);
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_first + MAX_NODES);
   uint64_t* bar = reinterpret_cast<uint64_t*>(s_bits + (WARP_B / 32) * 32 * 8);
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k < pb.N; ++k) { s_first[k] = acc; acc += pb.gpu_n[k]; }
-  }
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
   const uint8_t* S = S_of(s_blob, pb);
-  const uint8_t* upp = S + pb.T;
+  const uint8_t* G = G_of(S, pb);
+  const uint8_t* upp = G + pb.N;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < pb.N; ++k) { s_first[k] = acc; acc += G[k]; }
+  }
+  __syncthreads();
   const int T = pb.T;
-  const WarpLane L = warp_lane(pb);
+  const WarpLane L = warp_lane(pb, G);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gpw = 32 / L.seg;
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(EVN_B) k_evaluate_nodes(Problem pb, const uint
   const uint32_t* tab = tab_of(s_blob);
   const int T = pb.T;
   for (int64_t i = (int64_t)blockIdx.x * EVN_B + threadIdx.x; i < n; i += (int64_t)gridDim.x * EVN_B)
-    out[i] = decode_sorted_nodes<NN, GP>(tab, pb.stride, gcfg + i * T, gperm + i * T, gnode + i * T, T, pb,
+    out[i] = decode_sorted_nodes<NN, GP>(tab, G_of(S_of(s_blob, pb), pb), pb.stride, gcfg + i * T, gperm + i * T, gnode + i * T, T, pb,
                                          s_mask + threadIdx.x, EVN_B);
 }
 
