@@ -306,8 +306,8 @@ saturn_status saturn_probe_int_peak(saturn_plan *p, double *int_ops_per_s);
 
 /* Counters since the last reset (measurement support, row d): kernel launches issued by
  * the library, host<->device bytes it copied, and -- when profiling is on -- the summed
- * device time of the GA generations (the fused GA kernel, or breed + decode kernels when
- * SATURN_GA_SPLIT=1), measured with CUDA events on the launching stream. */
+ * device time of the GA generation kernels, measured with CUDA events on the launching
+ * stream. */
 typedef struct {
   int64_t kernel_launches;
   int64_t h2d_bytes;
@@ -315,8 +315,6 @@ typedef struct {
   int64_t ga_launches;      /* GA generation kernels timed (profiling on)            */
   double ga_kernel_ms;      /* their summed device time                             */
   int64_t ga_decodes;       /* children decoded by those launches                   */
-  double breed_kernel_ms;   /* of which the GA-operator (breed) kernel, split mode   */
-  double decode_kernel_ms;  /* and the population decode kernel (fused: everything) */
 } saturn_stats;
 /* on = 0: off; on = n >= 1: time every n-th GA generation kernel of saturn_search with CUDA
  * events on the launching stream (1 = all; an event record between two kernels costs a few

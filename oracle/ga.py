@@ -17,30 +17,37 @@ Initial genome of slot k (>= number of seed genomes), stream (k, 0, rank << 16 |
 consumed in order: cfg[t] = U(S_t) for t = 0..T-1, then a Fisher-Yates shuffle of the
 identity: for i = T-1 down to 1, j = U(i+1), swap perm[i], perm[j].
 
-Child of slot k >= E in generation g (GA v3: every word has a FIXED position, so the
-draws never depend on earlier outcomes; 16-bit fields are lo = w & 0xFFFF, hi = w >> 16,
-V(n, h) = (h * n) >> 16 and a 16-bit gate with q32 threshold p fires iff h < p >> 16),
-stream (k, g, rank << 16 | 0):
+Children of generation g come in PAIRS (GA v5): slots 2q and 2q+1 are the two children of
+pair q, made from one pair of parents by complementary crossover (the classic two-offspring
+crossover); slots < E hold the elites instead.  Every word has a FIXED position in the
+pair's stream (q, g, rank << 16 | 0), so the draws never depend on earlier outcomes.
+16-bit fields are lo = w & 0xFFFF, hi = w >> 16, V(n, h) = (h * n) >> 16, and a 16-bit gate
+with q32 threshold p fires iff h < p >> 16.
    w0, w1   tournament for parent A: i = U(P, w0), j = U(P, w1); A = smaller (ms, slot)
    w2, w3   tournament for parent B, same rule
    w4       lo: crossover gate (p_x)          hi: LOX cut a = V(T, hi)
-   w5       lo: LOX cut b = V(T, lo)          hi: permutation-mutation gate (p_m)
-   w6       lo: mutation kind = lo & 1        hi: mutation position i = V(T, hi)
-   w7       lo: mutation position j = V(T, lo) hi: config-mutation gate (p_c)
-   w8       lo: mutated job t* = V(T, lo)     hi: its new gene V(S_t*, hi)
-   w9 .. w9+nb-1   crossover bits, nb = ceil(T/32): bit t of word t // 32, 1 -> A's cfg gene
- Steps, in order:
-   1. tournaments;  2. child = copy of A;
-   3. if crossover: cfg[t] = B.cfg[t] where bit t is 0;
-   4. if crossover: LOX (linear order crossover, Falkenauer & Bouffouix 1991) -- a, b
-      swapped so a <= b; keep A.perm[a..b] in place; fill positions 0..a-1, then b+1..T-1,
-      with B's genes in B's order from position 0, skipping genes in A's slice.  (GA v4:
-      v3 used OX1, which treats the permutation as a cyclic tour; a priority list is
-      linear, and LOX keeps both the slice's positions and B's relative order without the
-      wrap-around.)
+   w5       lo: LOX cut b = V(T, lo)          hi: unused
+   crossover bits: word k (k = 0 .. ceil(T/32)-1) at w6, w7, w16, w17, ... (w6 + k for
+            k < 2, w16 + k - 2 after); bit t of word t // 32
+   child r (r = 0, 1) fields: block 2 + r, i.e. words c = 8 + 4r .. 11 + 4r:
+     w[c]     lo: permutation-mutation gate (p_m)   hi: mutation position i = V(T, hi)
+     w[c+1]   lo: mutation position j = V(T, lo)    hi: mutation kind = hi & 1
+     w[c+2]   lo: config-mutation gate (p_c)        hi: mutated job t* = V(T, hi)
+     w[c+3]   lo: its new gene V(S_t*, lo)          hi: unused
+ Child r of the pair, with (X, Y) = (A, B) for r = 0 and (B, A) for r = 1, in order:
+   1. tournaments;  2. child = copy of X;
+   3. if crossover: cfg[t] = Y.cfg[t] where crossover bit t is 0 (so the two children
+      split every gene between the parents: complementary uniform crossover);
+   4. if crossover: LOX (linear order crossover, Falkenauer & Bouffouix 1991) of X with Y,
+      same cuts for both children -- a, b swapped so a <= b; keep X.perm[a..b] in place;
+      fill positions 0..a-1, then b+1..T-1, with Y's genes in Y's order from position 0,
+      skipping genes in X's slice;
    5. if config mutation: cfg[t*] = new gene;
    6. if permutation mutation: kind 0 swaps positions i and j; kind 1 removes the gene at i
       and reinserts it at position j.
+ History: v1-v4 made one child per tournament pair (v3 OX1, v4 LOX; 3 Philox blocks and
+ 2 parent reads per child); v5 shares the tournaments, the parents, the cuts and the
+ crossover bits between two children (per child: 2 Philox blocks, 1 parent read).
 """
 from __future__ import annotations
 
@@ -91,12 +98,24 @@ def lox(A_perm, B_perm, a: int, b: int):
     return list(fill[:a]) + list(A_perm[a:b + 1]) + list(fill[a:])
 
 
+def xbit_word(k: int) -> int:
+    """Position of crossover-bit word k in the pair's stream."""
+    return 6 + k if k < 2 else 16 + (k - 2)
+
+
+def pair_words(seed: int, rank: int, gen: int, q: int, T: int):
+    nb = (T + 31) // 32
+    n = max(16, xbit_word(nb - 1) + 1)
+    st = Stream(_key(seed), q, gen, (rank << 16) | 0)
+    return [st.u32() for _ in range(n)]
+
+
 def make_child(S, cfg, perm, ms, slot: int, gen: int, seed: int, rank: int,
                p_x: int, p_c: int, p_m: int):
     P, T = cfg.shape
     nb = (T + 31) // 32
-    st = Stream(_key(seed), slot, gen, (rank << 16) | 0)
-    w = [st.u32() for _ in range(9 + nb)]                # every word has a fixed position
+    q, r = slot >> 1, slot & 1
+    w = pair_words(seed, rank, gen, q, T)
     lo = [x & 0xFFFF for x in w]
     hi = [x >> 16 for x in w]
 
@@ -112,22 +131,24 @@ def make_child(S, cfg, perm, ms, slot: int, gen: int, seed: int, rank: int,
 
     a_idx = tournament(w[0], w[1])
     b_idx = tournament(w[2], w[3])
-    child_cfg, child_perm = list(cfg[a_idx]), list(perm[a_idx])
-    B_cfg, B_perm = list(cfg[b_idx]), list(perm[b_idx])
+    x_idx, y_idx = (a_idx, b_idx) if r == 0 else (b_idx, a_idx)
+    child_cfg, child_perm = list(cfg[x_idx]), list(perm[x_idx])
+    Y_cfg, Y_perm = list(cfg[y_idx]), list(perm[y_idx])
     if lo[4] < (p_x >> 16):
         for t in range(T):
-            if not (w[9 + t // 32] >> (t % 32)) & 1:
-                child_cfg[t] = B_cfg[t]
+            if not (w[xbit_word(t // 32)] >> (t % 32)) & 1:
+                child_cfg[t] = Y_cfg[t]
         a, b = V(T, hi[4]), V(T, lo[5])
         if a > b:
             a, b = b, a
-        child_perm = lox(child_perm, B_perm, a, b)
-    if hi[7] < (p_c >> 16):
-        t = V(T, lo[8])
-        child_cfg[t] = V(int(S[t]), hi[8])
-    if hi[5] < (p_m >> 16):
-        kind = lo[6] & 1
-        i, j = V(T, hi[6]), V(T, lo[7])
+        child_perm = lox(child_perm, Y_perm, a, b)
+    c = 8 + 4 * r
+    if lo[c + 2] < (p_c >> 16):
+        t = V(T, hi[c + 2])
+        child_cfg[t] = V(int(S[t]), lo[c + 3])
+    if lo[c] < (p_m >> 16):
+        kind = hi[c + 1] & 1
+        i, j = V(T, hi[c]), V(T, lo[c + 1])
         if kind == 0:
             child_perm[i], child_perm[j] = child_perm[j], child_perm[i]
         else:

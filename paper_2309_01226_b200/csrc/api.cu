@@ -924,7 +924,7 @@ struct Island {
     CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p,
                               p->pms[0].p, p->cand.p, p->n_cand.p, p->sms, st));
     CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
-    p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
+    p->stats.kernel_launches += 2;
     // profiling: event triples around every `profiling`-th GA generation kernel (at most 512
     // per search).  An event record between kernels costs a few microseconds of drain, so
     // sampling keeps the instrumented step within ~1 % of the uninstrumented one.
@@ -949,15 +949,14 @@ struct Island {
     const int64_t ti = n_timed;
     if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * ti], st));
     CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
-                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st,
-                                    timed ? p->ev_pool[3 * ti + 1] : nullptr));
+                                    p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st));
     if (timed) {
-      CU(p, cudaEventRecord(p->ev_pool[3 * ti + 2], st));
+      CU(p, cudaEventRecord(p->ev_pool[3 * ti + 1], st));
       ++n_timed;
     }
     CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[nxt].p, p->rec_ms.p, p->rec_gen.p, st,
                              /*few=*/true));   // generations >= 1 append only keys beating the E-th elite
-    p->stats.kernel_launches += sat::ga_is_split() ? 3 : 2;
+    p->stats.kernel_launches += 2;
     evaluated += (uint64_t)(P - E);
     cur = nxt;
     return SATURN_OK;
@@ -1025,18 +1024,11 @@ struct Island {
     if (hs != SATURN_OK) return hs;
     p->stats.d2h_bytes += GS + sizeof best;
     for (int64_t g = 1; g <= n_timed; ++g) {
-      float ms = 0.f, m1 = 0.f;
-      CU(p, cudaEventElapsedTime(&ms, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 2]));
-      CU(p, cudaEventElapsedTime(&m1, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 1]));
+      float ms = 0.f;
+      CU(p, cudaEventElapsedTime(&ms, p->ev_pool[3 * (g - 1)], p->ev_pool[3 * (g - 1) + 1]));
       p->stats.ga_kernel_ms += ms;
       p->stats.ga_launches += 1;
       p->stats.ga_decodes += P - E;
-      if (sat::ga_is_split()) {
-        p->stats.breed_kernel_ms += m1;
-        p->stats.decode_kernel_ms += ms - m1;
-      } else {
-        p->stats.decode_kernel_ms += ms;
-      }
     }
     p->best_cfg.assign(g0.begin(), g0.begin() + T);
     p->best_perm.assign(g0.begin() + sat::perm_offset(T), g0.begin() + sat::perm_offset(T) + T);

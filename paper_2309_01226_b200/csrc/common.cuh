@@ -109,6 +109,14 @@ __device__ __forceinline__ uint4 philox_block(uint32_t k0, uint32_t k1, uint32_t
   return make_uint4(x0, x1, x2, x3);
 }
 
+// Word k of the stream (c0, c1, c2): word k % 4 of block k / 4.
+__device__ __forceinline__ uint32_t philox_word(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                                uint32_t k) {
+  const uint4 v = philox_block(k0, k1, c0, c1, c2, k >> 2);
+  const uint32_t j = k & 3u;
+  return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
+}
+
 // U(n) = (u32 * n) >> 32, an integer in [0, n)
 __device__ __forceinline__ uint32_t ubelow(uint32_t u, uint32_t n) { return (uint32_t)(((uint64_t)u * n) >> 32); }
 // V(n) on a 16-bit field h: (h * n) >> 16, an integer in [0, n) for n <= 65536

@@ -739,16 +739,17 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
 }
 
 // ------------------------------------------------------------------ K3 (+K1): GA
-// Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): the child,
-// then parent B, then the LOX slice bit set for T > 32 (ceil(T/32) words, interleaved per thread).
-// Long genomes (T > 32) read parent B straight from the population in global memory (L1)
-// instead of staging it: one row per thread instead of two lets more CTAs fit per SM.
-#ifndef SAT_GA_B_GLOBAL
-#define SAT_GA_B_GLOBAL 1
-#endif
-__host__ __device__ __forceinline__ int ga_rows(int T) { return (SAT_GA_B_GLOBAL && T > 32) ? 1 : 2; }
-static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)ga_rows(pb.T) * GA_B * odd_row_stride(GS) +
+// GA v5 (oracle/ga.py is the normative text): the generation kernel makes the two children
+// of a PAIR of parents per thread iteration (complementary uniform crossover of the configs,
+// LOX of the permutations with shared cuts, per-child mutations), so the tournaments, the
+// parent reads, the cuts and the crossover bits are shared by two children.
+// Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): for short
+// genomes (T <= 32) the child C, parent A and parent B; long genomes keep only C and read
+// the parents from the population in global memory (L1), plus the LOX slice bit set
+// (ceil(T/32) words per thread, interleaved).  The init kernel keeps one row.
+__host__ __device__ __forceinline__ int ga_rows(int T, bool init) { return (init || T > 32) ? 1 : 3; }
+static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS, bool init) {
+  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)ga_rows(pb.T, init) * GA_B * odd_row_stride(GS) +
          (size_t)4 * ((pb.T + 31) / 32) * GA_B + 8 * GA_B + 8;
 }
 
@@ -773,210 +774,243 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
 template <int NN, int GP>
 struct GaMinBlocks {
   static constexpr int STATE = (NN == 0 ? 1 : NN) * GP;
-#ifndef SAT_GA_MINB_SMALL
-#define SAT_GA_MINB_SMALL 7   // with dynamic chunks (SAT_GA_DYNAMIC_ONE); 8 without
-#endif
-#ifndef SAT_GA_MINB_16
-#define SAT_GA_MINB_16 7   // measured r1 with dynamic chunks: MIX k_ga 0.690 (6) -> 0.680 ms (7); 5: 0.702
-#endif
-#ifndef SAT_GA_MINB_32
-#define SAT_GA_MINB_32 4   // measured r1: 5 and 6 lose on SWEEP (its shared memory caps it at 3 CTAs anyway)
-#endif
+  // measured r1 (dynamic chunks): 7 CTAs/SM for one 8-GPU node and for 16-slot states,
+  // 4 for 32-slot states (SWEEP's shared memory caps it at 3-5 anyway), 8 for small states
   static constexpr int value = NN == 0 ? (GP <= 8 ? 6 : (GP <= 16 ? 4 : 2))
-                                       : (STATE < 8 ? 8 : STATE == 8 ? SAT_GA_MINB_SMALL
-                                                     : (STATE <= 16 ? SAT_GA_MINB_16 : (STATE <= 32 ? SAT_GA_MINB_32 : 2)));
+                                       : (STATE < 8 ? 8 : STATE <= 16 ? 7 : (STATE <= 32 ? 4 : 2));
 };
 
-#ifndef SAT_GA_DYNAMIC
-#define SAT_GA_DYNAMIC 1
-#endif
-#ifndef SAT_GA_DYNAMIC_ONE
-#define SAT_GA_DYNAMIC_ONE 1   // one-node shapes too: with 7 CTAs/SM (72 registers) TXT k_ga
-#endif                         // 0.3374 -> 0.3286 ms; at 8 CTAs (64 registers) it lost 4 %
-// Child construction follows oracle/ga.py (GA v4): every Philox
-// word has a fixed position, so all lanes draw the same blocks at the same program points
-// and the operators run as uniform loops with predicated writes (no divergent refills).
-// INIT: the generation-0 kernel (Philox genomes / seeds) is compiled separately from the
-// generation kernel, so each gets its own register allocation and code layout.
-#ifndef SAT_GA_INIT_KERNEL
-#define SAT_GA_INIT_KERNEL 1
-#endif
-// LONGT (T > 32: the shared-memory LOX bit set, parent B from global memory) is a template
-// parameter too, so the short-genome kernel carries no long-genome code (and vice versa).
-#ifndef SAT_GA_LONGT_KERNEL
-#define SAT_GA_LONGT_KERNEL 1
-#endif
-template <int NN, int GP, bool DECODE, bool INIT = false, bool LONGT = false>
+// Dynamic work distribution: a warp's first chunk of 32 units comes from the static grid
+// stride, later ones are claimed from a counter (n_cand[1], zeroed by the previous elite
+// selection) one iteration before they are needed, so warps that finish early take more
+// (the static stride left SMs idle in the tail -- measured r1: MIX k_ga -11 %, SWEEP -10 %).
+struct WarpChunks {
+  unsigned int* work;
+  int64_t nthr, next;
+  unsigned int pending;
+  int lane;
+  __device__ __forceinline__ unsigned int claim() const { return lane == 0 ? atomicAdd(work, 32u) : 0u; }
+  __device__ __forceinline__ WarpChunks(int* n_cand, int64_t nthr_, int lane_)
+      : work(reinterpret_cast<unsigned int*>(n_cand + 1)), nthr(nthr_), lane(lane_) {
+    next = nthr + (int64_t)__shfl_sync(0xffffffffu, claim(), 0);
+    pending = claim();
+  }
+  // the next chunk's base; the one after it is claimed now
+  __device__ __forceinline__ int64_t advance() {
+    const int64_t b = next;
+    next = nthr + (int64_t)__shfl_sync(0xffffffffu, pending, 0);
+    pending = claim();
+    return b;
+  }
+};
+
+// Block-level merge of the warps' top-E lists -> this block's real keys appended to cand[].
+__device__ __forceinline__ void emit_topE(uint64_t lst, uint64_t* s_lists, int E, unsigned long long* cand,
+                                          int* n_cand) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  s_lists[tid] = lst;
+  __syncthreads();
+  if (tid < 32) {
+    uint64_t m = ~0ull;
+    for (int w = 0; w < GA_B / 32; ++w) topE_insert(m, s_lists[w * 32 + lane], E);
+    // append only the real keys (after the first generation most blocks have none)
+    const bool real = lane < E && m != ~0ull;
+    const uint32_t mask = __ballot_sync(0xffffffffu, real);
+    int off = 0;
+    if (lane == 0 && mask) off = atomicAdd(n_cand, __popc(mask));
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (real) cand[off + __popc(mask & ((1u << lane) - 1u))] = m;
+  }
+}
+
+// Generation 0: seed genomes, then cfg[t] = U(S_t) and a Fisher-Yates shuffle from the
+// slot's own Philox stream; every genome decoded.
+template <int NN, int GP>
 __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
-    k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed,
-         const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
-         const int32_t* __restrict__ rec_ms, const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
-         int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand, int* __restrict__ n_cand) {
+    k_ga_init(Problem pb, GaParams gp, const uint8_t* __restrict__ seeds, int64_t n_seed, uint8_t* __restrict__ pop,
+              int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand, int* __restrict__ n_cand) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int T = pb.T;
-  const int GS = gp.GS;
-  const int RS = odd_row_stride(GS);
-  const int Tp = perm_offset(T);
+  const int T = pb.T, GS = gp.GS, RS = odd_row_stride(GS), Tp = perm_offset(T);
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_child = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
-  // short: T <= 32 (compile-time when SAT_GA_LONGT_KERNEL; LONGT == (T > 32) at launch)
-  const bool short_t = SAT_GA_LONGT_KERNEL ? !LONGT : (T <= 32);
-  const int rows = (SAT_GA_B_GLOBAL && !short_t) ? 1 : 2;   // == ga_rows(T)
-  uint8_t* s_B = s_child + GA_B * RS;   // (T <= 32 only)
-  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_child + rows * GA_B * RS);
-  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);   // [GA_B / 32][32]
+  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + GA_B * RS);
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
   const uint8_t* S = S_of(s_blob, pb);
   const int tid = threadIdx.x, lane = tid & 31;
-  const RowG ch{s_child + RS * tid, Tp};
-  const RowG gb{s_B + RS * tid, Tp};
-  uint32_t* inA = s_bits + tid;  // LOX slice set for T > 32: word w at inA[w * GA_B]
-  const uint32_t P = (uint32_t)gp.P;
-  const int nb = (T + 31) / 32;
+  const RowG ch{s_rows + RS * tid, Tp};
   int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  uint64_t lst = ~0ull;
+  WarpChunks wc(n_cand, (int64_t)gridDim.x * GA_B, lane);
+  for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P; base = wc.advance()) {
+    const int64_t slot = base + lane;
+    const bool live = slot < gp.P;
+    int msv = INT_MAX;
+    if (live) {
+      if (slot < n_seed) {
+        load_row(ch.base, seeds + slot * GS, GS);
+      } else {
+        Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
+        for (int t = 0; t < GS; ++t) ch.base[t] = 0;
+        for (int t = 0; t < T; ++t) ch.c(t) = (uint8_t)rng.below(S[t]);
+        for (int t = 0; t < T; ++t) ch.q(t) = (uint8_t)t;
+        for (int i = T - 1; i > 0; --i) {
+          const int j = (int)rng.below(i + 1);
+          const uint8_t a = ch.q(i);
+          ch.q(i) = ch.q(j);
+          ch.q(j) = a;
+        }
+      }
+      msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      store_row(pop + slot * GS, ch.base, GS);
+      ms_out[slot] = msv;
+    }
+    topE_insert(lst, live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull, gp.E);
+  }
+  emit_topE(lst, s_lists, gp.E, cand, n_cand);
+}
+
+// Generation gen >= 1 (pairs).  LONGT: T > 32 (parents from global memory, the LOX slice
+// as a shared-memory bit set); otherwise parents staged in rows and the slice in a register.
+template <int NN, int GP, bool LONGT>
+__global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
+    k_ga(Problem pb, GaParams gp, const uint8_t* __restrict__ prev_pop, const int32_t* __restrict__ prev_ms,
+         const int32_t* __restrict__ rec_ms, const uint8_t* __restrict__ rec_gen, uint8_t* __restrict__ pop,
+         int32_t* __restrict__ ms_out, unsigned long long* __restrict__ cand, int* __restrict__ n_cand) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int T = pb.T, GS = gp.GS, RS = odd_row_stride(GS), Tp = perm_offset(T);
+  constexpr int ROWS = LONGT ? 1 : 3;
+  uint8_t* s_blob = sm;
+  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
+  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + ROWS * GA_B * RS);
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);
+  uint64_t* bar = s_lists + GA_B;
+  stage_problem(s_blob, pb, bar);
+  const uint32_t* tab = tab_of(s_blob);
+  const uint8_t* S = S_of(s_blob, pb);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const RowG ch{s_rows + RS * tid, Tp};
+  uint8_t* const rowA = s_rows + GA_B * RS + RS * tid;   // (short genomes only)
+  uint8_t* const rowB = rowA + GA_B * RS;
+  uint32_t* inA = s_bits + tid;   // LOX slice set for T > 32: word w at inA[w * GA_B]
+  const uint32_t P = (uint32_t)gp.P;
+  const uint32_t NP = (P + 1) >> 1;
+  const int nb = (T + 31) / 32;
+  const int nw = (T + 3) >> 2;
+  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
+  const uint32_t k0 = (uint32_t)gp.seed, k1 = (uint32_t)(gp.seed >> 32), c2 = gp.rank << 16;
 
   uint64_t lst = ~0ull;
   // The next top-E can only contain keys <= the last elite's key (the elites are carried):
   // only those are offered to the list.
-  const uint64_t cap = (gp.gen == 0) ? ~0ull : (((uint64_t)(uint32_t)rec_ms[gp.E - 1] << 32) | (uint64_t)(gp.E - 1));
-  const int64_t nthr = (int64_t)gridDim.x * GA_B;
-  // Tournament prefetch: the candidates' makespans of the NEXT child of this thread are
-  // loaded one iteration ahead, so their latency hides behind the current decode.
+  const uint64_t cap = ((uint64_t)(uint32_t)rec_ms[gp.E - 1] << 32) | (uint64_t)(gp.E - 1);
+  // Tournament prefetch: the candidates' makespans of this thread's NEXT pair are loaded one
+  // iteration ahead, so their latency hides behind the current pair's decodes.
   uint32_t t_i1 = 0, t_j1 = 0, t_i2 = 0, t_j2 = 0, t_m1 = 0, t_n1 = 0, t_m2 = 0, t_n2 = 0;
-  auto prefetch = [&](int64_t nslot) {
-    if (gp.gen != 0 && nslot >= gp.E && nslot < gp.P) {
-      const uint4 w0 = philox_block((uint32_t)gp.seed, (uint32_t)(gp.seed >> 32), (uint32_t)nslot, gp.gen,
-                                    gp.rank << 16, 0u);
+  auto prefetch = [&](int64_t q) {
+    if (q < NP && 2 * q + 1 >= (int64_t)gp.E) {
+      const uint4 w0 = philox_block(k0, k1, (uint32_t)q, gp.gen, c2, 0u);
       t_i1 = ubelow(w0.x, P); t_j1 = ubelow(w0.y, P); t_i2 = ubelow(w0.z, P); t_j2 = ubelow(w0.w, P);
       t_m1 = (uint32_t)prev_ms[t_i1]; t_n1 = (uint32_t)prev_ms[t_j1];
       t_m2 = (uint32_t)prev_ms[t_i2]; t_n2 = (uint32_t)prev_ms[t_j2];
     }
   };
-  // DYN: warp chunks of 32 children, the first from the static grid stride, the rest
-  // claimed from a counter (n_cand[1], reset by the previous elite selection) so warps that
-  // finish early take more -- with the static stride the SMs idled in the tail (measured
-  // MIX k_ga -11 %, SWEEP -10 %, TXT -2.6 % with 7 CTAs/SM).  A claim is issued one
-  // iteration before its value is needed.
-  constexpr bool DYN = SAT_GA_DYNAMIC && (NN != 1 || (SAT_GA_DYNAMIC_ONE && GP >= 8));   // (TINY 1x4: +13 %)
-  unsigned int* work = reinterpret_cast<unsigned int*>(n_cand + 1);
-  const auto claim = [&]() -> unsigned int { return lane == 0 ? atomicAdd(work, 32u) : 0u; };
-  int64_t next_base = 0;
-  unsigned int pending = 0;
-  if constexpr (DYN) {
-    next_base = nthr + (int64_t)__shfl_sync(0xffffffffu, claim(), 0);
-    pending = claim();
-  }
+  WarpChunks chunks(n_cand, (int64_t)gridDim.x * GA_B, lane);
   prefetch((int64_t)blockIdx.x * GA_B + (tid & ~31) + lane);
-  for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P;) {
-    const int64_t slot = base + lane;
-    const bool live = slot < gp.P;
-    int msv = INT_MAX;
-    if (SAT_GA_INIT_KERNEL ? INIT : gp.gen == 0) {  // ---------------- initial population
-      if (live) {
-        if (slot < n_seed) {
-          load_row(ch.base, seeds + slot * GS, GS);
-        } else {  // cfg[t] = U(S_t), then Fisher-Yates on the identity
-          Philox rng(gp.seed, (uint32_t)slot, 0u, (gp.rank << 16) | 1u);
-          // (byte loops on purpose: word-wise zeroing here measured k_ga's generation path 7 %
-          // slower -- the one kernel's register allocation / layout changed)
-          for (int t = 0; t < GS; ++t) ch.base[t] = 0;
-          for (int t = 0; t < T; ++t) ch.c(t) = (uint8_t)rng.below(S[t]);
-          for (int t = 0; t < T; ++t) ch.q(t) = (uint8_t)t;
-          for (int i = T - 1; i > 0; --i) {
-            const int j = (int)rng.below(i + 1);
-            const uint8_t a = ch.q(i);
-            ch.q(i) = ch.q(j);
-            ch.q(j) = a;
-          }
-        }
-        if constexpr (DECODE) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+  for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < NP;) {
+    const uint32_t q = (uint32_t)base + lane;   // P < 2^32 (validated at the boundary)
+    const bool live = q < NP;
+    const uint32_t s0 = 2 * q;
+    const bool kid0 = live && s0 >= (uint32_t)gp.E;
+    const bool kid1 = live && s0 + 1 < P && s0 + 1 >= (uint32_t)gp.E;
+    const bool any = kid0 || kid1;
+    uint32_t A = 0, B = 0;
+    if (any) {  // 1. tournaments (words 0..3, makespans prefetched)
+      A = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
+      B = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
+    }
+    prefetch(chunks.next + lane);
+    const uint4 w1 = philox_block(k0, k1, (uint32_t)q, gp.gen, c2, 1u);   // shared fields
+    const uint8_t* gA = prev_pop + (uint64_t)A * GS;
+    const uint8_t* gB = prev_pop + (uint64_t)B * GS;
+    if (!LONGT && any) {
+      load_row(rowA, gA, GS);
+      load_row(rowB, gB, GS);
+    }
+    const bool xo = any && (w1.x & 0xffffu) < px16;
+    uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
+    if (a > b) { const uint32_t x = a; a = b; b = x; }
+#pragma unroll 1
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t slot = s0 + r;
+      const bool in = live && slot < P;
+      const bool elite = in && slot < (uint32_t)gp.E;
+      const bool child = r ? kid1 : kid0;
+      // 2. child r = X (A for r = 0, B for r = 1) crossed with Y (the other parent)
+      const uint8_t* X = LONGT ? (r ? gB : gA) : (r ? rowB : rowA);
+      const uint8_t* Y = LONGT ? (r ? gA : gB) : (r ? rowA : rowB);
+      const uint4 wk = philox_block(k0, k1, (uint32_t)q, gp.gen, c2, 2u + (uint32_t)r);   // child r's fields
+      int msv = INT_MAX;
+      if (elite) {
+        load_row(ch.base, rec_gen + (size_t)slot * GS, GS);
+        msv = rec_ms[slot];
       }
-    } else {  // ---------------- generation gen >= 1
-      const bool elite = live && slot < gp.E;
-      const bool child = live && slot >= gp.E;
-      PhiloxWords rw(gp.seed, (uint32_t)slot, gp.gen, gp.rank << 16);
-      uint32_t A = 0, B = 0;
-      if (child) {  // 1. tournaments (words 0..3, makespans prefetched)
-        A = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
-        B = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
-      }
-      if constexpr (DYN) prefetch(next_base + lane);
-      else prefetch(slot + nthr);
-      const uint4 w1 = rw.block(1), w2 = rw.block(2);
-      rw.blk = 2;
-      rw.cur = w2;
-      // 2. child = A (elites: the elite record)
-      if (elite) load_row(ch.base, rec_gen + slot * GS, GS);
       if (child) {
-        load_row(ch.base, prev_pop + (uint64_t)A * GS, GS);
-        if (rows == 2) load_row(gb.base, prev_pop + (uint64_t)B * GS, GS);
-      }
-      const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
-      const bool xo = child && (w1.x & 0xffffu) < px16;
-      uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
-      if (a > b) { const uint32_t x = a; a = b; b = x; }
-      // 3. uniform crossover of the config genes (bits from words 9 .. 9+nb-1), 4 genes per step
-      {
-        const uint32_t* ca = reinterpret_cast<const uint32_t*>(ch.base);
+        // 3. uniform crossover of the config genes, 4 genes per step (bit 1 -> X's gene);
+        //    the permutation starts as a copy of X's
+        const uint32_t* cx = reinterpret_cast<const uint32_t*>(X);
+        const uint32_t* cy = reinterpret_cast<const uint32_t*>(Y);
         uint32_t* cw = reinterpret_cast<uint32_t*>(ch.base);
         uint32_t bits = 0;
-        if (rows == 2) {
-          const uint32_t* cb = reinterpret_cast<const uint32_t*>(gb.base);
-          for (int t = 0; t < T; t += 4) {
-            if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
-            const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;     // 1 -> take B's gene
-            const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;  // nibble -> byte mask
-            const uint32_t wa = ca[t >> 2], wb = cb[t >> 2];
-            cw[t >> 2] = (wa & ~m) | (wb & m);                               // pad bytes: 0 in both
+        for (int t = 0; t < T; t += 4) {
+          if ((t & 31) == 0) {
+            const int k = t >> 5;
+            bits = k == 0 ? w1.z : (k == 1 ? w1.w : philox_word(k0, k1, (uint32_t)q, gp.gen, c2, 16u + (k - 2)));
           }
-        } else {   // B's config words from the population (global, L1-cached)
-          const uint32_t* cb = reinterpret_cast<const uint32_t*>(prev_pop + (uint64_t)B * GS);
-          for (int t = 0; t < T; t += 4) {
-            if ((t & 31) == 0) bits = rw.word(9 + (t >> 5));
-            const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;
-            const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
-            const uint32_t wa = ca[t >> 2], wb = cb[t >> 2];
-            cw[t >> 2] = (wa & ~m) | (wb & m);
-          }
+          const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;     // 1 -> take Y's gene
+          const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;  // nibble -> byte mask
+          cw[t >> 2] = (cx[t >> 2] & ~m) | (cy[t >> 2] & m);               // pad bytes: 0 in both
         }
+        for (int w = 0; w < nw; ++w) cw[(Tp >> 2) + w] = cx[(Tp >> 2) + w];
       }
-      // 4. LOX (linear order crossover): keep A.perm[a..b] in place; fill positions 0..a-1,
-      //    then b+1..T-1, with B's genes in B's order from position 0, skipping the slice's
-      //    genes.  No wrap-around: the write pointer jumps over the slice once.
+      // 4. LOX: keep X.perm[a..b] in place; fill positions 0..a-1, then b+1..T-1, with Y's
+      //    genes in Y's order from position 0, skipping the slice's genes.
       {
         uint8_t* const p0 = &ch.q(0);
         uint8_t* const pa = p0 + a;
         const uint32_t gap = b - a + 1;
         uint8_t* wp = (a == 0) ? p0 + gap : p0;
-        if (short_t) {
+        const uint8_t* Yq = Y + Tp;
+        if (!LONGT) {
           uint32_t kept = 0;
-          for (int q = 0; q < T; ++q) {
-            const uint32_t bit = 1u << ch.q(q);
-            kept |= ((uint32_t)q - a <= b - a) ? bit : 0u;
+          for (int k = 0; k < T; ++k) {
+            const uint32_t bit = 1u << ch.q(k);
+            kept |= ((uint32_t)k - a <= b - a) ? bit : 0u;
           }
-          if (!xo) kept = 0xffffffffu;   // nothing is taken
+          if (!(xo && child)) kept = 0xffffffffu;   // nothing is taken
           for (int k = 0; k < T; ++k) {   // branch-free: predicated store, pointer arithmetic
-            const uint32_t x = gb.q(k);
+            const uint32_t x = Yq[k];
             const uint32_t take = (~kept >> x) & 1u;
             if (take) *wp = (uint8_t)x;
             wp += take;
             wp = (wp == pa) ? wp + gap : wp;
           }
         } else {
-          // Rows of lanes without a child (elites, past the population) hold stale bytes: the
-          // word index is clamped so those lanes stay inside this thread's ceil(T/32) words.
+          // Rows of lanes without a child hold stale bytes: the word index is clamped so
+          // those lanes stay inside this thread's ceil(T/32) words.
           for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
-          for (int q = (int)a; q <= (int)b; ++q) {
-            const int x = ch.q(q);
+          for (int k = (int)a; k <= (int)b; ++k) {
+            const int x = ch.q(k);
             inA[min(x >> 5, nb - 1) * GA_B] |= 1u << (x & 31);
           }
-          const uint32_t xm = xo ? 1u : 0u;
-          const uint8_t* Bq = (rows == 2) ? gb.base + Tp : prev_pop + (uint64_t)B * GS + Tp;
+          const uint32_t xm = (xo && child) ? 1u : 0u;
           for (int k = 0; k < T; ++k) {
-            const int x = Bq[k];
+            const int x = child ? Yq[k] : 0;
             const uint32_t take = (~inA[min(x >> 5, nb - 1) * GA_B] >> (x & 31)) & xm;
             if (take) *wp = (uint8_t)x;
             wp += take;
@@ -985,24 +1019,22 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         }
       }
       // 5. config mutation of one job
-      if (child && (w1.w >> 16) < pc16) {
-        const int t = (int)v16(w2.x & 0xffffu, T);
-        ch.c(t) = (uint8_t)v16(w2.x >> 16, S[t]);
+      if (child && (wk.z & 0xffffu) < pc16) {
+        const int t = (int)v16(wk.z >> 16, T);
+        ch.c(t) = (uint8_t)v16(wk.w & 0xffffu, S[t]);
       }
       // 6. permutation mutation.  Swap (kind 0): two byte moves.  Insertion (kind 1, remove
       //    the gene at i, reinsert it at j): positions between i and j shift by one toward i,
-      //    done a word (4 genes) at a time with funnel shifts and byte masks, then x -> j.
-      const bool pmut = child && (w1.y >> 16) < pm16;
-      if (pmut) {
-        const int kind = (int)(w1.z & 1u);
-        const int mi = (int)v16(w1.z >> 16, T), mj = (int)v16(w1.w & 0xffffu, T);
+      //    a word (4 genes) at a time with funnel shifts and byte masks, then x -> j.
+      if (child && (wk.x & 0xffffu) < pm16) {
+        const int kind = (int)((wk.y >> 16) & 1u);
+        const int mi = (int)v16(wk.x >> 16, T), mj = (int)v16(wk.y & 0xffffu, T);
         const uint8_t xi = ch.q(mi), xj = ch.q(mj);
         if (kind == 0) {
           ch.q(mi) = xj;
           ch.q(mj) = xi;
         } else if (mi != mj) {
           const int lo = min(mi, mj), hi = max(mi, mj);
-          const int nw = (T + 3) >> 2;
           uint32_t* pw = reinterpret_cast<uint32_t*>(ch.base + Tp);
           int w = lo >> 2;
           uint32_t prev = (w > 0) ? pw[w - 1] : 0u, cur = pw[w];
@@ -1018,226 +1050,81 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           ch.q(mj) = xi;
         }
       }
-      if constexpr (DECODE) {
-        if (elite) msv = rec_ms[slot];
-        if (child) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      if (child) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      if (in) {
+        store_row(pop + (size_t)slot * GS, ch.base, GS);
+        ms_out[slot] = msv;
       }
+      topE_insert(lst, in ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull, gp.E, cap);
     }
-    if (live) {
-      store_row(pop + slot * GS, ch.base, GS);
-      if constexpr (DECODE) ms_out[slot] = msv;
-    }
-    if constexpr (DECODE) {
-      const uint64_t key = live ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
-      topE_insert(lst, key, gp.E, cap);
-    }
-    if constexpr (DYN) {
-      base = next_base;
-      next_base = nthr + (int64_t)__shfl_sync(0xffffffffu, pending, 0);
-      pending = claim();
-    } else {
-      base += nthr;
-    }
+    base = chunks.advance();
   }
-  if constexpr (!DECODE) return;
-  // block-level merge of the warps' lists -> one candidate list per block
-  s_lists[tid] = lst;
-  __syncthreads();
-  if (tid < 32) {
-    uint64_t m = ~0ull;
-    for (int w = 0; w < GA_B / 32; ++w) topE_insert(m, s_lists[w * 32 + lane], gp.E);
-    // append only the real keys (after the first generation most blocks have none)
-    const bool real = lane < gp.E && m != ~0ull;
-    const uint32_t mask = __ballot_sync(0xffffffffu, real);
-    int off = 0;
-    if (lane == 0 && mask) off = atomicAdd(n_cand, __popc(mask));
-    off = __shfl_sync(0xffffffffu, off, 0);
-    if (real) cand[off + __popc(mask & ((1u << lane) - 1u))] = m;
-  }
+  emit_topE(lst, s_lists, gp.E, cand, n_cand);
 }
 
-// The split generation (SATURN_GA_SPLIT=1): k_ga<..., false> breeds children into the
-// population (GA operators only), then k_decode_pop decodes the whole population like
-// k_evaluate (register-light decoder, full occupancy), keeping the elites' makespans and
-// the top-E bookkeeping.  Measured r1: breed 0.198 + decode 0.186 ms vs fused 0.361 ms per
-// TXT generation of 4.2M children, so the fused kernel (GA operators and decode of
-// different warps overlap on the SM) is the default.
-constexpr int DP_B = 128;
-static size_t dp_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, DP_B) + (size_t)DP_B * odd_row_stride(GS) + 8 * DP_B + 8;
-}
-
-template <int NN, int GP>
-__global__ void __launch_bounds__(DP_B) k_decode_pop(Problem pb, GaParams gp, const uint8_t* __restrict__ pop,
-                                                     const int32_t* __restrict__ rec_ms, int32_t* __restrict__ ms_out,
-                                                     unsigned long long* __restrict__ cand, int* __restrict__ n_cand) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  const int T = pb.T, GS = gp.GS, RS = odd_row_stride(GS), Tp = perm_offset(T);
-  uint8_t* s_blob = sm;
-  int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, DP_B);
-  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_rows + DP_B * RS + ((8 - (DP_B * RS) % 8) % 8));
-  uint64_t* bar = s_lists + DP_B;
-  stage_problem(s_blob, pb, bar);
-  const uint32_t* tab = tab_of(s_blob);
-  const uint8_t* S = S_of(s_blob, pb);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const RowG g{s_rows + RS * tid, Tp};
-  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
-  const uint64_t cap = (gp.gen == 0) ? ~0ull : (((uint64_t)(uint32_t)rec_ms[gp.E - 1] << 32) | (uint64_t)(gp.E - 1));
-  uint64_t lst = ~0ull;
-  const int per_rec = GS / 16;
-  for (int64_t base = (int64_t)blockIdx.x * DP_B; base < gp.P; base += (int64_t)gridDim.x * DP_B) {
-    const int cnt = (int)min((int64_t)DP_B, gp.P - base);
-    // coalesced tile load: uint4 k of the tile -> row k / per_rec, bytes 16 (k % per_rec) ..
-    const uint4* src = reinterpret_cast<const uint4*>(pop + base * GS);
-    for (int k = tid; k < cnt * per_rec; k += DP_B) {
-      const uint4 v = src[k];
-      uint32_t* d = reinterpret_cast<uint32_t*>(s_rows + RS * (k / per_rec) + 16 * (k % per_rec));
-      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-    }
-    __syncthreads();
-    const int64_t slot = base + tid;
-    int msv = INT_MAX;
-    if (tid < cnt) {
-      msv = (gp.gen != 0 && slot < gp.E) ? rec_ms[slot] : decode_T<NN, GP, 0>(tab, S, pb.stride, g, T, pb, ns);
-      ms_out[slot] = msv;
-    }
-    const uint64_t key = (tid < cnt) ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull;
-    topE_insert(lst, key, gp.E, cap);
-    __syncthreads();
-  }
-  s_lists[tid] = lst;
-  __syncthreads();
-  if (tid < 32) {
-    uint64_t m = ~0ull;
-    for (int w = 0; w < DP_B / 32; ++w) topE_insert(m, s_lists[w * 32 + lane], gp.E);
-    const bool real = lane < gp.E && m != ~0ull;
-    const uint32_t mask = __ballot_sync(0xffffffffu, real);
-    int off = 0;
-    if (lane == 0 && mask) off = atomicAdd(n_cand, __popc(mask));
-    off = __shfl_sync(0xffffffffu, off, 0);
-    if (real) cand[off + __popc(mask & ((1u << lane) - 1u))] = m;
-  }
-}
-
-static bool ga_split() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SATURN_GA_SPLIT");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-// One GA launch of shape (A, B): the kernel variant is picked by generation 0 (INIT) and
-// by T > 32 (LONGT).
-template <int A, int B, bool DEC, bool I, bool L>
-static cudaError_t ga_go(const Problem& pb, const GaParams& gp, const uint8_t* seeds, int64_t n_seed,
-                         const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen,
-                         uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, size_t smem, int sms,
-                         int64_t blocks, cudaStream_t st) {
-  const int g = grid_for(k_ga<A, B, DEC, I, L>, GA_B, smem, sms, blocks);
-  k_ga<A, B, DEC, I, L><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
-                                                cand, d_n_cand);
-  return cudaGetLastError();
-}
-template <int A, int B, bool DEC>
+template <int A, int B>
 static cudaError_t ga_shape(const Problem& pb, const GaParams& gp, const uint8_t* seeds, int64_t n_seed,
                             const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
                             const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand,
-                            size_t smem, int sms, int64_t blocks, cudaStream_t st) {
-  const bool init = gp.gen == 0, longt = pb.T > 32;
-#define SAT_GO(I, L) \
-  ga_go<A, B, DEC, I, L>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, smem, sms, \
-                         blocks, st)
-  if (init) return longt ? SAT_GO(true, true) : SAT_GO(true, false);
-  return longt ? SAT_GO(false, true) : SAT_GO(false, false);
-#undef SAT_GO
+                            int sms, cudaStream_t st) {
+  const bool init = gp.gen == 0;
+  const size_t smem = ga_smem_bytes(pb, A, B, gp.GS, init);
+  if (init) {
+    const int g = grid_for(k_ga_init<A, B>, GA_B, smem, sms, (gp.P + GA_B - 1) / GA_B);
+    k_ga_init<A, B><<<g, GA_B, smem, st>>>(pb, gp, seeds, n_seed, pop, ms, cand, d_n_cand);
+    return cudaGetLastError();
+  }
+  const int64_t blocks = ((gp.P + 1) / 2 + GA_B - 1) / GA_B;
+  if (pb.T > 32) {
+    const int g = grid_for(k_ga<A, B, true>, GA_B, smem, sms, blocks);
+    k_ga<A, B, true><<<g, GA_B, smem, st>>>(pb, gp, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand);
+  } else {
+    const int g = grid_for(k_ga<A, B, false>, GA_B, smem, sms, blocks);
+    k_ga<A, B, false><<<g, GA_B, smem, st>>>(pb, gp, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand);
+  }
+  return cudaGetLastError();
 }
 // grid size the largest variant of a shape can take (candidate buffer sizing)
 template <int A, int B>
-static int ga_grid_max(size_t smem, int sms, int64_t blocks) {
-  return std::max(std::max(grid_for(k_ga<A, B, true, false, false>, GA_B, smem, sms, blocks),
-                           grid_for(k_ga<A, B, true, true, false>, GA_B, smem, sms, blocks)),
-                  std::max(grid_for(k_ga<A, B, true, false, true>, GA_B, smem, sms, blocks),
-                           grid_for(k_ga<A, B, true, true, true>, GA_B, smem, sms, blocks)));
+static int ga_grid_max(const Problem& pb, int GS, int sms, int64_t P) {
+  const size_t s0 = ga_smem_bytes(pb, A, B, GS, true), s1 = ga_smem_bytes(pb, A, B, GS, false);
+  const int64_t b0 = (P + GA_B - 1) / GA_B, b1 = ((P + 1) / 2 + GA_B - 1) / GA_B;
+  return std::max(grid_for(k_ga_init<A, B>, GA_B, s0, sms, b0),
+                  std::max(grid_for(k_ga<A, B, false>, GA_B, s1, sms, b1), grid_for(k_ga<A, B, true>, GA_B, s1, sms, b1)));
 }
 
 static cudaError_t launch_ga(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
                              int64_t n_seed, const uint8_t* prev_pop, const int32_t* prev_ms, const int32_t* rec_ms,
                              const uint8_t* rec_gen, uint8_t* pop, int32_t* ms, unsigned long long* cand,
-                             int* d_n_cand, int sms, cudaStream_t st, cudaEvent_t mid) {
-  const int64_t blocks = (gp.P + GA_B - 1) / GA_B;
-  if (ga_split()) {
-    {
-      const size_t smem = ga_smem_bytes(pb, 1, 2, gp.GS);
-      const cudaError_t e = ga_shape<1, 2, false>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms,
-                                                  cand, d_n_cand, smem, sms, blocks, st);
-      if (e != cudaSuccess) return e;
-    }
-    if (mid) cudaEventRecord(mid, st);
-    const size_t smem = dp_smem_bytes(pb, NN, GP, gp.GS);
-    const int64_t dblocks = (gp.P + DP_B - 1) / DP_B;
-#define SAT_DP(a, b)                                                                                   \
-  if (NN == a && GP == b) {                                                                            \
-    const int g = grid_for(k_decode_pop<a, b>, DP_B, smem, sms, dblocks);                              \
-    k_decode_pop<a, b><<<g, DP_B, smem, st>>>(pb, gp, pop, rec_ms, ms, cand, d_n_cand);                \
-    return cudaGetLastError();                                                                         \
-  }
-    SAT_SHAPES(SAT_DP)
-#undef SAT_DP
-    return cudaErrorInvalidConfiguration;
-  }
-  const size_t smem = ga_smem_bytes(pb, NN, GP, gp.GS);
-#define SAT_GA(a, b)                                                                                        \
-  if (NN == a && GP == b) {                                                                                 \
-    const cudaError_t e = ga_shape<a, b, true>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen,   \
-                                               pop, ms, cand, d_n_cand, smem, sms, blocks, st);             \
-    if (mid) cudaEventRecord(mid, st);                                                                      \
-    return e;                                                                                               \
-  }
+                             int* d_n_cand, int sms, cudaStream_t st) {
+#define SAT_GA(a, b)                                                                                               \
+  if (NN == a && GP == b)                                                                                          \
+    return ga_shape<a, b>(pb, gp, seeds, n_seed, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, \
+                          st);
   SAT_SHAPES(SAT_GA)
 #undef SAT_GA
   return cudaErrorInvalidConfiguration;
 }
 
 int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms) {
-  const int64_t blocks = (P + GA_B - 1) / GA_B;
-  int g1 = 0, g2 = 0;
-  {
-    const size_t smem = dp_smem_bytes(pb, NN, GP, GS);
-    const int64_t dblocks = (P + DP_B - 1) / DP_B;
+  int g = 0;
 #define SAT_GAC(a, b) \
-    if (NN == a && GP == b) g1 = grid_for(k_decode_pop<a, b>, DP_B, smem, sms, dblocks);
-    SAT_SHAPES(SAT_GAC)
+  if (NN == a && GP == b) g = ga_grid_max<a, b>(pb, GS, sms, P);
+  SAT_SHAPES(SAT_GAC)
 #undef SAT_GAC
-  }
-  {
-    const size_t smem = ga_smem_bytes(pb, NN, GP, GS);
-#define SAT_GAC(a, b) \
-    if (NN == a && GP == b) g2 = ga_grid_max<a, b>(smem, sms, blocks);
-    SAT_SHAPES(SAT_GAC)
-#undef SAT_GAC
-  }
-  return std::max(g1, g2) * E;
+  return g * E;
 }
 
 cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* seeds,
                            int64_t n_seed, uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms,
                            cudaStream_t st) {
-  return launch_ga(pb, NN, GP, gp, seeds, n_seed, nullptr, nullptr, nullptr, nullptr, pop, ms, cand, d_n_cand, sms,
-                   st, nullptr);
+  return launch_ga(pb, NN, GP, gp, seeds, n_seed, nullptr, nullptr, nullptr, nullptr, pop, ms, cand, d_n_cand, sms, st);
 }
 cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
                                  const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen, uint8_t* pop,
-                                 int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms, cudaStream_t st,
-                                 cudaEvent_t mid) {
-  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, st,
-                   mid);
+                                 int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms, cudaStream_t st) {
+  return launch_ga(pb, NN, GP, gp, nullptr, 0, prev_pop, prev_ms, rec_ms, rec_gen, pop, ms, cand, d_n_cand, sms, st);
 }
-
-bool ga_is_split() { return ga_split(); }
 
 // ------------------------------------------------------------------ f4: local search
 // One CTA per genome: every thread decodes neighbours (insertion moves, then config moves;

@@ -77,9 +77,8 @@ cudaError_t launch_ga_init(const Problem& pb, int NN, int GP, const GaParams& gp
 cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaParams& gp, const uint8_t* prev_pop,
                                  const int32_t* prev_ms, const int32_t* rec_ms, const uint8_t* rec_gen,
                                  uint8_t* pop, int32_t* ms, unsigned long long* cand, int* d_n_cand, int sms,
-                                 cudaStream_t st, cudaEvent_t mid = nullptr);
+                                 cudaStream_t st);
 // True when a generation is two kernels (breed, then decode); `mid` is recorded between them.
-bool ga_is_split();
 // Upper bound of the candidates one GA launch can append (grid x E).
 int ga_max_candidates(const Problem& pb, int NN, int GP, int E, int GS, int64_t P, int sms);
 // Top-E of the *d_n_cand candidate keys -> elite records (ms, genome) copied from `pop`.

@@ -65,10 +65,10 @@ class Result(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("ga_launches", ctypes.c_int64), ("ga_kernel_ms", ctypes.c_double), ("ga_decodes", ctypes.c_int64),
-                ("breed_kernel_ms", ctypes.c_double), ("decode_kernel_ms", ctypes.c_double)]
+                ("_spare", ctypes.c_int64 * 4)]   # room for older builds' longer struct (A/B runs)
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
 
 
 class IntrospectParams(ctypes.Structure):

@@ -437,36 +437,6 @@ def test_island_group_rejects_mismatched_handles(sat, torch):
         sat.search_group([a, a], sat.SearchConfig(population=128, elites=4, max_generations=1))
 
 
-def test_split_generation_mode_replays(sat, torch):
-    """SATURN_GA_SPLIT=1 (breed kernel + population decode kernel) reproduces the same GA
-    trajectory as the oracle (run in a subprocess: the mode is read once per process)."""
-    import subprocess
-    import sys
-    from conftest import ROOT
-    code = r'''
-import sys; sys.path.insert(0, %r)
-import numpy as np, oracle, synth
-from oracle import ga as oga
-import paper_2309_01226_b200 as sat
-inst = synth.txt(2); c = oracle.compact(inst.node_gpus, inst.runtime)
-P, E, seed = 256, 8, 5
-cfg, perm = oga.initial_population(c.S, P, seed); ms = oracle.decode_batch(c, cfg, perm)
-for gen in (1, 2, 3):
-    cfg, perm, _ = oga.next_generation(c.S, cfg, perm, ms, gen, seed, 0, E, oga.q32(0.9), oga.q32(0.5), oga.q32(0.5))
-    ms = oracle.decode_batch(c, cfg, perm)
-plan = sat.Plan(inst.node_gpus, 0).load_runtime_table(inst.runtime)
-plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=3, elites=E, generations_per_epoch=1,
-                             p_xover=0.9, p_cfg_mut=0.5, p_perm_mut=0.5))
-gc, gq, gm = plan.search_population(P)
-assert np.array_equal(gc, cfg) and np.array_equal(gq, perm) and np.array_equal(gm, ms)
-print("SPLIT-OK")
-''' % ROOT
-    import os
-    env = dict(os.environ, SATURN_GA_SPLIT="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert "SPLIT-OK" in out.stdout, out.stderr[-2000:]
-
-
 # ------------------------------------------------------------------ f4: node genes
 def test_node_genes_match_oracle(sat, torch):
     for inst in (synth.mix(3), synth.sweep(2, n_jobs=40), synth.sweep(4, n_jobs=30, nodes=[2, 2, 4, 8]),
@@ -660,8 +630,9 @@ def test_bench_scale_search_sampled_replay(sat, torch, name):
     kq = np.array([k[1] for k in kids], np.uint8)
     assert np.array_equal(c16[slots], kc) and np.array_equal(q16[slots], kq)
     assert np.array_equal(m16[slots], oracle.decode_batch(c, kc, kq))
-    # the reported best = population minimum; its plan re-validates
-    assert r["makespan"] == int(m16.min()) == int(m16[0])
+    # the reported best = population minimum (a generation-16 child may beat the carried
+    # elites at slots 0..E-1); its plan re-validates
+    assert r["makespan"] == int(m16.min()) <= int(m16[0]) == int(m15.min())
     best, pl, bc, bp = plan.best_plan()
     ms, _ = oracle.decode(c, bc, bp)
     assert ms == best == r["makespan"] and oracle.validate(c, pl, best) == []

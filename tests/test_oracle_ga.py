@@ -56,6 +56,9 @@ def test_lox_hand_example():
 
 
 def test_lox_keeps_slice_and_order():
+    """GA v5: slots 2q, 2q+1 are the children of pair q (stream (q, gen, rank << 16)); child 0
+    keeps A's slice and fills in B's order, child 1 the reverse; the config genes are split
+    complementarily by the crossover bits (bit 1 -> the child's own parent X)."""
     from oracle.philox import Stream
     c, cfg, perm, ms = _setup(P=16)
     T = c.n_jobs
@@ -63,19 +66,42 @@ def test_lox_keeps_slice_and_order():
     for slot in range(4, 16):
         child_cfg, child_perm = ga.make_child(c.S, cfg, perm, ms, slot, 1, 3, 0,
                                               p_x=0xFFFFFFFF, p_c=0, p_m=0)
-        st = Stream((3, 0), slot, 1, 0)
-        w = [st.u32() for _ in range(10)]
+        st = Stream((3, 0), slot >> 1, 1, 0)
+        w = [st.u32() for _ in range(8)]
         i, j = (w[0] * 16) >> 32, (w[1] * 16) >> 32
         A = i if (ms[i], i) < (ms[j], j) else j
         i, j = (w[2] * 16) >> 32, (w[3] * 16) >> 32
         B = i if (ms[i], i) < (ms[j], j) else j
+        X, Y = (A, B) if slot % 2 == 0 else (B, A)
         a, b = sorted((((w[4] >> 16) * T) >> 16, ((w[5] & 0xFFFF) * T) >> 16))
-        assert list(child_perm[a:b + 1]) == list(perm[A][a:b + 1])
-        rest = [x for x in perm[B] if x not in set(perm[A][a:b + 1])]
+        assert list(child_perm[a:b + 1]) == list(perm[X][a:b + 1])
+        rest = [x for x in perm[Y] if x not in set(perm[X][a:b + 1])]
         filled = list(child_perm[:a]) + list(child_perm[b + 1:])
         assert filled == rest
         for t in range(T):
-            assert child_cfg[t] == (cfg[A][t] if (w[9] >> t) & 1 else cfg[B][t])
+            assert child_cfg[t] == (cfg[X][t] if (w[6] >> t) & 1 else cfg[Y][t])
+
+
+def test_pair_children_complementary():
+    """Both children of a pair, no mutation: every config gene of A and B goes to exactly one
+    child (uniform crossover's two offspring), and each child is a valid genome."""
+    c, cfg, perm, ms = _setup(P=32)
+    T = c.n_jobs
+    for q in range(2, 16):
+        c0, p0 = ga.make_child(c.S, cfg, perm, ms, 2 * q, 3, 5, 0, p_x=0xFFFFFFFF, p_c=0, p_m=0)
+        c1, p1 = ga.make_child(c.S, cfg, perm, ms, 2 * q + 1, 3, 5, 0, p_x=0xFFFFFFFF, p_c=0, p_m=0)
+        assert sorted(p0) == list(range(T)) and sorted(p1) == list(range(T))
+        # the multiset {c0[t], c1[t]} is the parents' {A[t], B[t]} for some parent pair
+        found = False
+        for A in range(32):
+            for B in range(32):
+                if all(sorted((int(c0[t]), int(c1[t]))) == sorted((int(cfg[A][t]), int(cfg[B][t])))
+                       for t in range(T)):
+                    found = True
+                    break
+            if found:
+                break
+        assert found
 
 
 def test_mutation_only_changes_what_fired():

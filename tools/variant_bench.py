@@ -46,6 +46,4 @@ step_ms = a.elapsed_time(b) / 10
 print(json.dumps({"lib": lib, "workload": name, "evaluate_plans_per_s": ev, "step_ms": step_ms,
                   "ga_kernel_ms": st["ga_kernel_ms"] / st["ga_launches"],
                   "ga_children_per_s": st["ga_decodes"] / (st["ga_kernel_ms"] * 1e-3), "best": r["makespan"],
-                  "breed_ms": st.get("breed_kernel_ms", 0) / st["ga_launches"],
-                  "decode_ms": st.get("decode_kernel_ms", 0) / st["ga_launches"],
-                  "split": os.environ.get("SATURN_GA_SPLIT", "0")}))
+}))
