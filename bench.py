@@ -175,7 +175,8 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
-def _config(args, extra):
+def _config(args, extra=None):
+    """The workload description -- identical in both arms (no result keys in here)."""
     cfg = {"workload": WORKLOADS[args.workload], "table_seed": 0, "population_per_gpu": args.population,
            "generations_per_step": args.generations, "elites": args.elites,
            "parallelism": f"islands x{args.gpus} (one GA population per GPU, elite exchange over "
@@ -189,13 +190,200 @@ def _config(args, extra):
     return cfg
 
 
-def _traffic(workload: str):
-    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+def _json(path):
     try:
-        with open(path) as f:
-            return json.load(f).get(workload)
+        with open(os.path.join(ROOT, path)) as f:
+            return json.load(f)
     except Exception:
         return None
+
+
+def _traffic(workload: str):
+    d = _json(os.path.join("profiles", "roofline_traffic.json")) or {}
+    return d.get(workload)
+
+
+def host_cpu():
+    """Host CPU model and core count (lscpu's 'Model name'; /proc/cpuinfo fallback)."""
+    model = None
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    if model is None:
+        try:
+            for ln in open("/proc/cpuinfo"):
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        except Exception:
+            pass
+    return {"model": model, "cores": os.cpu_count()}
+
+
+def _bar(workload: str, seed: int):
+    """The committed 5-minute CPU bar of (workload, table seed) and its lower bound."""
+    for rnd in ("r2", "r1"):
+        d = _json(os.path.join("profiles", rnd, "quality_bar.json" if workload == "TXT"
+                               else f"quality_bar_{workload}.json"))
+        if d and str(seed) in d.get("seeds", {}):
+            e = d["seeds"][str(seed)]
+            return {"bar": e.get("bar"), "bar_file": f"profiles/{rnd}/" + ("quality_bar.json" if workload == "TXT"
+                                                                          else f"quality_bar_{workload}.json"),
+                    "bar_lower_bound": e.get("lower_bound"), "bar_best_lower_bound": e.get("best_lower_bound")}
+    return {"bar": None}
+
+
+def measure_search(sat, torch, plan, inst, scfg, steps, warmup, stream, G, barrier=None, max_over_ranks=None):
+    """Device-timed search steps (CUDA events on the launching stream) plus the sampled k_ga
+    launch times; returns (dict, stats, last result)."""
+    barrier = barrier or torch.cuda.synchronize
+    max_over_ranks = max_over_ranks or (lambda x: x)
+    for _ in range(max(warmup, 0)):
+        plan.search(scfg, stream=stream)
+    barrier()
+    plan.reset_stats()
+    plan.set_profiling(4)          # k_ga launches 2, 6, 10, 14 of each step carry CUDA events
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evaluated = 0
+    barrier()
+    ev0.record(stream)
+    for _ in range(steps):
+        r = plan.search(scfg, stream=stream)
+        evaluated += r["evaluated"]
+    ev1.record(stream)
+    barrier()
+    st = plan.stats()
+    plan.set_profiling(False)
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    return {"value": evaluated / (dev_ms * 1e-3), "ms_per_step": dev_ms / steps, "evaluated": evaluated}, st, r
+
+
+def measure_e2e(plan, inst, scfg, steps, stream, torch, max_over_ranks=None):
+    """The same metric through the host API with host buffers: table upload, search, and the
+    trace-decoded best plan copied back, every step."""
+    max_over_ranks = max_over_ranks or (lambda x: x)
+    plan.reset_stats()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev = 0
+    for _ in range(steps):
+        plan.load_runtime_table(inst.runtime)
+        r = plan.search(scfg, stream=stream)
+        plan.best_plan()
+        ev += r["evaluated"]
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    st = plan.stats()
+    return {"value": ev / e2e_s, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"] // steps,
+            "d2h_bytes_per_step": st["d2h_bytes"] // steps}
+
+
+def ga_roofline(st, T, node_gpus, G, steps, dev_ms):
+    ops = algorithmic_ops_per_plan(T, node_gpus)
+    launch_s = st["ga_kernel_ms"] * 1e-3 / max(st["ga_launches"], 1)
+    units = st["ga_decodes"] / max(st["ga_launches"], 1)
+    achieved = ops * units / launch_s
+    return {"bound": "alu", "achieved": achieved / 1e12, "peak": ALU_PEAK_OPS / 1e12, "unit": "TOP/s",
+            "frac": achieved / ALU_PEAK_OPS,
+            "kernel": "k_ga (Philox GA operators fused with the sorted-multiset decode)",
+            "ops_per_plan": ops, "plans_per_launch": units, "launch_ms": launch_s * 1e3,
+            "launches_timed": st["ga_launches"],
+            # k_ga launches in the timed region (G per step; generation 0 is k_ga_init) x their
+            # mean duration / device time
+            "kernel_share_of_step": (launch_s * 1e3 * G * steps / dev_ms) if dev_ms > 0 else None}
+
+
+def evaluate_rate(sat, torch, plan, n, reps=5, kind=None):
+    """k_evaluate alone (caller genomes resident in HBM): plans/s."""
+    import synth
+    S = plan.num_configs()
+    cfg_h, perm_h = synth.random_genomes(S, n, seed=5)
+    cfg_d, perm_d = torch.from_numpy(cfg_h).cuda(), torch.from_numpy(perm_h).cuda()
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    if kind is not None:
+        plan.set_decoder(kind)
+    for _ in range(3):
+        plan.evaluate(cfg_d, perm_d, out)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        plan.evaluate(cfg_d, perm_d, out)
+    b.record()
+    torch.cuda.synchronize()
+    plan.set_decoder(sat.DECODER_AUTO)
+    return n * reps / (a.elapsed_time(b) * 1e-3)
+
+
+def workload_legs(sat, torch, args, local, stream, names):
+    """Every BASELINE config besides the headline one, same step definition: search
+    plans/s (device-timed), e2e, k_ga roofline fraction, k_evaluate plans/s and fraction."""
+    import synth
+    legs = {}
+    for name in names:
+        inst = synth.by_name(name, 0)
+        plan = sat.Plan(inst.node_gpus, local).load_runtime_table(inst.runtime)
+        G = args.generations
+        scfg = sat.SearchConfig(seed=2309, population=args.population, max_generations=G, elites=args.elites,
+                                generations_per_epoch=max(1, G // 2))
+        steps = 5 if name == "SWEEP" else 20
+        m, st, r = measure_search(sat, torch, plan, inst, scfg, steps, 2, stream, G)
+        e2e = measure_e2e(plan, inst, scfg, max(2, steps // 4), stream, torch)
+        rl = ga_roofline(st, inst.n_jobs, inst.node_gpus, G, steps, m["ms_per_step"] * steps)
+        n_eval = (1 << 21) if name == "SWEEP" else (1 << 24)
+        ev = evaluate_rate(sat, torch, plan, n_eval)
+        ops = algorithmic_ops_per_plan(inst.n_jobs, inst.node_gpus)
+        legs[name] = {"workload": WORKLOADS[name], "value": m["value"], "unit": UNIT, "ms_per_step": m["ms_per_step"],
+                      "steps": steps, "e2e": e2e["value"], "k_ga_frac": rl["frac"], "k_ga_launch_ms": rl["launch_ms"],
+                      "k_evaluate_plans_per_s": ev, "k_evaluate_frac": ops * ev / ALU_PEAK_OPS,
+                      "ops_per_plan": ops, "best_this_run": r["makespan"]}
+        del plan
+        torch.cuda.empty_cache()
+    return legs
+
+
+def quality_leg(sat, torch, local, budget_s, runs):
+    """The quality target: a `budget_s` saturn_search per (workload, table
+    seed), seeded with the paper's baseline heuristics (row f2), wall time measured from the
+    call; best against the committed 5-minute CPU bar and lower bound."""
+    import numpy as np
+    import synth
+    refs = _json(os.path.join("profiles", "r2", "oracle_refs.json")) or {}
+    out = []
+    for name, s in runs:
+        inst = synth.by_name(name, s)
+        plan = sat.Plan(inst.node_gpus, local).load_runtime_table(inst.runtime)
+        sc, sq, base = [], [], {}
+        for kind in ("max", "min", "optimus", "random"):
+            gc, gq = plan.baseline_genome(kind, s)
+            sc.append(gc)
+            sq.append(gq)
+            base[kind] = int(plan.evaluate_host(gc[None], gq[None])[0])
+        cfg = sat.SearchConfig(seed=100 + s, population=1 << 20, max_generations=1 << 30, time_budget_s=budget_s,
+                               elites=16, generations_per_epoch=32)
+        t0 = time.perf_counter()
+        r = plan.search(cfg, seed_genomes=(np.stack(sc), np.stack(sq)))
+        wall = time.perf_counter() - t0
+        t, h = plan.search_history()
+        anytime = {}
+        for target in (0.01, 0.1, 1.0, 5.0, budget_s):
+            k = int(np.searchsorted(t, target, side="right")) - 1
+            if k >= 0:
+                anytime[f"{target:g}s"] = int(h[k])
+        b = _bar(name, s)
+        lb = refs.get("lower_bound", {}).get(name, {}).get(str(s))
+        out.append({"workload": name, "table_seed": s, "best": r["makespan"], "wall_s": wall,
+                    "plans_evaluated": r["evaluated"], "generations": r["generations"], "anytime": anytime,
+                    "cpu_5min_bar": b["bar"], "bar_file": b.get("bar_file"),
+                    "beats_bar": (b["bar"] is not None and r["makespan"] <= b["bar"]),
+                    "lower_bound": lb, "best_over_lb": (r["makespan"] / lb) if lb else None,
+                    "best_lower_bound": b.get("bar_best_lower_bound"), "baselines": base})
+        del plan
+    return out
 
 
 def main():
@@ -212,6 +400,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-per-core", type=int, default=100000)
     ap.add_argument("--kernel-only-n", type=int, default=1 << 24)
+    ap.add_argument("--no-workloads", action="store_true", help="skip the other BASELINE configs' legs")
+    ap.add_argument("--quality-budget", type=float, default=10.0,
+                    help="seconds per quality search (0 skips the quality leg)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -221,7 +412,6 @@ def main():
         run_reference(args, rank, world)
         return
 
-    import numpy as np
     import torch
     import synth
     import paper_2309_01226_b200 as sat
@@ -270,85 +460,31 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up
-    for _ in range(max(args.warmup, 0)):
-        plan.search(scfg, stream=stream)
-    barrier()
-
     # ---- timed region: K steps, device time via CUDA events on the launching stream
-    plan.reset_stats()
-    plan.set_profiling(4)          # k_ga launches 2, 6, 10, 14 of each step carry CUDA events
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    evaluated = 0
     with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            r = plan.search(scfg, stream=stream)
-            evaluated += r["evaluated"]
-        ev1.record(stream)
-        barrier()
-    st = plan.stats()
-    plan.set_profiling(False)
-    dev_ms = max_over_ranks(ev0.elapsed_time(ev1))
+        m, st, r = measure_search(sat, torch, plan, inst, scfg, args.steps, args.warmup, stream, G, barrier,
+                                  max_over_ranks)
+    dev_ms = m["ms_per_step"] * args.steps
+    value = m["value"]                       # `evaluated` already sums all ranks
     best_ms = r["makespan"]
-    value = evaluated / (dev_ms * 1e-3)          # `evaluated` already sums all ranks
 
     # ---- e2e: host API with host buffers (table upload + search + best plan to host)
-    plan.reset_stats()
     barrier()
     with ClockSampler(local):          # same conditions as the device-timed region
-        t0 = time.perf_counter()
-        ev_e2e = 0
-        for _ in range(args.steps):
-            plan.load_runtime_table(inst.runtime)
-            r2 = plan.search(scfg, stream=stream)
-            ms_host, placements, _, _ = plan.best_plan()
-            ev_e2e += r2["evaluated"]
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0)
-    st_e2e = plan.stats()
-    e2e = {"value": ev_e2e / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": st_e2e["h2d_bytes"] // args.steps,
-           "d2h_bytes_per_step": st_e2e["d2h_bytes"] // args.steps}
+        e2e = measure_e2e(plan, inst, scfg, args.steps, stream, torch, max_over_ranks)
 
     # ---- roofline of the dominant kernel (the fused GA generation + decode kernel)
-    ops = algorithmic_ops_per_plan(T, inst.node_gpus)
-    launch_s = st["ga_kernel_ms"] * 1e-3 / max(st["ga_launches"], 1)
-    units = st["ga_decodes"] / max(st["ga_launches"], 1)
-    achieved = ops * units / launch_s
-    traffic = _traffic(args.workload)
-    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": ALU_PEAK_OPS / 1e12, "unit": "TOP/s",
-                "frac": achieved / ALU_PEAK_OPS, "traffic": traffic,
-                "kernel": "k_ga (Philox GA operators fused with the sorted-multiset decode)",
-                "ops_per_plan": ops, "plans_per_launch": units, "launch_ms": launch_s * 1e3,
-                "launches_timed": st["ga_launches"],
-                # k_ga launches in the timed region (G per step) x their mean duration / device time
-                "kernel_share_of_step": (launch_s * 1e3 * G * args.steps / dev_ms)
-                if dev_ms > 0 else None}
+    roofline = ga_roofline(st, T, inst.node_gpus, G, args.steps, dev_ms)
+    roofline["traffic"] = _traffic(args.workload)
 
     # ---- kernel-only evaluate throughput (K1 alone, genomes resident in HBM)
     kernel_only = None
     if rank == 0 and args.kernel_only_n > 0:
-        S = plan.num_configs()
         n = args.kernel_only_n
-        cfg_h, perm_h = synth.random_genomes(S, n, seed=5)
-        cfg_d, perm_d = torch.from_numpy(cfg_h).cuda(), torch.from_numpy(perm_h).cuda()
-        out = torch.empty(n, dtype=torch.int32, device="cuda")
-        kernel_only = {}
-        for name, kind in (("thread", sat.DECODER_THREAD), ("warp", sat.DECODER_WARP)):
-            plan.set_decoder(kind)
-            for _ in range(3):
-                plan.evaluate(cfg_d, perm_d, out)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 5
-            a.record()
-            for _ in range(reps):
-                plan.evaluate(cfg_d, perm_d, out)
-            b.record()
-            torch.cuda.synchronize()
-            kernel_only[name] = n * reps / (a.elapsed_time(b) * 1e-3)
-        plan.set_decoder(sat.DECODER_AUTO)
+        kernel_only = {"unit": UNIT, "genomes": n,
+                       "thread": evaluate_rate(sat, torch, plan, n, kind=sat.DECODER_THREAD),
+                       "warp": evaluate_rate(sat, torch, plan, n, kind=sat.DECODER_WARP)}
+        ops = algorithmic_ops_per_plan(T, inst.node_gpus)
         # exhaustive enumeration (row a4-ii): a 7-job TINY-shaped instance, 6^7 * 7! genomes
         tv = synth.tiny_variant(7, 7, (4,))
         ep = sat.Plan(tv.node_gpus, local).load_runtime_table(tv.runtime)
@@ -365,8 +501,6 @@ def main():
             "dfs_seconds": t_dfs, "dfs_leaves": er["leaves"], "dfs_leaves_per_s": er["leaves"] / t_dfs,
             "dfs_genomes_covered_per_s": er["evaluated"] / t_dfs,
             "same_result": (er["makespan"], er["genome_index"]) == (fr["makespan"], fr["genome_index"])}
-        kernel_only["unit"] = UNIT
-        kernel_only["genomes"] = n
         # the decode kernel alone against the same ALU roofline (algorithmic ops per plan)
         kernel_only["roofline_thread"] = {"bound": "alu", "achieved": ops * kernel_only["thread"] / 1e12,
                                           "peak": ALU_PEAK_OPS / 1e12, "unit": "TOP/s",
@@ -378,39 +512,54 @@ def main():
         if dist is not None:
             dist.destroy_process_group()
         return
-    import oracle
-    c = oracle.compact(inst.node_gpus, inst.runtime)
-    lb = oracle.lower_bound(c)
+    refs = _json(os.path.join("profiles", "r2", "oracle_refs.json")) or {}
     # "best makespan vs oracle": on TINY the GPU enumeration and a short GPU search against
-    # the oracle's brute-force optimum; on the bench workload the best found against the
-    # area lower bound and the committed 5-minute CPU bar (tools/quality_bar.py).
+    # the oracle's brute-force optimum (profiles/r2/oracle_refs.json, written by
+    # tools/oracle_refs.py from oracle/ only); on the bench workload the best found against
+    # the lower bound and the committed 5-minute CPU bar.
     tiny = synth.tiny(0)
     tplan = sat.Plan(tiny.node_gpus, local).load_runtime_table(tiny.runtime)
-    ct = oracle.compact(tiny.node_gpus, tiny.runtime)
     t_enum = tplan.enumerate()
     t_srch = tplan.search(sat.SearchConfig(seed=1, population=1024, max_generations=20, elites=8))
-    bar = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1", "quality_bar.json" if args.workload == "TXT"
-                               else f"quality_bar_{args.workload}.json")) as f:
-            bar = json.load(f)["seeds"]["0"]["bar"]
-    except Exception:
-        pass
-    vs_oracle = {"TINY": {"oracle_brute_force": oracle.brute_force(ct)[0], "gpu_enumerate": t_enum["makespan"],
-                          "gpu_search": t_srch["makespan"]},
-                 args.workload: {"gpu_best_this_run": best_ms, "lower_bound": lb,
-                                 "cpu_5min_bar_seed0": bar}}
+    opt = refs.get("tiny_brute_force", {}).get("0", {})
+    vs_oracle = {"TINY": {"oracle_brute_force": opt.get("makespan"), "oracle_genome_index": opt.get("genome_index"),
+                          "gpu_enumerate": t_enum["makespan"], "gpu_enumerate_index": t_enum["genome_index"],
+                          "gpu_search": t_srch["makespan"],
+                          "bit_exact": (t_enum["makespan"], t_enum["genome_index"]) ==
+                                       (opt.get("makespan"), opt.get("genome_index"))},
+                 args.workload: {"gpu_best_this_run": best_ms,
+                                 "lower_bound": refs.get("lower_bound", {}).get(args.workload, {}).get("0"),
+                                 "cpu_5min_bar_seed0": _bar(args.workload, 0)["bar"]}}
+    del tplan
+    legs = None
+    quality = None
+    if world == 1:
+        if not args.no_workloads:
+            del plan
+            torch.cuda.empty_cache()
+            legs = workload_legs(sat, torch, args, local, stream, [w for w in ("TINY", "TXT", "IMG", "MIX", "SWEEP")
+                                                                   if w != args.workload])
+            legs[args.workload] = {"workload": WORKLOADS[args.workload], "value": value, "unit": UNIT,
+                                   "ms_per_step": dev_ms / args.steps, "steps": args.steps, "e2e": e2e["value"],
+                                   "k_ga_frac": roofline["frac"], "k_ga_launch_ms": roofline["launch_ms"],
+                                   "k_evaluate_plans_per_s": kernel_only["thread"] if kernel_only else None,
+                                   "k_evaluate_frac": kernel_only["roofline_thread"]["frac"] if kernel_only else None,
+                                   "ops_per_plan": roofline["ops_per_plan"], "best_this_run": best_ms}
+        if args.quality_budget > 0:
+            quality = quality_leg(sat, torch, local, args.quality_budget,
+                                  [("TXT", 0), ("TXT", 1), ("TXT", 2), ("MIX", 0), ("SWEEP", 0)])
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.workload, args.cpu_seconds)
+        cpu["cpu"] = host_cpu()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (seeded runtime tables shaped like the paper's workloads; random-init GA)",
-            "config": _config(args, {"best_makespan_s": best_ms, "lower_bound_s": lb,
-                                     "best_over_lb": best_ms / lb}),
+            "config": _config(args),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": st["kernel_launches"],
-            "clocks": clk.summary(), "kernel_only": kernel_only, "best_vs_oracle": vs_oracle}
+            "clocks": clk.summary(), "kernel_only": kernel_only, "best_vs_oracle": vs_oracle,
+            "workloads": legs, "quality": quality, "host_cpu": host_cpu()}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -1,6 +1,12 @@
 # scratch GPU call used during round 2 (edited per call)
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
-for w in TXT MIX SWEEP; do
-  s="0 1 2"; [ $w != TXT ] && s=0
-  timeout 300 python tools/quality_gpu.py --workload $w --seeds $s --bar profiles/r1/quality_bar$([ $w != TXT ] && echo _$w).json --out gpurun_out/quality_v5_$w.json | cut -c1-200
-done
+start=$(date +%s); python bench.py > gpurun_out/bench_r2a.json 2> gpurun_out/bench_r2a.err; echo "bench wall $(( $(date +%s) - start )) s"; tail -3 gpurun_out/bench_r2a.err
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench_r2a.json').read().strip().splitlines()[-1])
+print({k: d[k] for k in ('value','ms_per_step','clocks','gpu_launches')})
+print('roofline', {k: d['roofline'][k] for k in ('frac','launch_ms','kernel_share_of_step')})
+print('e2e', d['e2e'])
+for k,v in (d['workloads'] or {}).items(): print(k, {kk: (round(vv,4) if isinstance(vv,float) else vv) for kk,vv in v.items() if kk!='workload'})
+for q in d['quality'] or []: print({k:q[k] for k in ('workload','table_seed','best','cpu_5min_bar','beats_bar','lower_bound','wall_s')})
+print(d['best_vs_oracle']); print(d['cpu_baseline']); print(d['host_cpu'])
+PY

@@ -32,7 +32,12 @@ def main():
     ap.add_argument("--ls", type=int, nargs="+", default=[0], help="memetic local-search iterations per epoch")
     ap.add_argument("--bar", default=None, help="quality_bar.json to compare against")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--lib", default=None, help="alternative libsaturn.so (A/B)")
+    ap.add_argument("--ga-seeds", type=int, nargs="+", default=None,
+                    help="GA seeds per table seed (default: 100 + table seed)")
     args = ap.parse_args()
+    if args.lib:
+        sat.load_library(args.lib)
     bar = json.load(open(args.bar)) if args.bar and os.path.exists(args.bar) else None
     import torch
     res = {"workload": args.workload, "budget_s": args.budget, "gpu": torch.cuda.get_device_name(0), "runs": []}
@@ -46,8 +51,9 @@ def main():
             seeds_c.append(gc)
             seeds_p.append(gq)
             base[kind] = int(plan.evaluate_host(gc[None], gq[None])[0])
-        for P, ls in [(P, ls) for P in args.populations for ls in args.ls]:
-            cfg = sat.SearchConfig(seed=100 + s, population=P, max_generations=1 << 30, time_budget_s=args.budget,
+        for P, ls, gs in [(P, ls, gs) for P in args.populations for ls in args.ls
+                          for gs in (args.ga_seeds or [100 + s])]:
+            cfg = sat.SearchConfig(seed=gs, population=P, max_generations=1 << 30, time_budget_s=args.budget,
                                    elites=args.elites, generations_per_epoch=args.epoch, local_search_iters=ls)
             r = plan.search(cfg, seed_genomes=(np.stack(seeds_c), np.stack(seeds_p)))
             best, pl, bc, bp = plan.best_plan()
@@ -59,7 +65,7 @@ def main():
                 k = np.searchsorted(t, target, side="right") - 1
                 if k >= 0:
                     marks[f"{target:g}s"] = int(h[k])
-            run = {"seed": s, "population": P, "local_search_iters": ls, "best": best, "lower_bound": oracle.lower_bound(c),
+            run = {"seed": s, "ga_seed": gs, "population": P, "local_search_iters": ls, "best": best, "lower_bound": oracle.lower_bound(c),
                    "seconds": r["seconds"], "evaluated": r["evaluated"], "generations": r["generations"],
                    "plans_per_s": r["evaluated"] / r["seconds"], "anytime": marks, "baselines": base}
             if bar:
