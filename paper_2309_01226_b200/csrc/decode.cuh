@@ -207,20 +207,31 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
     const uint32_t w = fetch(0);
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
-    int bn = NN;
+    if (NN == 1 && pb.full_nodes) {   // one node of exactly GP GPUs: R in the top g slots
 #pragma unroll
-    for (int n = NN - 1; n >= 0; --n) bn = (n < pb.N && g <= pb.gpu_n[n]) ? n : bn;
+      for (int i = 0; i < GP; ++i) a[0][i] = (i >= GP - g) ? R : 0;
+    } else {
+      int bn = NN;
 #pragma unroll
-    for (int n = 0; n < NN; ++n) {
-      const int gn = n < pb.N ? pb.gpu_n[n] : 0;
+      for (int n = NN - 1; n >= 0; --n) bn = (n < pb.N && g <= pb.gpu_n[n]) ? n : bn;
 #pragma unroll
-      for (int i = 0; i < GP; ++i) a[n][i] = (i < gn) ? ((n == bn && i >= gn - g) ? R : 0) : INF;
+      for (int n = 0; n < NN; ++n) {
+        const int gn = n < pb.N ? pb.gpu_n[n] : 0;
+#pragma unroll
+        for (int i = 0; i < GP; ++i) a[n][i] = (i < gn) ? ((n == bn && i >= gn - g) ? R : 0) : INF;
+      }
     }
     ms = R;
   }
-  // Positions 1 .. T-2: the full update.
+  // Positions 1 .. T-2: the full update.  The next position's config word is fetched one
+  // step ahead (its three dependent shared-memory loads -- perm byte, cfg byte, table word
+  // -- overlap this step's arithmetic instead of stalling the next one).
+  // (Not for 4-node states: their 128 registers leave no room -- measured SWEEP k_ga +1.6 %.)
+  constexpr bool AHEAD = NN <= 2;
+  uint32_t w = (AHEAD && T > 1) ? fetch(1) : 0u;
   for (int p = 1; p < T - 1; ++p) {
-    const uint32_t w = fetch(p);
+    if (!AHEAD) w = fetch(p);
+    const uint32_t wn = AHEAD ? fetch(p + 1) : 0u;
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
     int v;
@@ -252,15 +263,17 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
         for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
     }
     if constexpr (TRACK_MS) ms = max(ms, v);
+    if (AHEAD) w = wn;
   }
+  if (!AHEAD && T > 1) w = fetch(T - 1);
   if constexpr (!TRACK_MS) {
     ms = 0;
 #pragma unroll
     for (int n = 0; n < NN; ++n) ms = max(ms, a[n][GP - 1]);
   }
-  // Position T-1: only its end matters (no later job reads the state): earliest start + R.
+  // Position T-1 (its word is in w): only its end matters (no later job reads the state):
+  // earliest start + R.
   if (T > 1) {
-    const uint32_t w = fetch(T - 1);
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
     int best = mux<GP>(a[0], g - 1);

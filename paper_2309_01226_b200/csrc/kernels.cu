@@ -774,10 +774,11 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
 template <int NN, int GP>
 struct GaMinBlocks {
   static constexpr int STATE = (NN == 0 ? 1 : NN) * GP;
-  // measured r1 (dynamic chunks): 7 CTAs/SM for one 8-GPU node and for 16-slot states,
-  // 4 for 32-slot states (SWEEP's shared memory caps it at 3-5 anyway), 8 for small states
+  // measured r1 (dynamic chunks): 7 CTAs/SM (72 registers) for one 8-GPU node and for
+  // 16-slot states, 4 for 32-slot states (SWEEP's shared memory caps it at 3-5 anyway);
+  // small states too since GA v5 (8 CTAs = 64 registers spill)
   static constexpr int value = NN == 0 ? (GP <= 8 ? 6 : (GP <= 16 ? 4 : 2))
-                                       : (STATE < 8 ? 8 : STATE <= 16 ? 7 : (STATE <= 32 ? 4 : 2));
+                                       : (STATE <= 16 ? 7 : (STATE <= 32 ? 4 : 2));
 };
 
 // Dynamic work distribution: a warp's first chunk of 32 units comes from the static grid
