@@ -83,8 +83,10 @@ typedef struct {
                              branch-and-bound cut; these are not full decodes)          */
 } saturn_result;
 
-/* Genetic search parameters (row a7).  Probabilities are q32
- * thresholds: an event fires iff a Philox u32 < threshold. */
+/* Genetic search parameters (row a7, oracle/ga.py GA v5).
+ * Probabilities are given as q32 thresholds (floor(p * 2^32)); every gate compares a 16-bit
+ * Philox field h with threshold >> 16 and fires iff h < threshold >> 16, so the resolution is
+ * 2^-16 and p = 1.0 (0xFFFFFFFF) fires with probability 65535/65536. */
 typedef struct {
   uint64_t seed;
   int64_t population;            /* genomes per GPU, >= 64 and >= 2 * elites            */
@@ -92,9 +94,11 @@ typedef struct {
   double time_budget_s;          /* stop at the first epoch boundary past this; 0 = none */
   int32_t elites;                /* 1..32 genomes carried unchanged to the next generation */
   int32_t generations_per_epoch; /* island migration period (multi-GPU), >= 1           */
-  uint32_t p_xover_q32;          /* crossover probability                               */
-  uint32_t p_cfg_mut_q32;        /* per-job config mutation probability                  */
-  uint32_t p_perm_mut_q32;       /* per-child permutation mutation probability           */
+  uint32_t p_xover_q32;          /* per-pair crossover probability (both children)       */
+  uint32_t p_cfg_mut_q32;        /* per-child probability that ONE job (drawn uniformly) gets
+                                    a new config drawn uniformly from its S_t             */
+  uint32_t p_perm_mut_q32;       /* per-child permutation mutation probability (swap or
+                                    insertion, 50/50)                                    */
   const uint8_t *seed_cfg;       /* host [n_seed][T] genomes placed first, or NULL        */
   const uint8_t *seed_perm;      /* host [n_seed][T]                                      */
   int64_t n_seed;
@@ -106,10 +110,30 @@ typedef struct {
 /* Create a handle for a cluster of n_nodes nodes with node_gpus[n] GPUs each (Table 1: N,
  * GPU_n) on CUDA device `cuda_device`.  cuda_device = -1 creates a
  * HOST-ONLY handle: table loading/compaction, baselines and the other host calls work, every
- * device call returns ESTATE.  EINVAL: n_nodes < 1, any GPU_n < 1, sum GPU_n > 32.
- * ECUDA: device not usable. */
+ * device call returns ESTATE.  EINVAL: n_nodes < 1, n_nodes > 32, any GPU_n < 1,
+ * sum GPU_n > 32 (reading A15: the trace decoder gives every GPU of the cluster one
+ * lane of a warp; SURVEY.md §8b's u64 masks would allow 64).  ECUDA: device not usable. */
 saturn_status saturn_plan_create(const int32_t *node_gpus, int32_t n_nodes, int32_t cuda_device,
                                  saturn_plan **out);
+
+/* Device workspace (north star: "PyTorch used only for device memory").
+ * saturn_workspace_bytes: bytes a freshly bound workspace needs for one saturn_search with
+ * `sp` (NULL: evaluate / enumerate / best_plan only) on the loaded table, including the table
+ * itself, the two populations (2 x population x record bytes), their makespans, the candidate
+ * list, the elite records and the trace scratch.  Host-buffer calls (saturn_evaluate_host,
+ * saturn_improve) need min(n, 2^24) x (2T + 4) bytes more.  ESTATE before a table is loaded or
+ * on a host-only handle; EINVAL for out-of-range population / elites.
+ * saturn_bind_workspace: bind a caller-owned device buffer (e.g. a torch.empty(bytes,
+ * dtype=torch.uint8) tensor on the handle's device, 256-byte aligned) -- from then on every
+ * device buffer the handle needs is carved from it instead of cudaMalloc (the peer-link
+ * exchange buffers excepted: CUDA IPC needs their own allocations).  The caller keeps it
+ * alive until it unbinds (d_workspace = NULL) or destroys the handle.  Binding synchronises
+ * the device, drops the handle's previous buffers (the last search population becomes
+ * unavailable) and moves a loaded table into the workspace.  A call that runs out of the bound
+ * workspace returns ELIMIT naming the allocation.  EINVAL: not device memory of the
+ * handle's device, or misaligned. */
+saturn_status saturn_workspace_bytes(const saturn_plan *p, const saturn_search_params *sp, uint64_t *bytes);
+saturn_status saturn_bind_workspace(saturn_plan *p, void *d_workspace, uint64_t bytes);
 
 /* Load the profiled runtime table (row a1; Table 1 G_t, R_t; the Trial Runner grid over
  * "all supported parallelisms and GPU apportionment levels").
@@ -231,9 +255,12 @@ saturn_status saturn_improve(saturn_plan *p, uint8_t *h_cfg, uint8_t *h_perm, in
                              int32_t *h_makespan, void *stream);
 
 /* Final population of the last search on this device: host uint8 cfg [P][T], perm [P][T],
- * int32 makespan [P].  (Used for operator-replay parity.)  ESTATE before a search. */
-saturn_status saturn_search_population(const saturn_plan *p, uint8_t *h_cfg, uint8_t *h_perm,
-                                       int32_t *h_makespan);
+ * int32 makespan [P] (each may be NULL), P = that search's population, returned in *n_out.
+ * With every buffer NULL it only reports P.  (Used for operator-replay parity.)
+ * EINVAL: capacity < P (the buffers are never written past `capacity` genomes);
+ * ESTATE before a search (or after a workspace bind dropped the population). */
+saturn_status saturn_search_population(const saturn_plan *p, int64_t capacity, uint8_t *h_cfg, uint8_t *h_perm,
+                                       int32_t *h_makespan, int64_t *n_out);
 
 /* The best plan of the last enumerate/search (row a8): placements host [T] (job-id order),
  * genome_out host [2T] (cfg then perm) or NULL, makespan.  ESTATE before any search. */
@@ -244,7 +271,9 @@ saturn_status saturn_best_plan(saturn_plan *p, saturn_placement *out, uint8_t *g
  * the surplus dealt round-robin, OPTIMUS = Optimus*-Greedy (Alg. 1, per node), RANDOM = a
  * uniform random genome.  Configs: best runtime at the chosen width (ties to the lower UPP
  * index); order: LPT.  Multi-node job groups are drawn with probability GPU_n / sum GPU
- * (PAPER.md:1002).  Exact rules: DESIGN.md "Baselines" / oracle/baselines.py.
+ * (PAPER.md:1002).  Exact rules: DESIGN.md "Baselines" / oracle/baselines.py.  On multi-node
+ * clusters the per-node job groups fix each job's WIDTH only; the genome carries no node, so
+ * the decoder re-picks the node greedily (reading A16).
  * cfg, perm: host uint8 [T].  Host-only (works on host-only handles).  ESTATE without a table. */
 enum { SATURN_BASELINE_MAX = 1, SATURN_BASELINE_MIN = 2, SATURN_BASELINE_OPTIMUS = 3, SATURN_BASELINE_RANDOM = 4 };
 saturn_status saturn_baseline_genome(const saturn_plan *p, int32_t kind, uint64_t seed, uint8_t *cfg, uint8_t *perm);
@@ -289,9 +318,13 @@ saturn_status saturn_plan_attach_comm(saturn_plan *p, const uint8_t *id128, int3
  * buffer (device-to-device over NVLink, or within one device), passes a shared-memory
  * barrier and merges its own buffer -- the blocks an NCCL all-gather would produce, so the
  * island protocol and its results are those of saturn_plan_attach_comm / search_group.
- * saturn_enumerate reduces (MIN key, SUM leaves) the same way.  Collective and blocking;
- * a rank that does not arrive within SATURN_PEER_TIMEOUT_S (default 120 s) fails the others
- * with ECUDA instead of hanging.  Host-only handles attach the barrier alone (tests).
+ * saturn_enumerate reduces (MIN key, SUM leaves) the same way.  Collective and blocking.
+ * Liveness: every rank heartbeats in the shared segment while it waits for its own GPU work
+ * and at the barrier; a rank silent for SATURN_PEER_TIMEOUT_S (default 120 s: its process
+ * died or hangs outside the library) fails the others with ECUDA instead of hanging -- a
+ * rank that is only slow (long enumeration slice) keeps heartbeating and is waited for.
+ * A failed barrier poisons the link: every later exchange on it fails fast (ECUDA) on every
+ * rank until the handles re-attach.  Host-only handles attach the barrier alone (tests).
  * world <= 8.  ESTATE if the handle already has an NCCL communicator (and vice versa). */
 saturn_status saturn_plan_attach_peers(saturn_plan *p, const char *name, int32_t rank, int32_t world);
 /* Barrier over the ranks of the peer link (ESTATE without one). */

@@ -62,23 +62,49 @@ Nccl& nccl() {
   return n;
 }
 
+// Caller-provided device workspace (saturn_bind_workspace): a bump arena every DevBuf of the
+// handle carves from while it is bound, instead of cudaMalloc.  Nothing is freed inside it;
+// saturn_workspace_bytes sizes it for one search (+ best_plan) from a fresh bind.
+struct Arena {
+  uint8_t* base = nullptr;
+  size_t size = 0, off = 0;
+  bool bound() const { return base != nullptr; }
+};
+constexpr size_t ARENA_ALIGN = 256;
+inline size_t arena_round(size_t b) { return (b + ARENA_ALIGN - 1) & ~(ARENA_ALIGN - 1); }
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = false;   // cudaMalloc'ed by the handle (else carved from the arena)
+  Arena* arena = nullptr;
   cudaError_t ensure(size_t count) {
     if (count <= n && p) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
-    if (e == cudaSuccess) n = count;
+    release();
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (arena && arena->bound()) {
+      const size_t b = arena_round(bytes);
+      if (arena->off + b > arena->size) return cudaErrorMemoryAllocation;
+      p = reinterpret_cast<T*>(arena->base + arena->off);
+      arena->off += b;
+      n = count;
+      return cudaSuccess;
+    }
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) {
+      n = count;
+      owned = true;
+    } else {
+      p = nullptr;
+    }
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
+    owned = false;
   }
 };
 
@@ -103,6 +129,7 @@ struct saturn_plan {
   bool sorted_ok = false;
   int decoder = SATURN_DECODER_AUTO;
   uint32_t enum_options = 0;
+  Arena arena;                // bound caller workspace (saturn_bind_workspace), or none
   DevBuf<uint8_t> blob;
   int blob_bytes = 0;
   void* pinned = nullptr;     // pinned host staging for the table upload
@@ -152,6 +179,37 @@ struct saturn_plan {
 
 namespace {
 
+// Every device buffer the handle owns (table blob and workspaces; the peer-link exchange
+// buffers live in PeerLink: CUDA IPC needs their own allocations).
+template <class F>
+void for_each_buf(saturn_plan* p, F f) {
+  f(p->blob);
+  f(p->ws_cfg);
+  f(p->ws_perm);
+  f(p->ws_ms);
+  f(p->ws_key);
+  f(p->ws_place);
+  for (int b = 0; b < 2; ++b) {
+    f(p->pop[b]);
+    f(p->pms[b]);
+  }
+  f(p->cand);
+  f(p->n_cand);
+  f(p->flag);
+  f(p->ls_gen);
+  f(p->ls_ms);
+  f(p->rec_ms);
+  f(p->all_ms);
+  f(p->rec_gen);
+  f(p->all_gen);
+  f(p->seeds);
+  f(p->sink);
+}
+
+}  // namespace
+
+namespace {
+
 saturn_status fail(saturn_plan* p, saturn_status s, const char* fmt, ...) {
   if (p) {
     char buf[512];
@@ -167,6 +225,9 @@ saturn_status fail(saturn_plan* p, saturn_status s, const char* fmt, ...) {
 #define CU(p, call)                                                                                   \
   do {                                                                                                \
     cudaError_t e_ = (call);                                                                          \
+    if (e_ == cudaErrorMemoryAllocation && (p)->arena.bound())                                        \
+      return fail(p, SATURN_ELIMIT, "bound workspace exhausted (%zu of %zu B in use) at %s; size it "   \
+                  "with saturn_workspace_bytes", (p)->arena.off, (p)->arena.size, #call);             \
     if (e_ != cudaSuccess) return fail(p, SATURN_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));     \
   } while (0)
 
@@ -265,6 +326,7 @@ saturn_status saturn_plan_create(const int32_t* node_gpus, int32_t n_nodes, int3
   }
   saturn_plan* p = new saturn_plan();
   p->device = cuda_device;
+  for_each_buf(p, [p](auto& b) { b.arena = &p->arena; });
   p->gpu_n.assign(node_gpus, node_gpus + n_nodes);
   p->sumG = sum;
   p->maxG = mx;
@@ -275,6 +337,75 @@ saturn_status saturn_plan_create(const int32_t* node_gpus, int32_t n_nodes, int3
   }
   p->sms = prop.multiProcessorCount;
   *out = p;
+  return SATURN_OK;
+}
+
+// Device bytes one search with `sp` (NULL: evaluate / enumerate / best_plan only) needs from
+// a freshly bound workspace: the table blob, the trace and enumeration scratch, and -- for a
+// search -- two populations, their makespans, the candidate list, the elite records and the
+// seed genomes.  Every buffer is rounded up to ARENA_ALIGN bytes as the arena carves it.
+saturn_status saturn_workspace_bytes(const saturn_plan* pc, const saturn_search_params* sp, uint64_t* bytes) {
+  saturn_plan* p = const_cast<saturn_plan*>(pc);
+  if (!p || !bytes) return SATURN_EINVAL;
+  if (host_only(p)) return fail(p, SATURN_ESTATE, "host-only handle has no device workspace");
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "workspace_bytes before load_runtime_table");
+  const int T = p->T;
+  size_t b = arena_round(p->blob_bytes);
+  b += 2 * arena_round(T) + arena_round(4) + arena_round((size_t)T * sizeof(saturn_placement));   // trace
+  b += arena_round(3 * 8) + arena_round(4);                                                     // keys, flag
+  if (sp) {
+    const int64_t P = sp->population;
+    const int E = sp->elites;
+    if (P < 64 || P < 2 * E || P > (int64_t(1) << 31) - 1 || E < 1 || E > 32)
+      return fail(p, SATURN_EINVAL, "population=%lld / elites=%d out of range", (long long)P, E);
+    const int GS = gs_of(T);
+    const int world = std::max(p->world, 1);
+    DeviceGuard dg(p->device);
+    const size_t cand = (size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64;
+    b += 2 * arena_round((size_t)P * GS) + 2 * arena_round((size_t)P * 4) + arena_round(cand * 8) + arena_round(8);
+    b += arena_round((size_t)E * 4) + arena_round((size_t)E * GS) + arena_round((size_t)E * world * 4) +
+         arena_round((size_t)E * GS * world);
+    if (sp->n_seed > 0) b += arena_round((size_t)std::min<int64_t>(sp->n_seed, P) * GS);
+  }
+  *bytes = b;
+  return SATURN_OK;
+}
+
+// Bind (d_workspace != NULL) or unbind (NULL) a caller-owned device workspace.  Binding drops
+// every workspace buffer the handle holds (populations and search results become invalid:
+// search again) and re-homes the loaded table into the workspace.
+saturn_status saturn_bind_workspace(saturn_plan* p, void* d_workspace, uint64_t bytes) {
+  if (!p) return SATURN_EINVAL;
+  if (host_only(p)) return fail(p, SATURN_ESTATE, "host-only handle has no device workspace");
+  DeviceGuard dg(p->device);
+  if (d_workspace) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, d_workspace) != cudaSuccess || a.type != cudaMemoryTypeDevice ||
+        a.device != p->device) {
+      cudaGetLastError();
+      return fail(p, SATURN_EINVAL, "workspace is not device memory of device %d", p->device);
+    }
+    if (reinterpret_cast<uintptr_t>(d_workspace) % ARENA_ALIGN)
+      return fail(p, SATURN_EINVAL, "workspace must be %zu-byte aligned", ARENA_ALIGN);
+  }
+  CU(p, cudaDeviceSynchronize());   // nothing in flight may still use the old buffers
+  std::vector<uint8_t> blob;
+  if (p->loaded && p->blob.p) {
+    blob.resize(p->blob_bytes);
+    CU(p, cudaMemcpy(blob.data(), p->blob.p, p->blob_bytes, cudaMemcpyDeviceToHost));
+  }
+  for_each_buf(p, [](auto& b) { b.release(); });
+  p->arena = Arena{};
+  if (d_workspace) {
+    p->arena.base = static_cast<uint8_t*>(d_workspace);
+    p->arena.size = bytes;
+  }
+  p->have_pop = false;
+  if (!blob.empty()) {
+    CU(p, p->blob.ensure(blob.size()));
+    CU(p, cudaMemcpy(p->blob.p, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    p->pb.blob = p->blob.p;
+  }
   return SATURN_OK;
 }
 
@@ -565,7 +696,7 @@ saturn_status peer_reduce_keys(saturn_plan* p, unsigned long long* key, cudaStre
   sat::PeerLink& L = *p->peers;
   for (int q = 0; q < L.world; ++q)
     CU(p, cudaMemcpyAsync(L.peer[q] + sat::PeerLayout::keys + 16 * L.rank, key, 16, cudaMemcpyDeviceToDevice, st));
-  CU(p, cudaStreamSynchronize(st));
+  CU(p, L.wait_stream(st));
   if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
   unsigned long long all[2 * sat::PEER_MAX];
   CU(p, cudaMemcpy(all, L.local + sat::PeerLayout::keys, 16 * L.world, cudaMemcpyDeviceToHost));
@@ -604,14 +735,14 @@ saturn_status peer_shared_begin(saturn_plan* p, const unsigned long long init[2]
   sat::PeerLink& L = *p->peers;
   if (L.rank == 0) {
     CU(p, cudaMemcpyAsync(peer_shared_slot(p), init, 16, cudaMemcpyHostToDevice, st));
-    CU(p, cudaStreamSynchronize(st));
+    CU(p, L.wait_stream(st));
   }
   if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
   return SATURN_OK;
 }
 saturn_status peer_shared_end(saturn_plan* p, cudaStream_t st, unsigned long long out[2]) {
   sat::PeerLink& L = *p->peers;
-  CU(p, cudaStreamSynchronize(st));
+  CU(p, L.wait_stream(st));
   if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
   CU(p, cudaMemcpy(out, peer_shared_slot(p), 16, cudaMemcpyDeviceToHost));
   if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
@@ -1088,7 +1219,7 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
         CU(p, cudaMemcpyAsync(L.peer[q] + gen_off + (size_t)E * GS * L.rank, p->rec_gen.p, (size_t)E * GS,
                               cudaMemcpyDeviceToDevice, st));
       }
-      CU(p, cudaStreamSynchronize(st));
+      CU(p, L.wait_stream(st));
       if (!L.barrier()) return fail(p, SATURN_ECUDA, "%s", L.err.c_str());
       CU(p, sat::launch_merge_elites(reinterpret_cast<const int32_t*>(L.local + ms_off), L.local + gen_off, L.world,
                                      E, GS, p->rec_ms.p, p->rec_gen.p, st));
@@ -1283,22 +1414,27 @@ saturn_status saturn_search_history(const saturn_plan* p, int64_t n_max, double*
   return SATURN_OK;
 }
 
-saturn_status saturn_search_population(const saturn_plan* p, uint8_t* h_cfg, uint8_t* h_perm, int32_t* h_makespan) {
+saturn_status saturn_search_population(const saturn_plan* pc, int64_t capacity, uint8_t* h_cfg, uint8_t* h_perm,
+                                       int32_t* h_makespan, int64_t* n_out) {
+  saturn_plan* p = const_cast<saturn_plan*>(pc);
   if (!p) return SATURN_EINVAL;
-  if (!p->have_pop) return SATURN_ESTATE;
-  DeviceGuard dg(p->device);
+  if (!p->have_pop) return fail(p, SATURN_ESTATE, "no search population on this handle");
   const int64_t P = p->pop_P;
+  if (n_out) *n_out = P;
+  if (!h_cfg && !h_perm && !h_makespan) return SATURN_OK;
+  if (capacity < P)
+    return fail(p, SATURN_EINVAL, "capacity %lld < population %lld", (long long)capacity, (long long)P);
+  DeviceGuard dg(p->device);
   const int GS = p->pop_GS, T = p->T;
-  std::vector<uint8_t> buf((size_t)P * GS);
-  if (cudaMemcpy(buf.data(), p->pop[p->last_pop].p, buf.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
-    return SATURN_ECUDA;
-  if (h_makespan && cudaMemcpy(h_makespan, p->pms[p->last_pop].p, P * sizeof(int32_t), cudaMemcpyDeviceToHost) !=
-                        cudaSuccess)
-    return SATURN_ECUDA;
-  for (int64_t i = 0; i < P; ++i) {
-    if (h_cfg) memcpy(h_cfg + i * T, &buf[i * GS], T);
-    if (h_perm) memcpy(h_perm + i * T, &buf[i * GS + sat::perm_offset(T)], T);
+  if (h_cfg || h_perm) {
+    std::vector<uint8_t> buf((size_t)P * GS);
+    CU(p, cudaMemcpy(buf.data(), p->pop[p->last_pop].p, buf.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < P; ++i) {
+      if (h_cfg) memcpy(h_cfg + i * T, &buf[i * GS], T);
+      if (h_perm) memcpy(h_perm + i * T, &buf[i * GS + sat::perm_offset(T)], T);
+    }
   }
+  if (h_makespan) CU(p, cudaMemcpy(h_makespan, p->pms[p->last_pop].p, P * sizeof(int32_t), cudaMemcpyDeviceToHost));
   return SATURN_OK;
 }
 
@@ -1703,28 +1839,8 @@ void saturn_plan_destroy(saturn_plan* p) {
     DeviceGuard dg(p->device);
     if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
     p->peers.reset();
-    p->blob.release();
     if (p->pinned) cudaFreeHost(p->pinned);
-    p->ws_cfg.release();
-    p->ws_perm.release();
-    p->ws_ms.release();
-    p->ws_key.release();
-    p->ws_place.release();
-    for (int b = 0; b < 2; ++b) {
-      p->pop[b].release();
-      p->pms[b].release();
-    }
-    p->cand.release();
-    p->n_cand.release();
-    p->flag.release();
-    p->ls_gen.release();
-    p->ls_ms.release();
-    p->rec_ms.release();
-    p->all_ms.release();
-    p->rec_gen.release();
-    p->all_gen.release();
-    p->seeds.release();
-    p->sink.release();
+    for_each_buf(p, [](auto& b) { b.release(); });
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : p->hist_ev) cudaEventDestroy(e);
     if (p->hist_pin) cudaFreeHost(p->hist_pin);

@@ -704,6 +704,11 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
       tc = LV(level, NN * GP + 6);
       cc = LV(level, NN * GP + 7);
     }
+    // Share an improved incumbent as soon as this root's subtree is done, so other threads
+    // (and, over peer memory, other ranks) prune against it from their next root on.  Only
+    // improvements are published: a real leaf's (makespan, index) key, so the final
+    // atomicMin result is unchanged.
+    if ((int)(best >> 38) < inc) atomicMin(best_key, (unsigned long long)best);
   }
   best = warp_min_u64(best);
   const int lane = tid & 31, warp = tid >> 5;

@@ -32,36 +32,82 @@ void pause_briefly(int spins) {
 }
 }  // namespace
 
+static uint64_t mono_ms() {   // CLOCK_MONOTONIC: one clock for every process of the host
+  timespec ts{};
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (uint64_t)ts.tv_sec * 1000u + (uint64_t)(ts.tv_nsec / 1000000);
+}
+
 struct PeerLink::Shm {
   std::atomic<uint32_t> magic;
   int32_t world;
   std::atomic<uint32_t> count;       // arrivals at the current barrier
   std::atomic<uint32_t> generation;  // bumped by the last arrival
+  std::atomic<uint32_t> broken;      // set by a rank whose barrier failed: the link is poisoned
+  std::atomic<uint64_t> beat[PEER_MAX];   // last heartbeat of every rank (mono_ms)
   std::atomic<uint32_t> published[PEER_MAX];
   int32_t device[PEER_MAX];
   int32_t has_buffer[PEER_MAX];
   cudaIpcMemHandle_t handle[PEER_MAX];
 };
 
+void PeerLink::heartbeat() {
+  if (shm_) shm_->beat[rank].store(mono_ms(), std::memory_order_relaxed);
+}
+
+bool PeerLink::broken() const {
+  return broken_ || (shm_ && shm_->broken.load(std::memory_order_acquire) != 0);
+}
+
+cudaError_t PeerLink::wait_stream(cudaStream_t st) {
+  for (int spins = 0;; ++spins) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e != cudaErrorNotReady) return e;
+    if ((spins & 63) == 0) heartbeat();
+    timespec ts{0, 50000};  // 50 us
+    nanosleep(&ts, nullptr);
+  }
+}
+
 bool PeerLink::barrier() {
   if (!shm_) {
     err = "peer link not attached";
     return false;
   }
+  if (broken()) {
+    broken_ = true;
+    err = "peer link broken by an earlier failed barrier (re-attach to continue)";
+    return false;
+  }
+  heartbeat();
   const uint32_t g = shm_->generation.load(std::memory_order_acquire);
   if (shm_->count.fetch_add(1, std::memory_order_acq_rel) + 1 == (uint32_t)world) {
     shm_->count.store(0, std::memory_order_relaxed);
     shm_->generation.fetch_add(1, std::memory_order_release);
     return true;
   }
-  const double t0 = now_s();
+  const uint64_t limit = (uint64_t)(timeout_s * 1000.0);
   for (int spins = 0; shm_->generation.load(std::memory_order_acquire) == g; ++spins) {
-    if ((spins & 255) == 0 && now_s() - t0 > timeout_s) {
-      char b[160];
-      snprintf(b, sizeof b, "peer barrier: rank %d waited %.0f s for %d ranks (a peer died or diverged)", rank,
-               timeout_s, world);
-      err = b;
-      return false;
+    if ((spins & 255) == 0) {
+      heartbeat();
+      if (shm_->broken.load(std::memory_order_acquire)) {
+        broken_ = true;
+        err = "peer barrier: another rank's barrier failed (link broken)";
+        return false;
+      }
+      const uint64_t now = mono_ms();
+      for (int q = 0; q < world; ++q) {
+        const uint64_t b = shm_->beat[q].load(std::memory_order_relaxed);
+        if (now > b && now - b > limit) {   // q stopped heartbeating: dead or hung outside the library
+          broken_ = true;
+          shm_->broken.store(1, std::memory_order_release);
+          char m[200];
+          snprintf(m, sizeof m, "peer barrier: rank %d silent for %.0f s (rank %d waiting; link now broken)", q,
+                   (now - b) / 1000.0, rank);
+          err = m;
+          return false;
+        }
+      }
     }
     pause_briefly(spins);
   }
@@ -123,6 +169,8 @@ bool PeerLink::attach(const char* name, int rank_, int world_, int device, doubl
     memset(m, 0, shm_bytes_);
     new (&shm_->count) std::atomic<uint32_t>(0);
     new (&shm_->generation) std::atomic<uint32_t>(0);
+    new (&shm_->broken) std::atomic<uint32_t>(0);
+    for (int r = 0; r < PEER_MAX; ++r) new (&shm_->beat[r]) std::atomic<uint64_t>(mono_ms());
     for (int r = 0; r < PEER_MAX; ++r) new (&shm_->published[r]) std::atomic<uint32_t>(0);
     shm_->world = world;
     shm_->magic.store(MAGIC, std::memory_order_release);
@@ -184,6 +232,7 @@ bool PeerLink::attach(const char* name, int rank_, int world_, int device, doubl
 }
 
 void PeerLink::detach() {
+  broken_ = false;
   for (int q = 0; q < PEER_MAX; ++q) {
     if (peer[q] && peer[q] != local) cudaIpcCloseMemHandle(peer[q]);
     peer[q] = nullptr;

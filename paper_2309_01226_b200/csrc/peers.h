@@ -39,8 +39,15 @@ class PeerLink {
   ~PeerLink() { detach(); }
   // Collective over the `world` ranks that pass the same `name` (a fresh POSIX shm name,
   // e.g. "/saturn_<nonce>", created by rank 0).  device < 0: host-only (barrier only).
+  // `timeout_s` is a LIVENESS timeout: a rank that stops heartbeating for that long (its
+  // process died or hangs outside the library) fails every other rank's barrier.  A rank
+  // that is merely slow (its GPU still busy) keeps heartbeating from wait_stream, so a long
+  // or badly balanced enumeration never times out spuriously.
   bool attach(const char* name, int rank, int world, int device, double timeout_s);
   bool barrier();
+  // cudaStreamSynchronize that heartbeats while the GPU works (use before a barrier).
+  cudaError_t wait_stream(cudaStream_t st);
+  bool broken() const;   // a barrier failed on some rank: every later barrier fails fast
   void detach();
 
   int rank = 0, world = 1;
@@ -54,6 +61,8 @@ class PeerLink {
   struct Shm;
   Shm* shm_ = nullptr;
   size_t shm_bytes_ = 0;
+  bool broken_ = false;
+  void heartbeat();
   int device_ = -1;
   std::string name_;
 };

@@ -25,7 +25,7 @@ DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
 
 # Every symbol declared in include/saturn.h.
 EXPORTS = (
-    "saturn_plan_create", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
+    "saturn_plan_create", "saturn_workspace_bytes", "saturn_bind_workspace", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
     "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_nodes", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
     "saturn_enumerate", "saturn_enumerate_range", "saturn_set_enumeration_options", "saturn_search", "saturn_search_group", "saturn_search_history",
     "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
@@ -125,7 +125,9 @@ def load_library(path: str = LIB_PATH):
         "saturn_search": [h, P(SearchParams), vp, P(Result)],
         "saturn_search_group": [P(vp), i32, P(SearchParams), P(vp), P(Result)],
         "saturn_search_history": [h, i64, P(ctypes.c_double), P(i64), P(i64)],
-        "saturn_search_population": [h, P(u8), P(u8), P(i32)],
+        "saturn_search_population": [h, i64, P(u8), P(u8), P(i32), P(i64)],
+        "saturn_workspace_bytes": [h, vp, P(u64)],
+        "saturn_bind_workspace": [h, vp, u64],
         "saturn_best_plan": [h, P(Placement), P(u8), P(i64)],
         "saturn_get_unique_id": [P(u8)],
         "saturn_plan_attach_comm": [h, P(u8), i32, i32],
@@ -205,7 +207,7 @@ class SearchConfig:
     elites: int = 16
     generations_per_epoch: int = 8
     p_xover: float = 0.9
-    p_cfg_mut: float | None = 0.5    # per-child probability of re-drawing one job's config
+    p_cfg_mut: float = 0.5           # per-child probability of re-drawing one job's config
     p_perm_mut: float = 0.5
     local_search_iters: int = 0      # memetic elite improvement per epoch (row f4)
 
@@ -225,6 +227,7 @@ class Plan:
         if st != OK:
             raise SaturnError(st, f"saturn_plan_create(node_gpus={list(arr)}, device={device})")
         self._h = h
+        self._ws = None   # bound workspace tensor (bind_workspace)
         self.node_gpus = list(int(x) for x in arr)
         self.device = device
         self.n_jobs = 0
@@ -356,7 +359,7 @@ class Plan:
 
     def _search_params(self, cfg: SearchConfig):
         T = self.n_jobs
-        p_c = cfg.p_cfg_mut if cfg.p_cfg_mut is not None else 1.0 / max(T, 1)
+        p_c = cfg.p_cfg_mut
         return SearchParams(seed=cfg.seed, population=cfg.population, max_generations=cfg.max_generations,
                             time_budget_s=cfg.time_budget_s, elites=cfg.elites,
                             generations_per_epoch=cfg.generations_per_epoch, p_xover_q32=q32(cfg.p_xover),
@@ -414,14 +417,52 @@ class Plan:
                     "saturn_search_history")
         return t[:n.value], m[:n.value]
 
-    def search_population(self, P: int):
+    def search_population(self, P: int | None = None):
+        """Final population of the last search -> (cfg [P][T], perm [P][T], makespan [P]).
+        P is the library's (queried first); a given P must match it."""
         T = self.n_jobs
+        n = ctypes.c_int64()
+        self._check(self._lib.saturn_search_population(self._h, 0, None, None, None, ctypes.byref(n)),
+                    "saturn_search_population")
+        if P is not None and int(P) != n.value:
+            raise SaturnError(EINVAL, f"search_population(P={P}): the last search had population {n.value}")
+        P = n.value
         c = np.zeros((P, T), np.uint8)
         q = np.zeros((P, T), np.uint8)
         m = np.zeros(P, np.int32)
-        self._check(self._lib.saturn_search_population(self._h, _np_ptr(c, ctypes.c_uint8), _np_ptr(q, ctypes.c_uint8),
-                                                       _np_ptr(m, ctypes.c_int32)), "saturn_search_population")
+        self._check(self._lib.saturn_search_population(self._h, P, _np_ptr(c, ctypes.c_uint8),
+                                                       _np_ptr(q, ctypes.c_uint8), _np_ptr(m, ctypes.c_int32),
+                                                       ctypes.byref(n)), "saturn_search_population")
         return c, q, m
+
+    def workspace_bytes(self, cfg: SearchConfig | None = None, n_seed: int = 0) -> int:
+        """saturn_workspace_bytes: device bytes for one search with `cfg` (None: evaluate /
+        enumerate / best_plan only) from a freshly bound workspace."""
+        b = ctypes.c_uint64()
+        sp = None
+        if cfg is not None:
+            sp = self._search_params(cfg)
+            sp.n_seed = int(n_seed)
+        self._check(self._lib.saturn_workspace_bytes(self._h, None if sp is None else ctypes.byref(sp),
+                                                     ctypes.byref(b)), "saturn_workspace_bytes")
+        return b.value
+
+    def bind_workspace(self, workspace=None):
+        """saturn_bind_workspace: carve every device buffer of this handle from a caller-owned
+        torch uint8 tensor (an int = allocate torch.empty(n, dtype=uint8) on the handle's
+        device; None = unbind).  The tensor is kept alive by the Plan while bound."""
+        if workspace is None:
+            self._check(self._lib.saturn_bind_workspace(self._h, None, 0), "saturn_bind_workspace")
+            self._ws = None
+            return None
+        import torch
+        if isinstance(workspace, int):
+            workspace = torch.empty(int(workspace), dtype=torch.uint8, device=f"cuda:{self.device}")
+        assert workspace.dtype == torch.uint8 and workspace.is_contiguous()
+        self._check(self._lib.saturn_bind_workspace(self._h, ctypes.c_void_p(workspace.data_ptr()),
+                                                    workspace.numel()), "saturn_bind_workspace")
+        self._ws = workspace
+        return workspace
 
     def best_plan(self):
         """-> (makespan, placements list of dicts (job-id order), cfg, perm)."""

@@ -673,3 +673,53 @@ def test_profiling_samples_generations(sat, torch):
         assert st["ga_launches"] == want, (per, st)
         assert (st["ga_kernel_ms"] > 0) == (want > 0)
         assert st["ga_decodes"] == want * (4096 - 8)
+
+
+# ------------------------------------------------------------------ §8b workspace
+@pytest.mark.parametrize("name", ["TXT", "MIX"])
+def test_bound_workspace_search_bit_identical(sat, torch, name):
+    """saturn_bind_workspace: a torch.empty(saturn_workspace_bytes) buffer carries every
+    device allocation of a search + best_plan, and the result is bit-identical to the same
+    search on handle-owned (cudaMalloc) memory; one byte short of the requirement -> ELIMIT."""
+    inst = synth.by_name(name, 1)
+    cfg = sat.SearchConfig(seed=11, population=1 << 14, max_generations=6, elites=8, generations_per_epoch=3)
+    ref = _plan(sat, inst)
+    r0 = ref.search(cfg)
+    c0, q0, m0 = ref.search_population()
+    b0 = ref.best_plan()
+    plan = _plan(sat, inst)
+    need = plan.workspace_bytes(cfg)
+    assert need > 2 * (1 << 14) * 32
+    ws = plan.bind_workspace(need)
+    assert ws.numel() == need and ws.device.type == "cuda"
+    r1 = plan.search(cfg)
+    c1, q1, m1 = plan.search_population()
+    b1 = plan.best_plan()
+    assert (r0["makespan"], r0["evaluated"]) == (r1["makespan"], r1["evaluated"])
+    assert np.array_equal(c0, c1) and np.array_equal(q0, q1) and np.array_equal(m0, m1)
+    assert b0[0] == b1[0] and b0[1] == b1[1]
+    # the handle's buffers really live inside the tensor: zeroing it destroys the population
+    ws.zero_()
+    torch.cuda.synchronize()
+    assert (plan.search_population()[2] == 0).all()
+    # too small a workspace: ELIMIT, not a crash or a silent cudaMalloc
+    small = _plan(sat, inst)
+    small.bind_workspace(small.workspace_bytes(cfg) - 4096)
+    with pytest.raises(sat.SaturnError) as ei:
+        small.search(cfg)
+    assert ei.value.status == sat.ELIMIT
+    # unbinding returns to handle-owned memory
+    small.bind_workspace(None)
+    r2 = small.search(cfg)
+    assert r2["makespan"] == r0["makespan"]
+
+
+def test_search_population_capacity(sat, torch):
+    """search_population never writes past the caller's capacity."""
+    inst = synth.txt(0)
+    plan = _plan(sat, inst)
+    plan.search(sat.SearchConfig(seed=1, population=4096, max_generations=2, elites=8))
+    with pytest.raises(sat.SaturnError):
+        plan.search_population(1024)
+    c, q, m = plan.search_population()
+    assert c.shape == (4096, inst.n_jobs) and m.shape == (4096,)

@@ -77,3 +77,48 @@ def test_peer_attach_errors():
     # world 1: attaching and barriers are trivial
     plan.attach_peers(sat.peer_name(), 0, 1)
     plan.barrier()
+
+
+def _dead_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SATURN_PEER_TIMEOUT_S="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2309_01226_b200 as sat
+    plan = sat.Plan([4], device=-1)
+    sat.attach_peers(plan)
+    plan.barrier()
+    out = []
+    if rank == 1:
+        time.sleep(3.0)            # silent (no heartbeat) for longer than the 1 s liveness timeout
+    for _ in range(2):
+        t0 = time.monotonic()
+        try:
+            plan.barrier()
+            out.append(("ok", time.monotonic() - t0))
+        except sat.SaturnError as e:
+            out.append((str(e), time.monotonic() - t0))
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_barrier_silent_rank_poisons_link():
+    """a rank silent past the liveness timeout fails the waiting rank's barrier and
+    marks the link broken in the shared segment, so every later barrier -- on both ranks,
+    including the late one -- fails fast instead of pairing with a stale arrival count."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    ps = [ctx.Process(target=_dead_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get() for _ in range(2))
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    (m0a, t0a), (m0b, t0b) = res[0]
+    assert "silent" in m0a and 0.9 < t0a < 2.9          # detected after ~1 s, before rank 1 woke
+    assert "broken" in m0b and t0b < 0.5                 # then fails fast
+    for m, t in res[1]:
+        assert "broken" in m and t < 0.5                 # the late rank sees the poisoned link
