@@ -171,6 +171,56 @@ class SpaseMilp:
         x[self.idx[("C",)]] = makespan
         return x
 
+    # ---------------------------------------------------------------- LP export (row f3)
+    def var_name(self, key) -> str:
+        """B_t_s, O_t_n, P_t_n_g, A_t1_t2, I_t_n_g, C (Table 1's symbols)."""
+        return "_".join(str(k) for k in key)
+
+    def to_lp(self, f) -> None:
+        """Write the MILP in CPLEX LP format (the format PuLP hands to Gurobi/CBC):
+        objective, one named row per constraint (tag_index; ranged rows as two), bounds,
+        binaries.  `f` is a path or a text file object."""
+        if isinstance(f, str):
+            with open(f, "w") as fh:
+                return self.to_lp(fh)
+        names = [None] * self.n_vars
+        for key, j in self.idx.items():
+            names[j] = self.var_name(key)
+
+        def fmt(v):
+            return repr(float(v)) if not float(v).is_integer() else str(int(v))
+
+        def lin(r):
+            a, b = self.A.indptr[r], self.A.indptr[r + 1]
+            parts = []
+            for j, v in zip(self.A.indices[a:b], self.A.data[a:b]):
+                if v == 0:
+                    continue
+                parts.append(("- " if v < 0 else "+ ") + fmt(abs(v)) + " " + names[j])
+            return " ".join(parts) if parts else "0 C"
+
+        f.write("\\ SPASE MILP, PAPER.md Eqs. 1-11 (readings A1-A3, DESIGN.md)\n")
+        f.write(f"Minimize\n obj: {names[self.idx[('C',)]]}\nSubject To\n")
+        for r in range(self.n_rows):
+            lo, hi, e = self.lo[r], self.hi[r], lin(r)
+            tag = f"{self.tags[r].replace('-', '_')}_{r}"
+            if lo == hi:
+                f.write(f" {tag}: {e} = {fmt(lo)}\n")
+            else:
+                if np.isfinite(lo):
+                    f.write(f" {tag}_lo: {e} >= {fmt(lo)}\n")
+                if np.isfinite(hi):
+                    f.write(f" {tag}_hi: {e} <= {fmt(hi)}\n")
+        f.write("Bounds\n")
+        for j in range(self.n_vars):
+            if self.kinds[j] == 0:
+                f.write(f" {names[j]} >= 0\n")
+        f.write("Binaries\n")
+        for j in range(self.n_vars):
+            if self.kinds[j] == 1:
+                f.write(f" {names[j]}\n")
+        f.write("End\n")
+
     def solution_to_plan(self, x):
         c, plan = self.c, []
         for t in range(self.T):
@@ -186,6 +236,37 @@ class SpaseMilp:
             plan.append(dict(node=n, upp=c.config(t, s)[0], gpus=gg, cfg=s, start_s=st, end_s=st + r,
                              gpu_mask=mask))
         return plan
+
+
+def read_lp(text: str):
+    """Minimal reader of the LP files to_lp writes (for the round-trip pin): -> (objective
+    variable, {row name: ({var: coef}, sense, rhs)}, binaries, nonnegatives)."""
+    sec, rows, binaries, nonneg, obj = None, {}, [], [], None
+    for raw in text.splitlines():
+        ln = raw.strip()
+        if not ln or ln.startswith("\\"):
+            continue
+        if ln in ("Minimize", "Subject To", "Bounds", "Binaries", "End"):
+            sec = ln
+            continue
+        if sec == "Minimize":
+            obj = ln.split(":", 1)[1].strip()
+        elif sec == "Subject To":
+            name, rest = ln.split(":", 1)
+            for op in (">=", "<=", "="):
+                if f" {op} " in rest:
+                    lhs, rhs = rest.rsplit(f" {op} ", 1)
+                    break
+            toks, coef = lhs.split(), {}
+            for k in range(0, len(toks), 3):
+                sign, val, var = toks[k], float(toks[k + 1]), toks[k + 2]
+                coef[var] = coef.get(var, 0.0) + (val if sign == "+" else -val)
+            rows[name.strip()] = (coef, op, float(rhs))
+        elif sec == "Bounds":
+            nonneg.append(ln.split()[0])
+        elif sec == "Binaries":
+            binaries.append(ln)
+    return obj, rows, binaries, nonneg
 
 
 def milp_makespan(c, time_limit: float = 60.0):

@@ -723,3 +723,24 @@ def test_search_population_capacity(sat, torch):
         plan.search_population(1024)
     c, q, m = plan.search_population()
     assert c.shape == (4096, inst.n_jobs) and m.shape == (4096,)
+
+
+# ------------------------------------------------------------------ f3: GPU plans vs the paper's MILP rows
+@pytest.mark.parametrize("which", ["TXT", "MIX", "HETERO"])
+def test_gpu_best_plan_satisfies_paper_milp(sat, torch, which):
+    """f3: the plan the CUDA path returns (search, then
+    the trace decoder's placements) written as the paper's variables B, O, P, A, I, C violates
+    no row of the paper's MILP (Eqs. 1-11, readings A1-A3), and its C equals the makespan."""
+    from oracle.milp import SpaseMilp
+    inst = {"TXT": lambda: synth.txt(0), "MIX": lambda: synth.mix(0),
+            "HETERO": lambda: synth.sweep(5, n_jobs=20, nodes=[2, 2, 4, 8])}[which]()
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    plan = _plan(sat, inst)
+    r = plan.search(sat.SearchConfig(seed=4, population=1 << 14, max_generations=24, elites=8,
+                                     generations_per_epoch=8))
+    best, pl, bc, bp = plan.best_plan()
+    assert best == r["makespan"]
+    m = SpaseMilp(c)
+    x = m.plan_to_assignment(pl, best)
+    assert m.violations(x) == []
+    assert x[m.idx[("C",)]] == max(p["end_s"] for p in pl) == best

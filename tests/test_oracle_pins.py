@@ -309,3 +309,96 @@ def test_bounded_draw_is_uniform_multiply_shift():
     assert min(xs) == 0 and max(xs) == 6
     counts = np.bincount(xs, minlength=7)
     assert counts.min() > 850
+
+
+# ---------------------------------------------------------------- f3: LP export, check_solution == O3
+def test_lp_export_round_trip():
+    """to_lp writes every row of the paper's MILP (Eqs. 1-11) in CPLEX LP format; reading
+    the file back gives the same coefficients, senses and right-hand sides, 17 variables and
+    54 constraint rows on SPEC's 2-task instance, and a decoded plan satisfies
+    every row as read from the file."""
+    import io
+    from oracle.milp import read_lp
+    # SPEC's 2-task instance (golden SPEC-10: two jobs, each (UPP 3, 1 GPU, 10 s) or
+    # (UPP 1, 2 GPUs, 6 s), on 1 x 2 GPUs)
+    c = oracle.compact([2], dense_from_configs([[[3, 1, 10], [1, 2, 6]], [[3, 1, 10], [1, 2, 6]]]))
+    m = SpaseMilp(c)
+    buf = io.StringIO()
+    m.to_lp(buf)
+    obj, rows, binaries, nonneg = read_lp(buf.getvalue())
+    assert obj == "C" and len(binaries) + len(nonneg) == m.n_vars == 17
+    assert len({k.rsplit("_", 1)[0] if k.endswith(("_lo", "_hi")) else k for k in rows}) <= m.n_rows == 54
+    for seed in range(4):
+        rng = np.random.default_rng(900 + seed)
+        inst = synth.random_tiny(rng, max_jobs=4, node_choices=([2], [3, 2]), max_r=6)
+        cc = oracle.compact(inst.node_gpus, inst.runtime)
+        mm = SpaseMilp(cc)
+        b = io.StringIO()
+        mm.to_lp(b)
+        _, rows, bins, _ = read_lp(b.getvalue())
+        names = {j: mm.var_name(k) for k, j in mm.idx.items()}
+        assert sorted(bins) == sorted(names[j] for j in range(mm.n_vars) if mm.kinds[j] == 1)
+        # every matrix row appears with identical coefficients
+        A = mm.A.tocsr()
+        for r in range(mm.n_rows):
+            coef = {names[j]: v for j, v in zip(A.indices[A.indptr[r]:A.indptr[r + 1]], A.data[A.indptr[r]:A.indptr[r + 1]])
+                    if v != 0}
+            tag = f"{mm.tags[r].replace('-', '_')}_{r}"
+            for suffix, bound, op in (("", mm.lo[r], "="), ("_lo", mm.lo[r], ">="), ("_hi", mm.hi[r], "<=")):
+                if tag + suffix in rows:
+                    got, gop, rhs = rows[tag + suffix]
+                    assert gop == op and abs(rhs - bound) < 1e-9
+                    assert set(got) == set(coef) and all(abs(got[k] - coef[k]) < 1e-9 for k in coef)
+        # a decoded plan satisfies the rows as read back from the file
+        cfg, perm = synth.random_genomes(cc.S, 1, seed=seed)
+        ms, pl = oracle.decode(cc, cfg[0], perm[0])
+        x = mm.plan_to_assignment(pl, ms)
+        val = {names[j]: x[j] for j in range(mm.n_vars)}
+        for name, (coef, op, rhs) in rows.items():
+            lhs = sum(v * val[k] for k, v in coef.items())
+            assert {"=": abs(lhs - rhs) < 1e-6, ">=": lhs >= rhs - 1e-6, "<=": lhs <= rhs + 1e-6}[op], name
+
+
+def test_milp_check_solution_equals_validator():
+    """f3: the paper's MILP rows as a checker (check_solution) accept exactly the
+    plans O3 accepts: decoded plans pass both; each planted fault (overlap on a GPU, a GPU
+    too few, a wrong config width, a start moved into a busy GPU, a makespan below the last
+    end) fails both."""
+    seen = 0
+    for seed in range(12):
+        rng = np.random.default_rng(1000 + seed)
+        inst = synth.random_tiny(rng, max_jobs=4, node_choices=([2], [4], [2, 2], [3, 2]), max_r=6)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        m = SpaseMilp(c)
+        cfg, perm = synth.random_genomes(c.S, 3, seed=seed)
+        for i in range(3):
+            ms, pl = oracle.decode(c, cfg[i], perm[i])
+            assert oracle.validate(c, pl, ms) == [] and m.violations(m.plan_to_assignment(pl, ms)) == []
+            faults = []
+            for t, p in enumerate(pl):
+                gn = int(c.node_gpus[p["node"]])
+                for u in range(len(pl)):          # overlap: move job u onto job t's GPUs and start
+                    if u != t and pl[u]["node"] == p["node"] and pl[u]["gpus"] == p["gpus"] and \
+                            pl[u]["gpu_mask"] != p["gpu_mask"]:
+                        f = [dict(x) for x in pl]
+                        f[u]["gpu_mask"], f[u]["start_s"] = p["gpu_mask"], p["start_s"]
+                        f[u]["end_s"] = p["start_s"] + (pl[u]["end_s"] - pl[u]["start_s"])
+                        faults.append(f)
+                if p["gpus"] > 1:                  # a GPU too few
+                    f = [dict(x) for x in pl]
+                    f[t]["gpu_mask"] &= f[t]["gpu_mask"] - 1
+                    faults.append(f)
+                if p["gpus"] < gn and bin(p["gpu_mask"]).count("1") < gn:   # a GPU too many
+                    f = [dict(x) for x in pl]
+                    free = [g for g in range(gn) if not p["gpu_mask"] >> g & 1][0]
+                    f[t]["gpu_mask"] |= 1 << free
+                    faults.append(f)
+            for f in faults:
+                fms = max(x["end_s"] for x in f)
+                v_o3 = oracle.validate(c, f, fms)
+                v_milp = m.violations(m.plan_to_assignment(f, fms))
+                assert (v_o3 == []) == (v_milp == []), (v_o3, v_milp)
+                seen += v_o3 != []
+            low = m.plan_to_assignment(pl, ms - 1)
+            assert m.violations(low) and oracle.validate(c, pl, ms - 1)
+    assert seen > 20
