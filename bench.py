@@ -381,7 +381,9 @@ def quality_leg(sat, torch, local, budget_s, runs):
                     "cpu_5min_bar": b["bar"], "bar_file": b.get("bar_file"),
                     "beats_bar": (b["bar"] is not None and r["makespan"] <= b["bar"]),
                     "lower_bound": lb, "best_over_lb": (r["makespan"] / lb) if lb else None,
-                    "best_lower_bound": b.get("bar_best_lower_bound"), "baselines": base})
+                    "best_lower_bound": b.get("bar_best_lower_bound"),
+                    "gap_to_best_lower_bound": ((r["makespan"] - b["bar_best_lower_bound"]) / b["bar_best_lower_bound"])
+                    if b.get("bar_best_lower_bound") else None, "baselines": base})
         del plan
     return out
 

@@ -17,6 +17,7 @@ LIB = os.path.join(ROOT, "oracle", "liboracle.so")
 C_SRC = "oracle/saturn_oracle.c"
 LS_SRC = "oracle/local_search.py"
 GA_SRC = "oracle/ga.py"
+LB_SRC = "oracle/bounds.py"
 PINS = "tests/test_oracle_pins.py"
 SEARCH_PINS = "tests/test_oracle_search_pins.py"
 
@@ -41,6 +42,11 @@ MUTATIONS = [
     (GA_SRC, SEARCH_PINS, "last swap skipped", "for i in range(T - 1, 0, -1):", "for i in range(T - 1, 1, -1):"),
     (GA_SRC, SEARCH_PINS, "config range short by one", "cfg = [st.below(int(S[t])) for t in range(T)]",
      "cfg = [st.below(max(int(S[t]) - 1, 1)) for t in range(T)]"),
+    (LB_SRC, PINS, "knapsack capacity one too many", "best = [0.0] * (cap + 1)\n    choice = [[] for _ in range(cap + 1)]",
+     "cap = cap + 1\n    best = [0.0] * (cap + 1)\n    choice = [[] for _ in range(cap + 1)]"),
+    (LB_SRC, PINS, "job progress counted twice", "A[nK + t, j] = -1.0 / jobs[t][s][1]",
+     "A[nK + t, j] = -2.0 / jobs[t][s][1]"),
+    (LB_SRC, PINS, "longest-job row dropped", "[(longest, None)]", "[(0, None)]"),
 ]
 
 

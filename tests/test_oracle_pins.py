@@ -402,3 +402,33 @@ def test_milp_check_solution_equals_validator():
             low = m.plan_to_assignment(pl, ms - 1)
             assert m.violations(low) and oracle.validate(c, pl, ms - 1)
     assert seen > 20
+
+
+# ---------------------------------------------------------------- O5b configuration-LP bound
+def test_config_lp_bound_hand_examples():
+    """Hand-checked: on 1 x 3 GPUs two (2 GPUs, 10 s) jobs can never overlap (4 > 3), so the
+    bound is 20 = OPT while the area bound is ceil(40 / 3) = 14.  On 1 x 4 GPUs with A
+    (3 GPUs, 4 s), B (2, 4), C (1, 4): A and B exclude each other (5 > 4) -> 8 = OPT; area
+    ceil(24 / 4) = 6."""
+    from oracle.bounds import config_lp_bound
+    c = oracle.compact([3], dense_from_single([(2, 10), (2, 10)]))
+    assert config_lp_bound(c)[0] == 20 == oracle.brute_force(c)[0] and oracle.lower_bound(c) == 14
+    c = oracle.compact([4], dense_from_single([(3, 4), (2, 4), (1, 4)]))
+    assert config_lp_bound(c)[0] == 8 == oracle.brute_force(c)[0] and oracle.lower_bound(c) == 6
+
+
+def test_config_lp_bound_between_area_bound_and_optimum():
+    """A valid relaxation (never above the brute-force optimum) that dominates O5, on random
+    single- and multi-node tiny instances; strictly tighter than O5 on some of them."""
+    from oracle.bounds import config_lp_bound
+    tighter = 0
+    for seed in range(40):
+        rng = np.random.default_rng(1200 + seed)
+        inst = synth.random_tiny(rng, max_jobs=4, node_choices=([3], [4], [2, 2], [3, 2]), max_r=6)
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        lb, m_star, _ = config_lp_bound(c)
+        opt = oracle.brute_force(c)[0]
+        o5 = oracle.lower_bound(c)
+        assert o5 <= lb <= opt, (o5, lb, opt, inst.runtime)
+        tighter += lb > o5
+    assert tighter >= 5
