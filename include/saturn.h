@@ -55,8 +55,10 @@ typedef enum {
 /* saturn_result.flags */
 enum { SATURN_PROVEN_OPTIMAL = 1, SATURN_INCUMBENT = 2, SATURN_PREFIX_SHARED = 4, SATURN_SYMMETRY_REDUCED = 8 };
 
-/* saturn_set_decoder kinds (row a5: two device designs, chosen by measurement) */
-enum { SATURN_DECODER_AUTO = 0, SATURN_DECODER_THREAD = 1, SATURN_DECODER_WARP = 2 };
+/* saturn_set_decoder kinds (row a5: two device designs, chosen by measurement; NODE_SMEM =
+ * the thread design with every node's sorted free-time vector in shared memory and a runtime
+ * node count -- the default for clusters without a compiled register shape) */
+enum { SATURN_DECODER_AUTO = 0, SATURN_DECODER_THREAD = 1, SATURN_DECODER_WARP = 2, SATURN_DECODER_NODE_SMEM = 3 };
 
 /* One job of a decoded plan = the paper's per-task outputs (Table 1 B, O, P,
  * I): node n (O), UPP index and GPU count of the chosen config, the config index s into the
@@ -156,8 +158,10 @@ saturn_status saturn_num_configs(const saturn_plan *p, int32_t *n_jobs, int32_t 
 saturn_status saturn_config(const saturn_plan *p, int32_t job, int32_t cfg, int32_t *upp, int32_t *gpus,
                             int32_t *runtime_s);
 
-/* Select the device decoder design for evaluate (AUTO = thread design when compiled for the
- * cluster shape, else warp).  EINVAL for an unknown kind. */
+/* Select the device decoder design (AUTO = thread design when compiled for the cluster shape,
+ * else warp).  WARP applies to evaluate; NODE_SMEM applies to evaluate, search, local search
+ * and enumeration (index order instead of the register-state DFS).  EINVAL for an unknown
+ * kind. */
 saturn_status saturn_set_decoder(saturn_plan *p, int32_t kind);
 
 /* Decode n genomes (row a5).  d_cfg, d_perm: device uint8 [n][T] (genome-major rows);
@@ -282,18 +286,40 @@ saturn_status saturn_baseline_genome(const saturn_plan *p, int32_t kind, uint64_
  * the loaded workload W:  S = solve(W), M = makespan(S), time = 0; while M > I: W = W after I
  * seconds of S (residual runtimes, reading A10: a job that ran a s of its config with runtime
  * R0 keeps every config with R' = ceil(R (R0 - a) / R0); finished jobs leave), S = S[I:],
- * M -= I, time += I, P = solve(W), adopt P iff makespan(P) <= M - T.  E2E makespan =
- * time + M at the end.  solve = saturn_search (SATURN_SOLVER_SEARCH, with `search`) or
- * saturn_enumerate (SATURN_SOLVER_ENUMERATE, exact; tiny workloads).  The loaded table is
- * restored afterwards.  round_log (host, may be NULL): per round {time, M after the
- * shift, makespan(P), adopted} as 4 int64.  Synchronous. */
+ * M -= I, time += I, apply the round's events, P = solve(W), adopt P iff makespan(P) <= M - T
+ * (or unconditionally when a job arrived).  E2E makespan = time + M at the end.
+ * solve = saturn_search (SATURN_SOLVER_SEARCH, with `search`) or saturn_enumerate
+ * (SATURN_SOLVER_ENUMERATE, exact; tiny workloads).  The loaded table is restored afterwards.
+ * Events, applied at round boundaries after the advance:
+ * STOP removes job `job` (original id; arrivals are numbered T, T+1, ... in event order) from
+ * W and from the current plan (M = the plan's latest end); ARRIVE adds a job with runtime row
+ * runtime_s [n_upps][max_gpus] (the table's layout).  Events due after the workload is
+ * exhausted never fire; a STOP naming a finished or unknown job is EINVAL.
+ * Overlap mode: round k+1's proposal is solved on the SIMULATED
+ * next-interval state advance(W, S, I) while round k runs, so the solver latency hides behind
+ * the interval (interval_wall_s seconds of real time; 0 = interval_s); an event at that
+ * boundary makes it stale and a fresh solve replaces it -- the E2E schedule is identical to
+ * the sequential loop's.  round_log (host, may be NULL): per round {time, M after the shift,
+ * makespan(P), adopted} as 4 int64.  Synchronous. */
 enum { SATURN_SOLVER_SEARCH = 0, SATURN_SOLVER_ENUMERATE = 1 };
+enum { SATURN_EVENT_STOP = 1, SATURN_EVENT_ARRIVE = 2 };
+typedef struct {
+  int32_t at_round;                   /* >= 1: applied at time at_round * I         */
+  int32_t kind;                       /* SATURN_EVENT_STOP | SATURN_EVENT_ARRIVE     */
+  int32_t job;                        /* STOP: original job id                      */
+  int32_t pad;
+  const int32_t *runtime_s;           /* ARRIVE: host [n_upps][max_gpus]            */
+} saturn_introspect_event;
 typedef struct {
   int64_t interval_s;                 /* I (the paper uses 1000 s)   */
   int64_t threshold_s;                /* T (500 s)             */
   int32_t solver;
   int32_t max_rounds;
   const saturn_search_params *search; /* SEARCH: parameters of every round's solve  */
+  int32_t overlap;                    /* 1: overlap mode                            */
+  int32_t n_events;
+  const saturn_introspect_event *events;
+  double interval_wall_s;             /* overlap latency accounting; 0 = interval_s */
 } saturn_introspect_params;
 typedef struct {
   int64_t one_shot_makespan;  /* makespan of the round-0 plan                       */
@@ -301,6 +327,12 @@ typedef struct {
   int32_t rounds;
   int32_t adopted;
   uint64_t evaluated;         /* decodes of all solves                              */
+  int32_t stale;              /* overlap mode: proposals discarded because an event fired */
+  int32_t solves;             /* solver calls (incl. stale ones)                   */
+  double solve_s;             /* wall seconds of the re-solves (rounds >= 1)       */
+  double exposed_solve_s;     /* of which on the critical path: sequential = all of it;
+                                 overlap = sum max(0, t - interval_wall_s) + fresh
+                                 re-solves after events                            */
 } saturn_introspect_result;
 saturn_status saturn_introspect(saturn_plan *p, const saturn_introspect_params *ip, void *stream,
                                 saturn_introspect_result *out, int64_t *round_log);

@@ -14,6 +14,21 @@ keeps every config with R' = ceil(R * (R0 - a) / R0) (integers); finished jobs l
 not yet started are unchanged.  S[I:] keeps every placement (node, GPUs) and shifts its
 times by -I (a running job restarts at 0 with its residual runtime R0 - a).
 `solve` here is the exact brute force (oracle O2), so the whole loop is deterministic.
+
+Workload events ("early-stopping ... or new job
+arrivals"), applied at round boundaries only: after round r's advance, before its re-solve.
+  ("stop", job)       -- job (original id; arrivals are numbered T, T+1, ... in event order)
+                         leaves W and the current plan; M becomes the plan's latest end.
+  ("arrive", row)     -- a new job with runtime row [U][Gmax] joins W; the current plan does
+                         not hold it, so the round's proposal is adopted unconditionally.
+An event naming a finished or unknown job raises ValueError; events due after the workload
+is exhausted never fire.
+
+Overlap mode: the proposal for round r+1 is computed
+on the SIMULATED next-interval state advance(W, S, I) while round r runs (the solver's latency
+is hidden behind the interval).  If an event fires at that boundary the proposal is stale and
+a fresh solve of the mutated workload replaces it, so the E2E schedule is identical to the
+sequential loop's; `stale` counts the discarded proposals.
 """
 from __future__ import annotations
 
@@ -53,20 +68,56 @@ def residual(table, plan, I):
     return np.stack(rows), keep, shifted
 
 
-def introspect(nodes, table, I: int, T: int, max_rounds: int = 10_000):
+def introspect(nodes, table, I: int, T: int, max_rounds: int = 10_000, events=(), overlap: bool = False):
     table = np.asarray(table, np.int32)
+    ids = list(range(table.shape[0]))          # original job id of every row of `table`
+    next_id = table.shape[0]
     M, S, _ = _solve(nodes, table)
     one_shot = M
-    time, rounds, adopted, log = 0, 0, 0, []
+    time, rounds, adopted, stale, log = 0, 0, 0, 0, []
+    by_round = {}
+    for r, kind, arg in events:
+        by_round.setdefault(int(r), []).append((kind, arg))
     while M > I and rounds < max_rounds:
+        lookahead = None
+        if overlap:   # solved on the simulated next-interval state, before this round ends
+            nxt, _, _ = residual(table, S, I)
+            lookahead = None if nxt is None else _solve(nodes, nxt)[:2]
         table, keep, S = residual(table, S, I)
+        ids = [ids[k] for k in keep]
         M -= I
         time += I
         rounds += 1
-        Mp, P, _ = _solve(nodes, table)
-        take = Mp <= M - T
+        fired, arrived = by_round.get(rounds, []), False
+        for kind, arg in fired:
+            if kind == "stop":
+                if arg not in ids:
+                    raise ValueError(f"stop event names job {arg}, which is finished or unknown")
+                k = ids.index(arg)
+                table = np.delete(table, k, axis=0)
+                del ids[k]
+                del S[k]
+            elif kind == "arrive":
+                row = np.asarray(arg, np.int32)[None]
+                table = row if table is None else np.concatenate([table, row], axis=0)
+                ids.append(next_id)
+                next_id += 1
+                arrived = True
+            else:
+                raise ValueError(kind)
+        if fired:
+            stale += int(lookahead is not None)
+            lookahead = None
+            M = max((p["end_s"] for p in S), default=0)
+        if table is None or len(ids) == 0:   # every job stopped: the workload is exhausted
+            M = 0
+            log.append((time, 0, 0, 0))
+            break
+        Mp, P = lookahead if lookahead is not None else _solve(nodes, table)[:2]
+        take = arrived or Mp <= M - T
         log.append((time, M, Mp, int(take)))
         if take:
             S, M = P, Mp
             adopted += 1
-    return {"one_shot": one_shot, "e2e": time + M, "rounds": rounds, "adopted": adopted, "log": log}
+    return {"one_shot": one_shot, "e2e": time + M, "rounds": rounds, "adopted": adopted, "stale": stale,
+            "log": log}

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: ranges cost nothing without a profiler
 #include <memory>
 #include <chrono>
 #include <cstdarg>
@@ -111,6 +112,15 @@ struct DevBuf {
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+
+// NVTX range for profilers (nsys / ncu --nvtx): search, epochs, exchanges, enumeration,
+// introspection rounds.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 }  // namespace
 
@@ -258,19 +268,26 @@ struct DeviceGuard {
 
 int gs_of(int T) { return sat::record_bytes(T); }  // cfg | pad | perm | pad
 
+// Decoder shape of the search-side kernels (GA, local search, index-order enumeration):
+// the load-time shape, or node vectors in shared memory (NN = 0) when the caller selected
+// SATURN_DECODER_NODE_SMEM.
+void run_shape(const saturn_plan* p, int* nn, int* gp) {
+  if (p->decoder == SATURN_DECODER_NODE_SMEM) {
+    *nn = 0;
+    *gp = std::max(4, p->GP);
+  } else {
+    *nn = p->NN;
+    *gp = p->GP;
+  }
+}
+
 // Decoder shape for the evaluate kernel: 4-node register states (SWEEP 4x8) are ALU-bound on
 // their gather/scatter selects, and there the shared-memory node-state decoder (dynamic
 // indexing on the LSU pipe) measured faster: evaluate 1.15e9 -> 1.37e9 plans/s (its GA
 // kernel is slower, so k_ga keeps the register states).  MIX 2x8: equal -> registers.
-// SATURN_EVAL_REGISTERS=1 keeps the register shape.
 void eval_shape(const saturn_plan* p, int* nn, int* gp) {
-  static const bool regs = [] {
-    const char* e = getenv("SATURN_EVAL_REGISTERS");
-    return e && e[0] == '1';
-  }();
-  *nn = p->NN;
-  *gp = p->GP;
-  if (!regs && p->NN >= 4 && sat::have_sorted_shape(0, std::max(4, p->GP)) &&
+  run_shape(p, nn, gp);
+  if (*nn >= 4 && sat::have_sorted_shape(0, std::max(4, p->GP)) &&
       sat::eval_smem_bytes(p->pb, 0, std::max(4, p->GP)) <= 227 * 1024) {
     *nn = 0;
     *gp = std::max(4, p->GP);
@@ -288,6 +305,7 @@ bool host_only(saturn_plan* p) {
 saturn_status use_decoder_kind(saturn_plan* p, int* kind) {
   if (host_only(p)) return SATURN_ESTATE;
   int k = p->decoder;
+  if (k == SATURN_DECODER_NODE_SMEM) k = SATURN_DECODER_THREAD;   // (shape from eval_shape)
   if (k == SATURN_DECODER_AUTO) k = p->sorted_ok ? SATURN_DECODER_THREAD : SATURN_DECODER_WARP;
   if (k == SATURN_DECODER_THREAD && !p->sorted_ok)
     return fail(p, SATURN_EINVAL, "thread decoder not compiled for %d nodes x %d GPUs (padded)", p->NN, p->GP);
@@ -361,7 +379,9 @@ saturn_status saturn_workspace_bytes(const saturn_plan* pc, const saturn_search_
     const int GS = gs_of(T);
     const int world = std::max(p->world, 1);
     DeviceGuard dg(p->device);
-    const size_t cand = (size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64;
+    int rnn, rgp;
+    run_shape(p, &rnn, &rgp);
+    const size_t cand = (size_t)sat::ga_max_candidates(p->pb, rnn, rgp, E, GS, P, p->sms) + 64;
     b += 2 * arena_round((size_t)P * GS) + 2 * arena_round((size_t)P * 4) + arena_round(cand * 8) + arena_round(8);
     b += arena_round((size_t)E * 4) + arena_round((size_t)E * GS) + arena_round((size_t)E * world * 4) +
          arena_round((size_t)E * GS * world);
@@ -504,13 +524,13 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   p->pb = pb;
   // Decoder shape: node vectors in registers when that shape is compiled (faster: measured
   // r1 on MIX 2x8 and SWEEP 4x8, profiles/r1/README.md), else node vectors in shared
-  // memory with a runtime node count (NN = 0).  SATURN_MULTINODE_SMEM=1 forces the latter.
+  // memory with a runtime node count (NN = 0; SATURN_DECODER_NODE_SMEM selects it for any
+  // cluster).
   p->GP = std::max(2, pow2_at_least(p->maxG));
   p->NN = 1;
   if (p->gpu_n.size() > 1) {
-    const char* env = getenv("SATURN_MULTINODE_SMEM");
     const int nn = pow2_at_least((int)p->gpu_n.size());
-    if (!(env && env[0] == '1') && sat::have_sorted_shape(nn, p->GP)) {
+    if (sat::have_sorted_shape(nn, p->GP)) {
       p->NN = nn;
     } else {
       p->NN = 0;
@@ -551,7 +571,7 @@ saturn_status saturn_config(const saturn_plan* p, int32_t job, int32_t cfg, int3
 
 saturn_status saturn_set_decoder(saturn_plan* p, int32_t kind) {
   if (!p) return SATURN_EINVAL;
-  if (kind < SATURN_DECODER_AUTO || kind > SATURN_DECODER_WARP) return fail(p, SATURN_EINVAL, "decoder %d", kind);
+  if (kind < SATURN_DECODER_AUTO || kind > SATURN_DECODER_NODE_SMEM) return fail(p, SATURN_EINVAL, "decoder %d", kind);
   p->decoder = kind;
   return SATURN_OK;
 }
@@ -716,18 +736,9 @@ saturn_status peer_reduce_keys(saturn_plan* p, unsigned long long* key, cudaStre
 // for the other GPUs), and the DFS reads that slot as its live branch-and-bound incumbent,
 // so every rank prunes with every rank's best.  begin: rank 0 initialises the pair, barrier;
 // end: barrier after all kernels, read the pair, barrier (before the next call re-inits).
-// DFS root scheduling: the static grid stride by default; SATURN_DFS_DYNAMIC=1 claims batches
-// of roots from a counter (ws_key[2]).  Measured r1: dynamic is slower (7 jobs on 1x4: 4.7 vs
-// 3.7 ms; 9 on 2x2: 0.83 vs 0.77 s) -- batches of consecutive roots find the good leaves
-// later, the shared incumbent tightens later and 30 % more leaves are visited.
-unsigned long long* dfs_work(saturn_plan* p) {
-  static const bool dyn = [] {
-    const char* e = getenv("SATURN_DFS_DYNAMIC");
-    return e && e[0] == '1';
-  }();
-  return dyn ? p->ws_key.p + 2 : nullptr;
-}
-
+// DFS roots by the static grid stride (measured r1: batches of roots claimed from a counter
+// were slower -- 7 jobs on 1x4: 4.7 vs 3.7 ms -- consecutive roots find the good leaves later,
+// the shared incumbent tightens later and 30 % more leaves are visited).
 unsigned long long* peer_shared_slot(saturn_plan* p) {
   return reinterpret_cast<unsigned long long*>(p->peers->peer[0] + sat::PeerLayout::shared);
 }
@@ -771,7 +782,9 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
     const unsigned long long init[2] = {~0ull, 0ull};
     saturn_status sr = peer_shared_begin(p, init, st);
     if (sr != SATURN_OK) return sr;
-    CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, peer_shared_slot(p), p->sms, st));
+    int enn, egp;
+    run_shape(p, &enn, &egp);
+    CU(p, sat::launch_enumerate(p->pb, enn, egp, es, begin, end, peer_shared_slot(p), p->sms, st));
     p->stats.kernel_launches += 1;
     unsigned long long r[2];
     sr = peer_shared_end(p, st, r);
@@ -780,7 +793,9 @@ saturn_status enumerate_impl(saturn_plan* p, uint64_t begin, uint64_t end, uint6
   } else {
     CU(p, p->ws_key.ensure(1));
     CU(p, cudaMemsetAsync(p->ws_key.p, 0xff, sizeof(unsigned long long), st));
-    CU(p, sat::launch_enumerate(p->pb, p->NN, p->GP, es, begin, end, p->ws_key.p, p->sms, st));
+    int enn, egp;
+    run_shape(p, &enn, &egp);
+    CU(p, sat::launch_enumerate(p->pb, enn, egp, es, begin, end, p->ws_key.p, p->sms, st));
     p->stats.kernel_launches += 1;
     if (collective && p->comm) {
       NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
@@ -877,7 +892,7 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
     unsigned long long* g = peer_shared_slot(p);
     CU(p, p->ws_key.ensure(3));
     CU(p, cudaMemsetAsync(p->ws_key.p + 2, 0, sizeof(unsigned long long), st));   // this rank's root counter
-    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, g, g + 1, p->sms, st, dfs_work(p)));
+    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, g, g + 1, p->sms, st));
     p->stats.kernel_launches += 1;
     sr = peer_shared_end(p, st, kl);
     if (sr != SATURN_OK) return sr;
@@ -885,8 +900,7 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
     CU(p, p->ws_key.ensure(3));
     CU(p, cudaMemcpyAsync(p->ws_key.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
     CU(p, cudaMemsetAsync(p->ws_key.p + 1, 0, 2 * sizeof(unsigned long long), st));   // leaves, root counter
-    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st,
-                                    dfs_work(p)));
+    CU(p, sat::launch_enumerate_dfs(p->pb, p->NN, p->GP, ds, rb, re, p->ws_key.p, p->ws_key.p + 1, p->sms, st));
     p->stats.kernel_launches += 1;
     if (p->comm && p->world > 1) {
       NC(p, nccl().allReduce(p->ws_key.p, p->ws_key.p, 1, ncclUint64, ncclMin, p->comm, st));
@@ -915,6 +929,7 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
 }
 
 saturn_status saturn_enumerate(saturn_plan* p, uint64_t max_genomes, void* stream, saturn_result* out) {
+  Nvtx r("saturn_enumerate");
   if (!p) return SATURN_EINVAL;
   if (!p->loaded) return fail(p, SATURN_ESTATE, "enumerate before load_runtime_table");
   if (p->T > sat::ENUM_MAX_T) return fail(p, SATURN_ELIMIT, "T=%d > %d jobs for enumeration", p->T, sat::ENUM_MAX_T);
@@ -928,8 +943,7 @@ saturn_status saturn_enumerate(saturn_plan* p, uint64_t max_genomes, void* strea
   int kind;
   saturn_status s0 = use_decoder_kind(p, &kind);
   if (s0 != SATURN_OK) return s0;
-  const char* env = getenv("SATURN_ENUM_ODOMETER");
-  if (p->T >= 3 && p->NN >= 1 && !(env && env[0] == '1'))
+  if (p->T >= 3 && p->NN >= 1 && p->decoder != SATURN_DECODER_NODE_SMEM)
     return enumerate_dfs_impl(p, size, static_cast<cudaStream_t>(stream), out);
   uint64_t b = 0, e = size;
   saturn_partition(size, p->rank, p->world, &b, &e);
@@ -971,6 +985,7 @@ struct Island {
   int world = 1;            // number of islands in the exchange
   int64_t P = 0;
   int E = 0, GS = 0, T = 0;
+  int NN = 0, GP = 0;   // decoder shape of this search (run_shape)
   sat::GaParams gp{};
   uint64_t evaluated = 0;
   int cur = 0;
@@ -1022,7 +1037,8 @@ struct Island {
       CU(p, p->pop[b].ensure((size_t)P * GS));
       CU(p, p->pms[b].ensure((size_t)P));
     }
-    CU(p, p->cand.ensure((size_t)sat::ga_max_candidates(p->pb, p->NN, p->GP, E, GS, P, p->sms) + 64));
+    run_shape(p, &NN, &GP);
+    CU(p, p->cand.ensure((size_t)sat::ga_max_candidates(p->pb, NN, GP, E, GS, P, p->sms) + 64));
     CU(p, p->n_cand.ensure(2));   // [0] appended candidates, [1] the GA kernels' work counter
     CU(p, cudaMemsetAsync(p->n_cand.p, 0, 2 * sizeof(int), st));
     CU(p, p->rec_ms.ensure(E));
@@ -1052,7 +1068,7 @@ struct Island {
     gp.pm = sp->p_perm_mut_q32;
     evaluated = (uint64_t)P;
     cur = 0;
-    CU(p, sat::launch_ga_init(p->pb, p->NN, p->GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p,
+    CU(p, sat::launch_ga_init(p->pb, NN, GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p,
                               p->pms[0].p, p->cand.p, p->n_cand.p, p->sms, st));
     CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
     p->stats.kernel_launches += 2;
@@ -1079,7 +1095,7 @@ struct Island {
     const bool timed = per > 0 && n_timed < n_prof && (gen % per) == (per / 2) % per;
     const int64_t ti = n_timed;
     if (timed) CU(p, cudaEventRecord(p->ev_pool[3 * ti], st));
-    CU(p, sat::launch_ga_generation(p->pb, p->NN, p->GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
+    CU(p, sat::launch_ga_generation(p->pb, NN, GP, gp, p->pop[cur].p, p->pms[cur].p, p->rec_ms.p,
                                     p->rec_gen.p, p->pop[nxt].p, p->pms[nxt].p, p->cand.p, p->n_cand.p, p->sms, st));
     if (timed) {
       CU(p, cudaEventRecord(p->ev_pool[3 * ti + 1], st));
@@ -1099,7 +1115,7 @@ struct Island {
     DeviceGuard dg(p->device);
     CU(p, cudaMemcpyAsync(p->all_ms.p, p->rec_ms.p, E * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     CU(p, cudaMemcpyAsync(p->all_gen.p, p->rec_gen.p, (size_t)E * GS, cudaMemcpyDeviceToDevice, st));
-    CU(p, sat::launch_local_search(p->pb, p->NN, p->GP, p->all_gen.p, p->all_ms.p, E, GS, sp->local_search_iters,
+    CU(p, sat::launch_local_search(p->pb, NN, GP, p->all_gen.p, p->all_ms.p, E, GS, sp->local_search_iters,
                                    st));
     CU(p, sat::launch_merge_elites(p->all_ms.p, p->all_gen.p, 1, E, GS, p->rec_ms.p, p->rec_gen.p, st));
     p->stats.kernel_launches += 2;
@@ -1230,14 +1246,23 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     NC(p, nccl().allGather(p->rec_gen.p, p->all_gen.p, (size_t)E * GS, ncclUint8, p->comm, st));
     return is.merge();
   };
-  if ((s = exchange()) != SATURN_OK) return s;
-  if ((s = is.record()) != SATURN_OK) return s;
+  {
+    Nvtx r("saturn_search: initial population + exchange");
+    if ((s = exchange()) != SATURN_OK) return s;
+    if ((s = is.record()) != SATURN_OK) return s;
+  }
   int64_t gen = 1;
+  std::unique_ptr<Nvtx> epoch;
   for (; gen <= sp->max_generations; ++gen) {
+    if (!epoch) epoch.reset(new Nvtx("saturn_search: epoch"));
     if ((s = is.generation(gen)) != SATURN_OK) return s;
     if (gen % sp->generations_per_epoch == 0) {
-      if ((s = exchange()) != SATURN_OK) return s;
+      {
+        Nvtx r("exchange");
+        if ((s = exchange()) != SATURN_OK) return s;
+      }
       if ((s = is.record()) != SATURN_OK) return s;
+      epoch.reset();
       if (sp->time_budget_s > 0) {
         // The stop decision must be collective: every island runs the same number of
         // epochs, or the elite all-gathers would mismatch.  MAX-all-reduce of the flag.
@@ -1266,7 +1291,9 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
       }
     }
   }
+  epoch.reset();
   const int64_t gens_run = gen - 1;
+  Nvtx r("saturn_search: final exchange");
   if ((s = exchange()) != SATURN_OK) return s;
   if ((s = is.record()) != SATURN_OK) return s;
   return is.finish(gens_run, is.evaluated * (uint64_t)is.world, out);
@@ -1385,10 +1412,12 @@ saturn_status saturn_improve(saturn_plan* p, uint8_t* h_cfg, uint8_t* h_perm, in
   CU(p, p->ws_perm.ensure((size_t)n * T));
   CU(p, cudaMemcpyAsync(p->ws_cfg.p, h_cfg, (size_t)n * T, cudaMemcpyHostToDevice, st));
   CU(p, cudaMemcpyAsync(p->ws_perm.p, h_perm, (size_t)n * T, cudaMemcpyHostToDevice, st));
-  CU(p, sat::launch_evaluate(p->pb, p->NN, p->GP, SATURN_DECODER_THREAD, p->ws_cfg.p, p->ws_perm.p, n, p->ls_ms.p,
+  int inn, igp;
+  run_shape(p, &inn, &igp);
+  CU(p, sat::launch_evaluate(p->pb, inn, igp, SATURN_DECODER_THREAD, p->ws_cfg.p, p->ws_perm.p, n, p->ls_ms.p,
                              p->sms, st));
   CU(p, cudaMemcpyAsync(p->ls_gen.p, packed.data(), packed.size(), cudaMemcpyHostToDevice, st));
-  CU(p, sat::launch_local_search(p->pb, p->NN, p->GP, p->ls_gen.p, p->ls_ms.p, (int)n, GS, iters, st));
+  CU(p, sat::launch_local_search(p->pb, inn, igp, p->ls_gen.p, p->ls_ms.p, (int)n, GS, iters, st));
   CU(p, cudaMemcpyAsync(packed.data(), p->ls_gen.p, packed.size(), cudaMemcpyDeviceToHost, st));
   CU(p, cudaMemcpyAsync(h_makespan, p->ls_ms.p, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CU(p, cudaStreamSynchronize(st));
@@ -1628,26 +1657,43 @@ saturn_status saturn_introspect(saturn_plan* p, const saturn_introspect_params* 
   if (!p) return SATURN_EINVAL;
   if (host_only(p)) return SATURN_ESTATE;
   if (!p->loaded) return fail(p, SATURN_ESTATE, "introspect before load_runtime_table");
-  if (!ip || ip->interval_s < 1 || ip->threshold_s < 0 || ip->max_rounds < 0)
+  if (!ip || ip->interval_s < 1 || ip->threshold_s < 0 || ip->max_rounds < 0 || ip->n_events < 0 ||
+      (ip->n_events > 0 && !ip->events))
     return fail(p, SATURN_EINVAL, "bad introspection parameters");
   if (ip->solver == SATURN_SOLVER_SEARCH && !ip->search) return fail(p, SATURN_EINVAL, "search params missing");
   const std::vector<int32_t> orig = p->dense;
   const int U = p->U, G = p->Gmax;
   const int64_t I = ip->interval_s, Tthr = ip->threshold_s;
+  const double wall_I = ip->interval_wall_s > 0 ? ip->interval_wall_s : (double)I;
+  for (int e = 0; e < ip->n_events; ++e) {
+    const saturn_introspect_event& ev = ip->events[e];
+    if (ev.at_round < 1 || (ev.kind != SATURN_EVENT_STOP && ev.kind != SATURN_EVENT_ARRIVE) ||
+        (ev.kind == SATURN_EVENT_ARRIVE && !ev.runtime_s))
+      return fail(p, SATURN_EINVAL, "bad introspection event %d", e);
+  }
   std::vector<int32_t> W = orig;
   int Tn = p->T;
+  std::vector<int> ids(Tn);   // original job id of every row of W
+  for (int t = 0; t < Tn; ++t) ids[t] = t;
+  int next_id = Tn;
   uint64_t evaluated = 0;
+  int solves = 0;
+  double solve_s = 0, exposed_s = 0;
   std::vector<saturn_placement> S;
   // solve the currently loaded workload -> S (placements, job-id order) and its makespan
-  auto solve = [&](std::vector<saturn_placement>& plan, int64_t& ms) -> saturn_status {
+  auto solve = [&](std::vector<saturn_placement>& plan, int64_t& ms, double* secs) -> saturn_status {
+    const double t0 = now_s();
     saturn_status st;
     saturn_result r;
     if (ip->solver == SATURN_SOLVER_ENUMERATE) st = saturn_enumerate(p, uint64_t(1) << 38, stream, &r);
     else st = saturn_search(p, ip->search, stream, &r);
     if (st != SATURN_OK) return st;
     evaluated += r.evaluated;
+    ++solves;
     plan.resize(p->T);
-    return saturn_best_plan(p, plan.data(), nullptr, &ms);
+    st = saturn_best_plan(p, plan.data(), nullptr, &ms);
+    if (secs) *secs = now_s() - t0;
+    return st;
   };
   auto restore = [&](saturn_status st) {
     const std::string keep = p->err;
@@ -1655,45 +1701,122 @@ saturn_status saturn_introspect(saturn_plan* p, const saturn_introspect_params* 
     if (st != SATURN_OK) p->err = keep;
     return st;
   };
-  int64_t M = 0;
-  saturn_status st = solve(S, M);
-  if (st != SATURN_OK) return restore(st);
-  const int64_t one_shot = M;
-  int64_t time = 0;
-  int rounds = 0, adopted = 0;
-  while (M > I && rounds < ip->max_rounds) {
-    // W after I seconds of S; S = S[I:]
-    std::vector<int32_t> W2;
-    std::vector<saturn_placement> S2;
-    for (int t = 0; t < Tn; ++t) {
-      const saturn_placement& pl = S[t];
+  // W after I seconds of S (residual runtimes, reading A10) and S[I:]; `keep` = surviving rows
+  auto advance = [&](const std::vector<int32_t>& Win, const std::vector<saturn_placement>& Sin,
+                     std::vector<int32_t>& Wout, std::vector<saturn_placement>& Sout, std::vector<int>* keep) {
+    Wout.clear();
+    Sout.clear();
+    if (keep) keep->clear();
+    for (size_t t = 0; t < Sin.size(); ++t) {
+      const saturn_placement& pl = Sin[t];
       if (pl.end_s <= I) continue;
-      const int32_t* row = &W[(size_t)t * U * G];
+      const int32_t* row = &Win[t * U * G];
       if (pl.start_s < I) {
         const int64_t R0 = pl.end_s - pl.start_s, a = I - pl.start_s;
         for (int k = 0; k < U * G; ++k)
-          W2.push_back(row[k] > 0 ? (int32_t)(((int64_t)row[k] * (R0 - a) + R0 - 1) / R0) : 0);
+          Wout.push_back(row[k] > 0 ? (int32_t)(((int64_t)row[k] * (R0 - a) + R0 - 1) / R0) : 0);
       } else {
-        W2.insert(W2.end(), row, row + U * G);
+        Wout.insert(Wout.end(), row, row + U * G);
       }
       saturn_placement q = pl;
       q.start_s = (int32_t)std::max<int64_t>(pl.start_s - I, 0);
       q.end_s = (int32_t)(pl.end_s - I);
-      S2.push_back(q);
+      Sout.push_back(q);
+      if (keep) keep->push_back((int)t);
     }
+  };
+  int64_t M = 0;
+  saturn_status st = solve(S, M, nullptr);
+  if (st != SATURN_OK) return restore(st);
+  const int64_t one_shot = M;
+  int64_t time = 0;
+  int rounds = 0, adopted = 0, stale = 0;
+  while (M > I && rounds < ip->max_rounds) {
+    Nvtx nr("saturn_introspect: round");
+    // overlap mode: round k+1's proposal from the simulated next-interval state, solved
+    // while round k runs (its latency hides behind the interval)
+    bool have_look = false;
+    std::vector<saturn_placement> Plook;
+    int64_t Mlook = 0;
+    double t_look = 0;
+    if (ip->overlap) {
+      std::vector<int32_t> Wn;
+      std::vector<saturn_placement> Sn;
+      advance(W, S, Wn, Sn, nullptr);
+      if (!Sn.empty()) {
+        st = saturn_load_runtime_table(p, Wn.data(), (int32_t)Sn.size(), U, G);
+        if (st != SATURN_OK) return restore(st);
+        st = solve(Plook, Mlook, &t_look);
+        if (st != SATURN_OK) return restore(st);
+        have_look = true;
+        solve_s += t_look;
+        exposed_s += std::max(0.0, t_look - wall_I);
+      }
+    }
+    std::vector<int32_t> W2;
+    std::vector<saturn_placement> S2;
+    std::vector<int> keep;
+    advance(W, S, W2, S2, &keep);
     W.swap(W2);
     S.swap(S2);
-    Tn = (int)S.size();
+    {
+      std::vector<int> ids2;
+      for (int k : keep) ids2.push_back(ids[k]);
+      ids.swap(ids2);
+    }
     M -= I;
     time += I;
     ++rounds;
-    st = saturn_load_runtime_table(p, W.data(), Tn, U, G);
-    if (st != SATURN_OK) return restore(st);
+    // events due at this boundary
+    bool fired = false, arrived = false;
+    for (int e = 0; e < ip->n_events; ++e) {
+      const saturn_introspect_event& ev = ip->events[e];
+      if (ev.at_round != rounds) continue;
+      fired = true;
+      if (ev.kind == SATURN_EVENT_STOP) {
+        const auto it = std::find(ids.begin(), ids.end(), ev.job);
+        if (it == ids.end()) {
+          restore(SATURN_OK);
+          return fail(p, SATURN_EINVAL, "stop event at round %d names job %d, finished or unknown", rounds, ev.job);
+        }
+        const size_t k = (size_t)(it - ids.begin());
+        W.erase(W.begin() + k * U * G, W.begin() + (k + 1) * U * G);
+        S.erase(S.begin() + k);
+        ids.erase(it);
+      } else {
+        W.insert(W.end(), ev.runtime_s, ev.runtime_s + (size_t)U * G);
+        ids.push_back(next_id++);
+        arrived = true;
+      }
+    }
+    if (fired) {
+      stale += have_look ? 1 : 0;
+      have_look = false;
+      M = 0;
+      for (const auto& q : S) M = std::max<int64_t>(M, q.end_s);
+    }
+    Tn = (int)ids.size();
+    if (Tn == 0) {   // every job stopped: the workload is exhausted
+      M = 0;
+      if (round_log)
+        for (int k = 0; k < 4; ++k) round_log[4 * (rounds - 1) + k] = k == 0 ? time : 0;
+      break;
+    }
     std::vector<saturn_placement> P;
     int64_t Mp = 0;
-    st = solve(P, Mp);
-    if (st != SATURN_OK) return restore(st);
-    const bool take = Mp <= M - Tthr;
+    if (have_look) {
+      P.swap(Plook);
+      Mp = Mlook;
+    } else {
+      st = saturn_load_runtime_table(p, W.data(), Tn, U, G);
+      if (st != SATURN_OK) return restore(st);
+      double t_fresh = 0;
+      st = solve(P, Mp, &t_fresh);
+      if (st != SATURN_OK) return restore(st);
+      solve_s += t_fresh;
+      exposed_s += t_fresh;   // solved at the boundary: on the critical path
+    }
+    const bool take = arrived || Mp <= M - Tthr;
     if (round_log) {
       round_log[4 * (rounds - 1) + 0] = time;
       round_log[4 * (rounds - 1) + 1] = M;
@@ -1709,11 +1832,16 @@ saturn_status saturn_introspect(saturn_plan* p, const saturn_introspect_params* 
   st = restore(SATURN_OK);
   if (st != SATURN_OK) return st;
   if (out) {
+    memset(out, 0, sizeof *out);
     out->one_shot_makespan = one_shot;
     out->e2e_makespan = time + M;
     out->rounds = rounds;
     out->adopted = adopted;
     out->evaluated = evaluated;
+    out->stale = stale;
+    out->solves = solves;
+    out->solve_s = solve_s;
+    out->exposed_solve_s = exposed_s;
   }
   return SATURN_OK;
 }

@@ -48,31 +48,6 @@ __device__ __forceinline__ int sel_fma(int p, int a, int b) {
   asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(p), "r"(d), "r"(a));
   return r;
 }
-// mux on the FMA pipe: a[k] via the same binary tree, each level a sel_fma on one bit of k.
-template <int GP>
-__device__ __forceinline__ int mux_fma(const int (&a)[GP], int k) {
-  if constexpr (GP == 1) {
-    return a[0];
-  } else {
-    int v[GP / 2];
-    const int p = k & 1;
-#pragma unroll
-    for (int i = 0; i < GP / 2; ++i) v[i] = sel_fma(p, a[2 * i], a[2 * i + 1]);
-    return mux_fma<GP / 2>(v, k >> 1);
-  }
-}
-#ifndef SAT_FMA_MUX
-#define SAT_FMA_MUX 0          // 1: multi-node starts by a mux tree on the FMA pipe (A/B)
-#endif
-#ifndef SAT_FMA_SEL_STAGES
-#define SAT_FMA_SEL_STAGES 8   // all barrel-shift stages (measured r1: +5 % TXT, +8 % MIX evaluate)
-#endif
-#ifndef SAT_INF_SEL
-#define SAT_INF_SEL 1          // lanes that shift in +inf use an ALU select (pipe balance)
-#endif
-#ifndef SAT_FMA_MULTI
-#define SAT_FMA_MULTI 0        // multi-node gather / scatter on the FMA pipe too
-#endif
 
 // In-place update of one node's sorted free-time vector after placing (g, R) at its
 // g-th smallest free time.  Returns s + R.
@@ -82,22 +57,19 @@ __device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R) {
   int b[GP];
 #pragma unroll
   for (int i = 0; i < GP; ++i) b[i] = x[i];
+  // Every stage on the FMA pipe (measured r1: +5 % TXT, +8 % MIX evaluate), except the lanes
+  // that shift in +inf: one ALU select beats two FMA-pipe ops there (pipe balance, +1.7 %).
   int stage = 0;
 #pragma unroll
   for (int sh = 1; sh < GP; sh <<= 1, ++stage) {
     const bool on = (k & sh) != 0;
-    if (stage >= (int)(__builtin_ctz(GP)) - SAT_FMA_SEL_STAGES) {
-      const int p = (k >> stage) & 1;
+    const int p = (k >> stage) & 1;
 #pragma unroll
-      for (int i = 0; i < GP; ++i) {
-        if (SAT_INF_SEL && i + sh >= GP)
-          b[i] = on ? INF : b[i];   // shifted-in +inf: one ALU select beats two FMA-pipe ops
-        else
-          b[i] = sel_fma(p, b[i], i + sh < GP ? b[i + sh] : INF);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < GP; ++i) b[i] = on ? (i + sh < GP ? b[i + sh] : INF) : b[i];
+    for (int i = 0; i < GP; ++i) {
+      if (i + sh >= GP)
+        b[i] = on ? INF : b[i];
+      else
+        b[i] = sel_fma(p, b[i], b[i + sh]);
     }
   }
   const int s = b[0];
@@ -351,80 +323,6 @@ __device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ 
   }
   bad |= maxt >= T || minw == 0u;
   return bad ? -1 : ms;
-}
-
-// K genomes per thread, decoded in lock-step (same T): K independent dependency chains per
-// step give the scheduler instruction-level parallelism (register-resident designs only).
-template <int NN, int GP, int CHECK, int K, class G>
-__device__ __forceinline__ void decode_sorted_k(const uint32_t* __restrict__ tab, int stride, const G (&gen)[K],
-                                                int T, const Problem& pb, int (&out)[K]) {
-  int a[K][NN][GP];
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int n = 0; n < NN; ++n)
-#pragma unroll
-      for (int i = 0; i < GP; ++i) a[k][n][i] = (n < pb.N && i < pb.gpu_n[n]) ? 0 : INF;
-  int maxt[K], ms[K];
-  uint32_t seen[K], minw[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) { maxt[k] = 0; ms[k] = 0; seen[k] = 0u; minw[k] = 0xffffffffu; }
-  for (int p = 0; p < T; ++p) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      int t = gen[k].perm(p);
-      int c;
-      if constexpr (CHECK != 0) {
-        maxt[k] = max(maxt[k], t);
-        t = min(t, T - 1);
-        seen[k] |= 1u << t;
-        c = min(gen[k].cfg(t), stride - 1);
-      } else {
-        c = gen[k].cfg(t);
-      }
-      const uint32_t w = tab[t * stride + c];
-      if constexpr (CHECK != 0) minw[k] = min(minw[k], w);
-      const int g = (int)(w >> 24);
-      const int R = (int)(w & R_MASK);
-      int v;
-      if constexpr (NN == 1) {
-        v = place_sorted<GP>(a[k][0], g, R);
-      } else {
-        int best = mux<GP>(a[k][0], g - 1);
-        int bn = 0;
-#pragma unroll
-        for (int n = 1; n < NN; ++n) {
-          const int st = mux<GP>(a[k][n], g - 1);
-          const bool lt = st < best;
-          best = lt ? st : best;
-          bn = lt ? n : bn;
-        }
-        int x[GP];
-#pragma unroll
-        for (int i = 0; i < GP; ++i) {
-          int y = a[k][0][i];
-#pragma unroll
-          for (int n = 1; n < NN; ++n) y = (bn == n) ? a[k][n][i] : y;
-          x[i] = y;
-        }
-        v = place_sorted<GP>(x, g, R);
-#pragma unroll
-        for (int n = 0; n < NN; ++n)
-#pragma unroll
-          for (int i = 0; i < GP; ++i) a[k][n][i] = (bn == n) ? x[i] : a[k][n][i];
-      }
-      ms[k] = max(ms[k], v);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if constexpr (CHECK != 0) {
-      const bool bad = __popc(seen[k]) != T || maxt[k] >= T || minw[k] == 0u;
-      out[k] = bad ? -1 : ms[k];
-    } else {
-      out[k] = ms[k];
-    }
-  }
 }
 
 // Thread-private node-state stride (words) for decode_smem: >= N * GP words and 4 x odd,

@@ -21,11 +21,7 @@ namespace sat {
 #define SAT_EVAL_B 128
 #endif
 constexpr int EVAL_B = SAT_EVAL_B;  // threads of the evaluate kernel
-#ifndef SAT_EVAL_X
-#define SAT_EVAL_X 1          // genomes per thread in k_evaluate (register designs, T <= 32)
-#endif
-constexpr int EVAL_X = SAT_EVAL_X;
-constexpr int EVAL_TILE = EVAL_B * EVAL_X;  // genomes per tile
+constexpr int EVAL_TILE = EVAL_B;  // genomes per tile (one per thread; 2 per thread measured no gain, r1)
 constexpr int ENUM_B = 128;
 constexpr int GA_B = 128;
 constexpr int WARP_B = 128;
@@ -168,32 +164,11 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
         bulk_g2s(nc + tileB, gperm + nt * tileB, tileB, &bars[buf ^ 1]);
       }
     }
-    if constexpr (EVAL_X > 1 && NN >= 1) {
-      if (T <= 32) {
-        RowGenome gens[EVAL_X];
-        int res[EVAL_X];
-#pragma unroll
-        for (int k = 0; k < EVAL_X; ++k) {
-          const int j = tid + k * EVAL_B;
-          const int jj = (first + j < n) ? j : tid;   // dead lanes decode a live genome, result dropped
-          gens[k] = RowGenome{bc + jj * T, bp + jj * T};
-        }
-        decode_sorted_k<NN, GP, 1, EVAL_X>(tab, pb.stride, gens, T, pb, res);
-#pragma unroll
-        for (int k = 0; k < EVAL_X; ++k)
-          if (first + tid + k * EVAL_B < n) out[first + tid + k * EVAL_B] = res[k];
-        __syncthreads();
-        continue;
-      }
-    }
-    for (int k = 0; k < EVAL_X; ++k) {
-      const int j = tid + k * EVAL_B;
-      if (first + j < n) {
-        RowGenome gen{bc + j * T, bp + j * T};
-        int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
-        out[first + j] = (T <= 32) ? decode_T<NN, GP, 1, true>(tab, S, pb.stride, gen, T, pb, ns)
+    if (first + tid < n) {
+      RowGenome gen{bc + tid * T, bp + tid * T};
+      int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+      out[first + tid] = (T <= 32) ? decode_T<NN, GP, 1, true>(tab, S, pb.stride, gen, T, pb, ns)
                                    : decode_T<NN, GP, 2, true>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
-      }
     }
     __syncthreads();
     if (nbuf == 1 && tid == 0) {  // one buffer: the next tile's copy starts once it is free
@@ -559,8 +534,7 @@ __device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R) {
 template <int NN, int GP>
 __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds, uint64_t root_begin,
                                                          uint64_t root_end, unsigned long long* best_key,
-                                                         unsigned long long* leaves_out,
-                                                         unsigned long long* work) {
+                                                         unsigned long long* leaves_out) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint8_t* s_blob = sm;
   int* s_lv = reinterpret_cast<int*>(sm + pb.blob_bytes);
@@ -577,22 +551,10 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
   const uint64_t C = ds.es.cfg_space;
 
   uint64_t best = ~0ull, leaves = 0;
-  // Roots: pruning makes subtree sizes very uneven, so with `work` each thread takes a first
-  // batch of DFS_BATCH roots by its position and then claims further batches from the
-  // counter as it finishes (dynamic); without it, the static grid stride.
+  // Roots by the static grid stride (dynamic batches measured slower, r1: see api.cu).
   const uint64_t nthr = (uint64_t)gridDim.x * DFS_B;
   const uint64_t gtid = (uint64_t)blockIdx.x * DFS_B + tid;
-  uint64_t batch_end = work ? min(root_begin + (gtid + 1) * DFS_BATCH, root_end) : root_begin + gtid + 1;
-  for (uint64_t root = work ? root_begin + gtid * DFS_BATCH : root_begin + gtid;; ++root) {
-    if (root >= batch_end) {
-      if (work) {
-        root = root_begin + nthr * DFS_BATCH + atomicAdd(work, (unsigned long long)DFS_BATCH);
-        batch_end = min(root + DFS_BATCH, root_end);
-      } else {
-        root = batch_end - 1 + nthr;
-        batch_end = root + 1;
-      }
-    }
+  for (uint64_t root = root_begin + gtid;; root += nthr) {
     if (root >= root_end) break;
     const int inc = (int)(*reinterpret_cast<volatile unsigned long long*>(best_key) >> 38);
     const int inc_ms = min(inc, (int)(best >> 38));
@@ -725,7 +687,7 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
 
 cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
                                  uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,
-                                 int sms, cudaStream_t st, unsigned long long* work) {
+                                 int sms, cudaStream_t st) {
   if (root_end <= root_begin) return cudaSuccess;
   const size_t smem = dfs_smem_bytes(pb, NN, GP);
   const uint64_t total = root_end - root_begin;
@@ -735,7 +697,7 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
     const int g0 = grid_for(k_enumerate_dfs<A_, b>, DFS_B, smem, sms, 1 << 30);                    \
     const uint64_t need = (total + DFS_B - 1) / DFS_B;                                             \
     const int g = (int)(need < (uint64_t)g0 ? need : (uint64_t)g0);                                \
-    k_enumerate_dfs<A_, b><<<g, DFS_B, smem, st>>>(pb, ds, root_begin, root_end, best_key, leaves, work); \
+    k_enumerate_dfs<A_, b><<<g, DFS_B, smem, st>>>(pb, ds, root_begin, root_end, best_key, leaves);       \
     return cudaGetLastError();                                                                     \
   }
   SAT_SHAPES(SAT_DFS)
@@ -1308,13 +1270,10 @@ __global__ void __launch_bounds__(32) k_select_warp(const unsigned long long* __
   }
   if (lane == 0) { n_cand[0] = 0; n_cand[1] = 0; }
 }
-#ifndef SAT_SELECT_WARP
-#define SAT_SELECT_WARP 1
-#endif
 
 cudaError_t launch_select(const unsigned long long* cand, int* n_cand, int E, int GS, const uint8_t* pop,
                           int32_t* rec_ms, uint8_t* rec_gen, cudaStream_t st, bool few) {
-  if (SAT_SELECT_WARP && few)
+  if (few)
     k_select_warp<<<1, 32, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);
   else
     k_select<<<1, 1024, 0, st>>>(cand, n_cand, E, GS, pop, rec_ms, rec_gen);

@@ -54,8 +54,7 @@ struct DfsSpace {
 };
 cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpace& ds, uint64_t root_begin,
                                  uint64_t root_end, unsigned long long* best_key, unsigned long long* leaves,
-                                 int sms, cudaStream_t st,
-                                 unsigned long long* work = nullptr);
+                                 int sms, cudaStream_t st);
 
 struct GaParams {
   uint64_t seed;

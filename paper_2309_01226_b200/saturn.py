@@ -21,7 +21,7 @@ OK, EINVAL, EUNSCHEDULABLE, ELIMIT, ECUDA, ENCCL, ESTATE = range(7)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EUNSCHEDULABLE", 3: "ELIMIT", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE"}
 PROVEN_OPTIMAL, INCUMBENT, PREFIX_SHARED, SYMMETRY_REDUCED = 1, 2, 4, 8
 ENUM_SYMMETRY = 1
-DECODER_AUTO, DECODER_THREAD, DECODER_WARP = 0, 1, 2
+DECODER_AUTO, DECODER_THREAD, DECODER_WARP, DECODER_NODE_SMEM = 0, 1, 2, 3
 
 # Every symbol declared in include/saturn.h.
 EXPORTS = (
@@ -71,14 +71,24 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
 
 
+class IntrospectEvent(ctypes.Structure):
+    _fields_ = [("at_round", ctypes.c_int32), ("kind", ctypes.c_int32), ("job", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("runtime_s", ctypes.c_void_p)]
+
+
+EVENT_STOP, EVENT_ARRIVE = 1, 2
+
+
 class IntrospectParams(ctypes.Structure):
     _fields_ = [("interval_s", ctypes.c_int64), ("threshold_s", ctypes.c_int64), ("solver", ctypes.c_int32),
-                ("max_rounds", ctypes.c_int32), ("search", ctypes.c_void_p)]
+                ("max_rounds", ctypes.c_int32), ("search", ctypes.c_void_p), ("overlap", ctypes.c_int32),
+                ("n_events", ctypes.c_int32), ("events", ctypes.c_void_p), ("interval_wall_s", ctypes.c_double)]
 
 
 class IntrospectResult(ctypes.Structure):
     _fields_ = [("one_shot_makespan", ctypes.c_int64), ("e2e_makespan", ctypes.c_int64), ("rounds", ctypes.c_int32),
-                ("adopted", ctypes.c_int32), ("evaluated", ctypes.c_uint64)]
+                ("adopted", ctypes.c_int32), ("evaluated", ctypes.c_uint64), ("stale", ctypes.c_int32),
+                ("solves", ctypes.c_int32), ("solve_s", ctypes.c_double), ("exposed_solve_s", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -367,13 +377,31 @@ class Plan:
                             local_search_iters=cfg.local_search_iters)
 
     def introspect(self, interval_s: int = 1000, threshold_s: int = 500, solver: str = "search",
-                   search: SearchConfig | None = None, max_rounds: int = 100000, stream=None):
-        """Round introspection (row f1) on the loaded workload; -> (result dict, round log)."""
+                   search: SearchConfig | None = None, max_rounds: int = 100000, stream=None,
+                   overlap: bool = False, events=None, interval_wall_s: float = 0.0):
+        """Round introspection (row f1) on the loaded workload; -> (result dict, round log).
+        events: [(at_round, "stop", job_id) | (at_round, "arrive", runtime row [U][Gmax])]."""
         sp = self._search_params(search or SearchConfig())
         cap = min(int(max_rounds), 1 << 16)
+        evs = list(events or [])
+        arr = (IntrospectEvent * max(len(evs), 1))()
+        rows = []
+        for k in range(len(evs)):          # (module-level enumerate() shadows the builtin)
+            r, kind, arg = evs[k]
+            arr[k].at_round = int(r)
+            if kind == "stop":
+                arr[k].kind, arr[k].job = EVENT_STOP, int(arg)
+            elif kind == "arrive":
+                row = np.ascontiguousarray(arg, dtype=np.int32)
+                rows.append(row)
+                arr[k].kind, arr[k].runtime_s = EVENT_ARRIVE, row.ctypes.data
+            else:
+                raise ValueError(kind)
         ip = IntrospectParams(interval_s=int(interval_s), threshold_s=int(threshold_s),
                               solver={"search": 0, "enumerate": 1}[solver], max_rounds=cap,
-                              search=ctypes.cast(ctypes.pointer(sp), ctypes.c_void_p))
+                              search=ctypes.cast(ctypes.pointer(sp), ctypes.c_void_p), overlap=int(bool(overlap)),
+                              n_events=len(evs), events=ctypes.cast(arr, ctypes.c_void_p) if evs else None,
+                              interval_wall_s=float(interval_wall_s))
         r = IntrospectResult()
         log = np.zeros((cap, 4), np.int64)
         self._check(self._lib.saturn_introspect(self._h, ctypes.byref(ip), self._stream(stream), ctypes.byref(r),

@@ -310,16 +310,23 @@ def test_nccl_single_rank_communicator_path(sat, torch):
     assert (a.search_population(4096)[0] == b.search_population(4096)[0]).all()
 
 
-def test_multinode_shared_memory_decoder(sat, torch, monkeypatch):
+def test_multinode_shared_memory_decoder(sat, torch):
     """The NN = 0 decoder (node vectors in shared memory, runtime node count): the default
-    for node counts without a compiled register shape, forced here on every multi-node case."""
-    monkeypatch.setenv("SATURN_MULTINODE_SMEM", "1")
+    for node counts without a compiled register shape, selected here (SATURN_DECODER_NODE_SMEM)
+    on every multi-node case and on one node."""
     for inst in (synth.mix(2), synth.sweep(2), synth.sweep(5, n_jobs=20, nodes=[2, 2, 4, 8]),
-                 synth.sweep(6, n_jobs=16, nodes=[4] * 8)):
+                 synth.sweep(6, n_jobs=16, nodes=[4] * 8), synth.txt(4)):
         c = oracle.compact(inst.node_gpus, inst.runtime)
         plan = _plan(sat, inst)
+        plan.set_decoder(sat.DECODER_NODE_SMEM)
         cfg, perm = synth.random_genomes(c.S, 3001, seed=8)
         assert np.array_equal(_ms(plan, torch, cfg, perm), oracle.decode_batch(c, cfg, perm))
+    tv = synth.tiny_variant(3, 5, (2, 2))   # index-order enumeration on the smem shape = brute force
+    ct = oracle.compact(tv.node_gpus, tv.runtime)
+    tp = _plan(sat, tv)
+    tp.set_decoder(sat.DECODER_NODE_SMEM)
+    r = tp.enumerate()
+    assert (r["makespan"], r["genome_index"]) == oracle.brute_force(ct)
     inst = synth.mix(1)
     c = oracle.compact(inst.node_gpus, inst.runtime)
     P, E, seed = 128, 4, 77
@@ -327,6 +334,7 @@ def test_multinode_shared_memory_decoder(sat, torch, monkeypatch):
     ms = oracle.decode_batch(c, cfg, perm)
     rc, rq, _ = oga.next_generation(c.S, cfg, perm, ms, 1, seed, 0, E, oga.q32(0.9), oga.q32(0.5), oga.q32(0.5))
     plan = _plan(sat, inst)
+    plan.set_decoder(sat.DECODER_NODE_SMEM)
     plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=1, elites=E, generations_per_epoch=1,
                                  p_xover=0.9, p_cfg_mut=0.5, p_perm_mut=0.5))
     gc, gq, gm = plan.search_population(P)

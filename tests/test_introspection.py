@@ -79,3 +79,90 @@ def test_library_introspection_matches_oracle():
                                search=sat.SearchConfig(seed=1, population=1 << 14, max_generations=20, elites=8,
                                                        generations_per_epoch=5))
     assert got["e2e_makespan"] <= got["one_shot_makespan"] and got["rounds"] == len(log) > 5
+
+
+# ------------------------------------------------------------------ events and overlap mode
+def test_early_stop_of_critical_task_shortens_makespan():
+    """early-stop of the longest task at round 1 -> strictly smaller makespan
+    than without the event, on a 2-task instance.  1 x 2 GPUs, A (1 GPU, 20 s), B (1 GPU, 6 s),
+    I = 5: A is critical (20); stopping it at t = 5 leaves B, which ends at 6."""
+    table = dense_from_single([(1, 20), (1, 6)])
+    base = oi.introspect([2], table, I=5, T=0)
+    assert base["e2e"] == 20
+    stop = oi.introspect([2], table, I=5, T=0, events=[(1, "stop", 0)])
+    assert stop["e2e"] == 6 < base["e2e"]
+
+
+def test_arrival_is_scheduled_and_adopted():
+    """A job arriving at round 1 joins the workload; the round's proposal (which holds it) is
+    adopted unconditionally, even with an infinite threshold."""
+    table = dense_from_single([(1, 8), (1, 8)])
+    arr = np.zeros((1, 1), np.int32)
+    arr[0, 0] = 4                                   # (1 GPU, 4 s)
+    r = oi.introspect([2], table, I=4, T=10 ** 6, events=[(1, "arrive", arr)])
+    assert r["adopted"] == 1 and r["log"][0][3] == 1
+    assert r["e2e"] == 4 + 8                        # at t = 4: A, B have 4 s left, C needs 4 s: 8 on 2 GPUs
+    with pytest.raises(ValueError):
+        oi.introspect([2], table, I=4, T=0, events=[(1, "stop", 7)])
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_overlap_mode_equals_sequential(seed):
+    """with no events overlap on/off produce identical schedules; an event at
+    a boundary makes the precomputed proposal stale (fresh solve) and the result still
+    equals the sequential loop's."""
+    rng = np.random.default_rng(50 + seed)
+    inst = synth.random_tiny(rng, max_jobs=4, node_choices=([2], [3], [2, 2]), max_r=9)
+    for I, T in ((2, 0), (3, 1)):
+        a = oi.introspect(inst.node_gpus, inst.runtime, I=I, T=T)
+        b = oi.introspect(inst.node_gpus, inst.runtime, I=I, T=T, overlap=True)
+        assert (a["e2e"], a["log"], a["adopted"]) == (b["e2e"], b["log"], b["adopted"]) and b["stale"] == 0
+        if a["rounds"] >= 1:
+            ev = [(1, "stop", int(np.argmax([1] * inst.n_jobs)))]
+            try:
+                a2 = oi.introspect(inst.node_gpus, inst.runtime, I=I, T=T, events=ev)
+            except ValueError:
+                continue                            # job 0 already finished by round 1
+            b2 = oi.introspect(inst.node_gpus, inst.runtime, I=I, T=T, events=ev, overlap=True)
+            assert (a2["e2e"], a2["log"]) == (b2["e2e"], b2["log"]) and b2["stale"] == 1
+
+
+@pytest.mark.gpu
+def test_library_events_and_overlap_match_oracle():
+    """saturn_introspect with STOP / ARRIVE events and overlap mode (exact solver) reproduces
+    the oracle round by round; overlap leaves the schedule unchanged, counts stale proposals,
+    and with the GA solver its latency is hidden behind the interval (exposed < sequential)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2309_01226_b200 as sat
+    n = 0
+    for seed in range(10):
+        rng = np.random.default_rng(700 + seed)
+        inst = synth.random_tiny(rng, max_jobs=4, node_choices=([2], [3], [2, 2]), max_r=12)
+        arr = np.zeros_like(inst.runtime[0])
+        arr[0, 0] = 3
+        for I, T in ((3, 0), (4, 2)):
+            for events in ([], [(1, "stop", 0)], [(1, "arrive", arr)], [(1, "arrive", arr), (2, "stop", 1)]):
+                try:
+                    ref = oi.introspect(inst.node_gpus, inst.runtime, I=I, T=T, events=events)
+                except ValueError:
+                    continue
+                for ov in (False, True):
+                    plan = sat.Plan(inst.node_gpus, 0).load_runtime_table(inst.runtime)
+                    got, log = plan.introspect(I, T, solver="enumerate", events=events, overlap=ov)
+                    assert (got["one_shot_makespan"], got["e2e_makespan"], got["rounds"], got["adopted"]) == \
+                        (ref["one_shot"], ref["e2e"], ref["rounds"], ref["adopted"]), (seed, I, T, events, ov)
+                    assert [tuple(x) for x in ref["log"]] == log
+                    if ov:
+                        refo = oi.introspect(inst.node_gpus, inst.runtime, I=I, T=T, events=events, overlap=True)
+                        assert got["stale"] == refo["stale"]
+                    n += got["rounds"]
+    assert n > 40
+    inst = synth.mix(0)
+    cfg = sat.SearchConfig(seed=1, population=1 << 14, max_generations=20, elites=8, generations_per_epoch=5)
+    plan = sat.Plan(inst.node_gpus, 0).load_runtime_table(inst.runtime)
+    seq, lseq = plan.introspect(1000, 500, search=cfg)
+    ovl, lovl = plan.introspect(1000, 500, search=cfg, overlap=True)
+    assert (seq["e2e_makespan"], lseq) == (ovl["e2e_makespan"], lovl)
+    assert ovl["exposed_solve_s"] == 0.0 < seq["exposed_solve_s"] and ovl["stale"] == 0
