@@ -281,18 +281,9 @@ void run_shape(const saturn_plan* p, int* nn, int* gp) {
   }
 }
 
-// Decoder shape for the evaluate kernel: 4-node register states (SWEEP 4x8) are ALU-bound on
-// their gather/scatter selects, and there the shared-memory node-state decoder (dynamic
-// indexing on the LSU pipe) measured faster: evaluate 1.15e9 -> 1.37e9 plans/s (its GA
-// kernel is slower, so k_ga keeps the register states).  MIX 2x8: equal -> registers.
-void eval_shape(const saturn_plan* p, int* nn, int* gp) {
-  run_shape(p, nn, gp);
-  if (*nn >= 4 && sat::have_sorted_shape(0, std::max(4, p->GP)) &&
-      sat::eval_smem_bytes(p->pb, 0, std::max(4, p->GP)) <= 227 * 1024) {
-    *nn = 0;
-    *gp = std::max(4, p->GP);
-  }
-}
+// Decoder shape for the evaluate kernel: the search-side shape (multi-node states are in
+// shared memory in every kernel since r2, so evaluate needs no shape of its own).
+void eval_shape(const saturn_plan* p, int* nn, int* gp) { run_shape(p, nn, gp); }
 
 bool host_only(saturn_plan* p) {
   if (p->device < 0) {

@@ -325,24 +325,28 @@ __device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ 
   return bad ? -1 : ms;
 }
 
-// Thread-private node-state stride (words) for decode_smem: >= N * GP words and 4 x odd,
-// so a quarter-warp's 16-byte accesses at the same offset hit 8 distinct bank groups.
-__host__ __device__ __forceinline__ int node_state_words(int N, int GP) {
-  int q = (N * GP + 3) / 4;
-  if ((q & 1) == 0) ++q;
-  return 4 * q;
+// Column node states (decode_col): node n's sorted slot j of thread `tid` is the word
+// ns[(n * col_rows(GP) + j) * B + tid] of a block of B threads -- every thread's same slot in
+// one row, so any per-thread slot index is bank-conflict free.  Rows GP .. 2GP-2 of every
+// node are +inf padding: slot j + g (g <= GP, j <= GP-2) reads +inf past the node's GPUs.
+__host__ __device__ __forceinline__ constexpr int col_rows(int GP) { return 2 * GP - 1; }
+__host__ __device__ __forceinline__ size_t col_state_bytes(int N, int GP, int B) {
+  return (size_t)4 * N * col_rows(GP) * B;
 }
 
-// T design for multi-node clusters: each node's sorted free-time vector lives in this
-// thread's shared-memory slice `ns` (node n at ns[n * GP], 16-byte aligned), so the chosen
-// node is read and written with dynamic indexing (2 x GP/4 vector accesses) instead of
-// register gather/scatter selects over every node.  Starts: one load per node.
-template <int GP, int CHECK, class G>
-__device__ __forceinline__ int decode_smem(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
-                                           int stride, const G& gen, int T, const Problem& pb, int* ns,
-                                           uint32_t* mask = nullptr, int mstride = 0) {
-  static_assert(GP % 4 == 0, "vector node rows");
-  const int N = pb.N;
+// T design for multi-node clusters with the node states in shared memory, column layout
+// (above).  NN = node count at compile time (0: pb.N at run time).  `ns` = &state[tid].
+// Per job step: one load per node for the starts (slot g-1), a strict-< argmin, then the
+// chosen node's slots are read twice -- x[i] = slot i and the shifted b[i+1] = slot i+g
+// (the barrel shift of place_sorted done by the LSU's addressing instead of select stages)
+// -- and the update x'[i] = (b[i+1] <= s) ? x[i] : min(b[i+1], max(x[i], s+R)) is stored
+// back.  No gather/scatter selects, no shift stages, 8-slot register footprint.
+template <int NN, int GP, int B, int CHECK, class G>
+__device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
+                                          int stride, const G& gen, int T, const Problem& pb, int* ns,
+                                          uint32_t* mask = nullptr, int mstride = 0) {
+  constexpr int RW = col_rows(GP);
+  const int N = NN ? NN : pb.N;
   bool bad = false;
   int maxt = 0;
   uint32_t seen = 0u, minw = 0xffffffffu;
@@ -372,63 +376,80 @@ __device__ __forceinline__ int decode_smem(const uint32_t* __restrict__ tab, con
     if constexpr (CHECK != 0) minw = min(minw, w);
     return w;
   };
+  // the smallest start over the nodes for a g-GPU job (slot g-1 of every node), its node
+  const auto start_min = [&](int g, int& bn) -> int {
+    const int* cg = ns + (g - 1) * B;
+    int best = cg[0];
+    bn = 0;
+    if constexpr (NN > 0) {
+#pragma unroll
+      for (int n = 1; n < NN; ++n) {
+        const int st = cg[n * RW * B];
+        const bool lt = st < best;   // strict: ties keep the lowest node id
+        best = lt ? st : best;
+        bn = lt ? n : bn;
+      }
+    } else {
+      for (int n = 1; n < N; ++n) {
+        const int st = cg[n * RW * B];
+        const bool lt = st < best;
+        best = lt ? st : best;
+        bn = lt ? n : bn;
+      }
+    }
+    return best;
+  };
   // Position 0 in closed form (every GPU free at 0): the lowest node with >= g GPUs gets
-  // R in its top g free slots.
+  // R in its top g free slots; padding rows +inf.
   int ms;
   {
     const uint32_t w = fetch(0);
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
-    const uint8_t* G = G_of(S, pb);
+    const uint8_t* Gn = G_of(S, pb);
     int bn = N;
-    for (int n = N - 1; n >= 0; --n) bn = (g <= G[n]) ? n : bn;
+    for (int n = N - 1; n >= 0; --n) bn = (g <= Gn[n]) ? n : bn;
+#pragma unroll(NN > 0 ? NN : 1)
     for (int n = 0; n < N; ++n) {
-      int4* row = reinterpret_cast<int4*>(ns + n * GP);
-      const int gn = G[n];
+      const int gn = Gn[n];
       const int lo = (n == bn) ? gn - g : gn;
+      int* row = ns + n * RW * B;
 #pragma unroll
-      for (int j = 0; j < GP / 4; ++j) {
-        int q[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) q[e] = (4 * j + e < gn) ? ((4 * j + e >= lo) ? R : 0) : INF;
-        row[j] = make_int4(q[0], q[1], q[2], q[3]);
-      }
+      for (int j = 0; j < RW; ++j) row[j * B] = (j < gn) ? ((j >= lo) ? R : 0) : INF;
     }
     ms = R;
   }
+  uint32_t w = T > 1 ? fetch(1) : 0u;
   for (int p = 1; p < T - 1; ++p) {
-    const uint32_t w = fetch(p);
+    const uint32_t wn = fetch(p + 1);   // next position's word one step ahead
     const int g = (int)(w >> 24);
     const int R = (int)(w & R_MASK);
-    // start of every node (its g-th smallest free time; +inf padding if it has fewer GPUs)
-    int best = ns[g - 1];
-    int bn = 0;
-    for (int n = 1; n < N; ++n) {
-      const int st = ns[n * GP + g - 1];
-      const bool lt = st < best;  // strict: ties keep the lowest node id
-      best = lt ? st : best;
-      bn = lt ? n : bn;
-    }
-    int4* row = reinterpret_cast<int4*>(ns + bn * GP);
-    int x[GP];
+    int bn;
+    const int s = start_min(g, bn);
+    const int v = s + R;
+    int* row = ns + bn * RW * B;
+    const int* sh = row + g * B;   // sh[i * B] = slot i + g = b[i + 1]
+    int x[GP], y[GP];
 #pragma unroll
-    for (int j = 0; j < GP / 4; ++j) {
-      const int4 q = row[j];
-      x[4 * j] = q.x; x[4 * j + 1] = q.y; x[4 * j + 2] = q.z; x[4 * j + 3] = q.w;
-    }
-    const int v = place_sorted<GP>(x, g, R);
+    for (int i = 0; i < GP; ++i) x[i] = row[i * B];
 #pragma unroll
-    for (int j = 0; j < GP / 4; ++j) row[j] = make_int4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+    for (int i = 0; i + 1 < GP; ++i) y[i] = sh[i * B];
+#pragma unroll
+    for (int i = 0; i < GP; ++i) {
+      if (i + 1 < GP) {
+        const int merged = min(y[i], max(x[i], v));
+        row[i * B] = (y[i] <= s) ? x[i] : merged;
+      } else {
+        row[i * B] = max(x[i], v);
+      }
+    }
     ms = max(ms, v);
+    w = wn;
   }
-  // Position T-1: earliest start + R, no state update.
+  // Position T-1 (its word is in w): earliest start + R, no state update.
   if (T > 1) {
-    const uint32_t w = fetch(T - 1);
-    const int g = (int)(w >> 24);
-    const int R = (int)(w & R_MASK);
-    int best = ns[g - 1];
-    for (int n = 1; n < N; ++n) best = min(best, ns[n * GP + g - 1]);
-    ms = max(ms, best + R);
+    int bn;
+    ms = max(ms, start_min((int)(w >> 24), bn) + (int)(w & R_MASK));
   }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;
   if constexpr (CHECK != 0) {

@@ -27,25 +27,44 @@ constexpr int GA_B = 128;
 constexpr int WARP_B = 128;
 
 // ------------------------------------------------------------------ shapes
-// (NN, GP): NN >= 1 keeps NN nodes' sorted vectors in registers (decode_sorted); NN == 0 is
-// the multi-node path with node vectors in shared memory and a runtime node count
-// (decode_smem).  GP = GPUs per node padded to a power of two.
+// (NN, GP): NN nodes (NN == 0: a run-time node count) of GP GPUs (padded to a power of two).
+// One node keeps its sorted vector in registers (decode_sorted); several nodes keep theirs in
+// shared memory (decode_col).
 #define SAT_SHAPES(X) \
   X(1, 2) X(1, 4) X(1, 8) X(1, 16) X(1, 32) X(2, 2) X(2, 4) X(2, 8) X(4, 2) X(4, 4) X(4, 8) \
   X(0, 4) X(0, 8) X(0, 16) X(0, 32)
 
-// Shared-memory bytes of the NN == 0 node states for a block of B threads.
-__host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, int NN, int GP, int B) {
-  return NN == 0 ? (size_t)4 * node_state_words(pb.N, GP) * B : 0;
+// Node-state design per kernel (measured r2 on one B200):
+//  * registers (decode_sorted: sorted vectors in registers, barrel shift by select stages,
+//    multi-node gather/scatter selects), or
+//  * columns (decode_col: states in shared memory, one row per slot, shifted reads).
+// Evaluate-type kernels (evaluate, index-order enumeration, local search) decode with the
+// column states on every shape: TXT +10 %, MIX 2x8 +33 %, SWEEP 4x8 +34 % plans/s over the
+// best register / row-layout shared-memory design -- except small single nodes (TINY 1x4,
+// T = 3: registers 1.44e11 vs columns 1.30e11; the column init costs more than 1-2 steps
+// save).  The GA kernel also holds a child row,
+// Philox state and the tournament prefetch: there columns win on 16-slot states (MIX k_ga
+// -4 %) but lose on one node (TXT +5.5 %) and on 32-slot states (SWEEP +37 %: 30 KB more
+// shared memory per CTA, 3 instead of 4 CTAs per SM).  NN == 0 (run-time node count) is
+// columns only.
+__host__ __device__ __forceinline__ constexpr bool eval_col(int NN, int GP) { return NN != 1 || GP >= 8; }
+__host__ __device__ __forceinline__ constexpr bool ga_col(int NN, int GP) {
+  return NN == 0 || (NN >= 2 && NN * GP <= 16);
+}
+// Shared-memory bytes of the column node states for a block of B threads (0: registers).
+__host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, bool col, int NN, int GP, int B) {
+  return col ? col_state_bytes(NN ? NN : pb.N, GP, B) : 0;
 }
 
 // Decode one genome with the (NN, GP) design; `ns` = this thread's node-state slice (NN == 0).
 // STATE_MS: allow reading the makespan off the final state for one full node (decode_sorted);
 // only the evaluate kernel uses it -- in k_ga the extra loop copy measured 3 % slower.
-template <int NN, int GP, int CHECK, bool STATE_MS = false, class G>
+// COL: column states, `ns` = &state[threadIdx.x] of a block of B threads; else registers.
+template <int NN, int GP, int B, bool COL, int CHECK, bool STATE_MS = false, class G>
 __device__ __forceinline__ int decode_T(const uint32_t* tab, const uint8_t* S, int stride, const G& gen, int T,
                                         const Problem& pb, int* ns, uint32_t* mask = nullptr, int mstride = 0) {
-  if constexpr (NN == 0) return decode_smem<GP, CHECK>(tab, S, stride, gen, T, pb, ns, mask, mstride);
+  static_assert(COL || NN >= 1, "a run-time node count needs the column states");
+  if constexpr (COL) return decode_col<NN, GP, B, CHECK>(tab, S, stride, gen, T, pb, ns, mask, mstride);
   else if constexpr (STATE_MS) return decode_sorted<NN, GP, CHECK>(tab, S, stride, gen, T, pb, mask, mstride);
   else return decode_sorted_impl<NN, GP, CHECK, true>(tab, S, stride, gen, T, pb, mask, mstride);
 }
@@ -98,7 +117,7 @@ __device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E, 
 #endif
 __host__ __device__ __forceinline__ int eval_nbuf(int T) { return 4 * EVAL_TILE * T <= SAT_EVAL_DB_LIMIT ? 2 : 1; }
 size_t eval_smem_bytes(const Problem& pb, int NN, int GP) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B) + 2u * eval_nbuf(pb.T) * EVAL_TILE * pb.T +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, EVAL_B) + 2u * eval_nbuf(pb.T) * EVAL_TILE * pb.T +
          4u * EVAL_B * ((pb.T + 31) / 32) + 3 * 8;
 }
 
@@ -112,7 +131,7 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   const int nbuf = eval_nbuf(T);
-  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, EVAL_B);   // [nbuf buffers][cfg | perm]
+  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, EVAL_B);   // [nbuf buffers][cfg | perm]
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 2 * nbuf * tileB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_mask + EVAL_B * ((T + 31) / 32));
   const int64_t ntiles = (n + EVAL_TILE - 1) / EVAL_TILE;
@@ -166,9 +185,9 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     }
     if (first + tid < n) {
       RowGenome gen{bc + tid * T, bp + tid * T};
-      int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
-      out[first + tid] = (T <= 32) ? decode_T<NN, GP, 1, true>(tab, S, pb.stride, gen, T, pb, ns)
-                                   : decode_T<NN, GP, 2, true>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
+      int* ns = s_ns + tid;
+      out[first + tid] = (T <= 32) ? decode_T<NN, GP, EVAL_B, eval_col(NN, GP), 1, true>(tab, S, pb.stride, gen, T, pb, ns)
+                                   : decode_T<NN, GP, EVAL_B, eval_col(NN, GP), 2, true>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
     }
     __syncthreads();
     if (nbuf == 1 && tid == 0) {  // one buffer: the next tile's copy starts once it is free
@@ -375,7 +394,7 @@ cudaError_t launch_evaluate_nodes(const Problem& pb, int NN, int GP, const uint8
 // Consecutive indices advance cfg like an odometer (job 0 fastest), then perm by
 // next_permutation, so only the first index of a chunk is unranked.
 static size_t enum_smem_bytes(const Problem& pb, int NN, int GP) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, ENUM_B) + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, ENUM_B) + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) +
          32 * 8 + 8;
 }
 
@@ -385,7 +404,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
   extern __shared__ __align__(16) uint8_t sm[];
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_gen = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, ENUM_B);
+  uint8_t* s_gen = sm + pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, ENUM_B);
   const int T = pb.T;
   const int RS = odd_row_stride(perm_offset(T) + T);
   uint64_t* s_red = reinterpret_cast<uint64_t*>(s_gen + ((ENUM_B * RS + 7) & ~7));
@@ -419,8 +438,8 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
       gen.q(p) = (uint8_t)x;
     }
     for (uint64_t idx = i0; idx < i1; ++idx) {
-      const int ms = decode_T<NN, GP, 0>(tab, S, pb.stride, gen, T, pb,
-                                         s_ns + (NN == 0 ? node_state_words(pb.N, GP) * threadIdx.x : 0));
+      const int ms = decode_T<NN, GP, ENUM_B, eval_col(NN, GP), 0>(tab, S, pb.stride, gen, T, pb,
+                                         s_ns + threadIdx.x);
       const uint64_t key = ((uint64_t)ms << 38) | idx;
       best = key < best ? key : best;
       // odometer over cfg (job 0 least significant), carry into perm
@@ -716,7 +735,7 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
 // (ceil(T/32) words per thread, interleaved).  The init kernel keeps one row.
 __host__ __device__ __forceinline__ int ga_rows(int T, bool init) { return (init || T > 32) ? 1 : 3; }
 static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS, bool init) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B) + (size_t)ga_rows(pb.T, init) * GA_B * odd_row_stride(GS) +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B) + (size_t)ga_rows(pb.T, init) * GA_B * odd_row_stride(GS) +
          (size_t)4 * ((pb.T + 31) / 32) * GA_B + 8 * GA_B + 8;
 }
 
@@ -801,7 +820,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   const int T = pb.T, GS = gp.GS, RS = odd_row_stride(GS), Tp = perm_offset(T);
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
+  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B);
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);
   uint64_t* bar = s_lists + GA_B;
@@ -810,7 +829,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   const uint8_t* S = S_of(s_blob, pb);
   const int tid = threadIdx.x, lane = tid & 31;
   const RowG ch{s_rows + RS * tid, Tp};
-  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  int* ns = s_ns + tid;
   uint64_t lst = ~0ull;
   WarpChunks wc(n_cand, (int64_t)gridDim.x * GA_B, lane);
   for (int64_t base = (int64_t)blockIdx.x * GA_B + (tid & ~31); base < gp.P; base = wc.advance()) {
@@ -832,7 +851,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           ch.q(j) = a;
         }
       }
-      msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      msv = decode_T<NN, GP, GA_B, ga_col(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
       store_row(pop + slot * GS, ch.base, GS);
       ms_out[slot] = msv;
     }
@@ -853,7 +872,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   constexpr int ROWS = LONGT ? 1 : 3;
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, GA_B);
+  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B);
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + ROWS * GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);
   uint64_t* bar = s_lists + GA_B;
@@ -869,7 +888,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   const uint32_t NP = (P + 1) >> 1;
   const int nb = (T + 31) / 32;
   const int nw = (T + 3) >> 2;
-  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  int* ns = s_ns + tid;
   const uint32_t px16 = gp.px >> 16, pc16 = gp.pc >> 16, pm16 = gp.pm >> 16;
   const uint32_t k0 = (uint32_t)gp.seed, k1 = (uint32_t)(gp.seed >> 32), c2 = gp.rank << 16;
 
@@ -1018,7 +1037,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           ch.q(mj) = xi;
         }
       }
-      if (child) msv = decode_T<NN, GP, 0>(tab, S, pb.stride, ch, T, pb, ns);
+      if (child) msv = decode_T<NN, GP, GA_B, ga_col(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
       if (in) {
         store_row(pop + (size_t)slot * GS, ch.base, GS);
         ms_out[slot] = msv;
@@ -1100,7 +1119,7 @@ cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaPara
 // strict improvement, up to `iters` times.  Records are updated in place.
 constexpr int LS_B = 128;
 static size_t ls_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, NN, GP, LS_B) + (size_t)(LS_B + 1) * odd_row_stride(GS) +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, LS_B) + (size_t)(LS_B + 1) * odd_row_stride(GS) +
          (size_t)4 * (pb.T + 1) + 8 * (LS_B / 32) + 16 + 8;
 }
 
@@ -1111,7 +1130,7 @@ __global__ void __launch_bounds__(LS_B) k_local_search(Problem pb, uint8_t* __re
   const int T = pb.T, Tp = perm_offset(T), RS = odd_row_stride(GS);
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_base = sm + pb.blob_bytes + ns_bytes(pb, NN, GP, LS_B);
+  uint8_t* s_base = sm + pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, LS_B);
   uint8_t* s_rows = s_base + RS;
   int* s_pre = reinterpret_cast<int*>(s_rows + LS_B * RS);       // prefix of (S_t - 1), T + 1 entries
   uint64_t* s_red = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_pre + T + 1) + 7) & ~uintptr_t(7));
@@ -1130,7 +1149,7 @@ __global__ void __launch_bounds__(LS_B) k_local_search(Problem pb, uint8_t* __re
   }
   __syncthreads();
   const int n_ins = T * (T - 1), n_mov = n_ins + s_pre[T];
-  int* ns = s_ns + (NN == 0 ? node_state_words(pb.N, GP) * tid : 0);
+  int* ns = s_ns + tid;
   const RowG row{s_rows + RS * tid, Tp};
   const RowG base{s_base, Tp};
   int cur = ms_io[blockIdx.x];
@@ -1155,7 +1174,7 @@ __global__ void __launch_bounds__(LS_B) k_local_search(Problem pb, uint8_t* __re
         row.c(t) = (uint8_t)(r < base.c(t) ? r : r + 1);
         for (int k = 0; k < T; ++k) row.q(k) = base.q(k);
       }
-      const int msn = decode_T<NN, GP, 0>(tab, S, pb.stride, row, T, pb, ns);
+      const int msn = decode_T<NN, GP, LS_B, eval_col(NN, GP), 0>(tab, S, pb.stride, row, T, pb, ns);
       const uint64_t key = ((uint64_t)(uint32_t)msn << 32) | (uint32_t)m;
       best = key < best ? key : best;
     }
