@@ -48,8 +48,11 @@ constexpr int WARP_B = 128;
 // shared memory per CTA, 3 instead of 4 CTAs per SM).  NN == 0 (run-time node count) is
 // columns only.
 __host__ __device__ __forceinline__ constexpr bool eval_col(int NN, int GP) { return NN != 1 || GP >= 8; }
+#ifndef SAT_GA_COL_MAX
+#define SAT_GA_COL_MAX 16   // largest NN * GP the GA kernel decodes with column states
+#endif
 __host__ __device__ __forceinline__ constexpr bool ga_col(int NN, int GP) {
-  return NN == 0 || (NN >= 2 && NN * GP <= 16);
+  return NN == 0 || (NN >= 2 && NN * GP <= SAT_GA_COL_MAX);
 }
 // Shared-memory bytes of the column node states for a block of B threads (0: registers).
 __host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, bool col, int NN, int GP, int B) {
@@ -499,7 +502,6 @@ cudaError_t launch_enumerate(const Problem& pb, int NN, int GP, const EnumSpace&
 
 // ------------------------------------------------------------------ K2b: DFS enumeration
 constexpr int DFS_B = 64;
-constexpr uint64_t DFS_BATCH = 4;   // roots per claim (dynamic root scheduling)
 // per-level thread-private words: state (NN*GP), ms, rperm lo/hi, rcfg lo/hi, used, t, c
 template <int NN, int GP>
 struct DfsLayout {
@@ -731,12 +733,15 @@ cudaError_t launch_enumerate_dfs(const Problem& pb, int NN, int GP, const DfsSpa
 // parent reads, the cuts and the crossover bits are shared by two children.
 // Thread-private genome rows in shared memory (RowG, odd-word stride RS >= GS): for short
 // genomes (T <= 32) the child C, parent A and parent B; long genomes keep only C and read
-// the parents from the population in global memory (L1), plus the LOX slice bit set
+// the parents from the population in global memory (L1/L2), plus the LOX slice bit set
 // (ceil(T/32) words per thread, interleaved).  The init kernel keeps one row.
 __host__ __device__ __forceinline__ int ga_rows(int T, bool init) { return (init || T > 32) ? 1 : 3; }
+__host__ __device__ __forceinline__ size_t lox_bits_bytes(const Problem& pb, bool init) {
+  return (init || pb.T <= 32) ? 0 : (size_t)4 * ((pb.T + 31) / 32) * GA_B;
+}
 static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS, bool init) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B) + (size_t)ga_rows(pb.T, init) * GA_B * odd_row_stride(GS) +
-         (size_t)4 * ((pb.T + 31) / 32) * GA_B + 8 * GA_B + 8;
+  return (size_t)pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B) +
+         (size_t)ga_rows(pb.T, init) * GA_B * odd_row_stride(GS) + lox_bits_bytes(pb, init) + 8 * GA_B + 8;
 }
 
 // Copy a GS-byte global record into a smem row (4-byte stores) and back.
@@ -756,6 +761,10 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
   const uint32_t* s = reinterpret_cast<const uint32_t*>(row);
   for (int k = 0; k < GS / 16; ++k) dst[k] = make_uint4(s[4 * k], s[4 * k + 1], s[4 * k + 2], s[4 * k + 3]);
 }
+
+#ifndef SAT_GA_L2PF
+#define SAT_GA_L2PF 1   // long genomes: L2 prefetch of the next pair's parent records
+#endif
 
 template <int NN, int GP>
 struct GaMinBlocks {
@@ -821,8 +830,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B);
-  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + GA_B * RS);
-  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_rows + GA_B * RS);
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
@@ -874,7 +882,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B);
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + ROWS * GA_B * RS);
-  uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_bits + ((T + 31) / 32) * GA_B);
+  uint64_t* s_lists = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s_bits) + lox_bits_bytes(pb, false));
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
   const uint32_t* tab = tab_of(s_blob);
@@ -953,16 +961,24 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         const uint32_t* cx = reinterpret_cast<const uint32_t*>(X);
         const uint32_t* cy = reinterpret_cast<const uint32_t*>(Y);
         uint32_t* cw = reinterpret_cast<uint32_t*>(ch.base);
-        uint32_t bits = 0;
-        for (int t = 0; t < T; t += 4) {
-          if ((t & 31) == 0) {
-            const int k = t >> 5;
-            bits = k == 0 ? w1.z : (k == 1 ? w1.w : philox_word(k0, k1, (uint32_t)q, gp.gen, c2, 16u + (k - 2)));
-          }
+        const auto mix = [&](int t, uint32_t bits) {
           const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;     // 1 -> take Y's gene
           const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;  // nibble -> byte mask
           cw[t >> 2] = (cx[t >> 2] & ~m) | (cy[t >> 2] & m);               // pad bytes: 0 in both
+        };
+        if (!LONGT) {
+          for (int t = 0; t < T; t += 4) mix(t, w1.z);
+        } else {   // 32 genes per crossover word; the parents' 8 words of a block loaded together
+          for (int t0 = 0; t0 < T; t0 += 32) {
+            const int k = t0 >> 5;
+            const uint32_t bits =
+                k == 0 ? w1.z : (k == 1 ? w1.w : philox_word(k0, k1, (uint32_t)q, gp.gen, c2, 16u + (k - 2)));
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (t0 + 4 * j < T) mix(t0 + 4 * j, bits);
+          }
         }
+#pragma unroll 4
         for (int w = 0; w < nw; ++w) cw[(Tp >> 2) + w] = cx[(Tp >> 2) + w];
       }
       // 4. LOX: keep X.perm[a..b] in place; fill positions 0..a-1, then b+1..T-1, with Y's
@@ -1043,6 +1059,23 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         ms_out[slot] = msv;
       }
       topE_insert(lst, in ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull, gp.E, cap);
+    }
+    if constexpr (LONGT && SAT_GA_L2PF) {
+      // The next pair's tournaments are decided now (their makespans arrived during this
+      // pair's decodes) and both winners' records are pulled into L2: long genomes read
+      // their parents straight from the population (an HBM-sized array), and the
+      // crossover / LOX loops would otherwise wait for DRAM.
+      if (chunks.next + lane < NP) {
+        const uint32_t An = ((((uint64_t)t_m1 << 32) | t_i1) < (((uint64_t)t_n1 << 32) | t_j1)) ? t_i1 : t_j1;
+        const uint32_t Bn = ((((uint64_t)t_m2 << 32) | t_i2) < (((uint64_t)t_n2 << 32) | t_j2)) ? t_i2 : t_j2;
+        const uint8_t* ra = prev_pop + (uint64_t)An * GS;
+        const uint8_t* rb = prev_pop + (uint64_t)Bn * GS;
+        for (int o = 0; o < GS + 127; o += 128) {
+          const int oo = min(o, GS - 1);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(ra + oo));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + oo));
+        }
+      }
     }
     base = chunks.advance();
   }
