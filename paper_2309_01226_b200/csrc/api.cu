@@ -532,6 +532,7 @@ saturn_status saturn_load_runtime_table(saturn_plan* p, const int32_t* runtime_s
   // makespan read off the final state (decode_sorted) for one full node: measured r1 TXT
   // evaluate +2.7 %, k_ga -0.8 %; on 2x8 (MIX) the second loop copy cost k_ga 1 %, so
   // multi-node shapes keep the running max
+  p->pb.one = 1;
   p->pb.full_nodes = (p->NN == 1 && p->gpu_n.size() == 1 && p->gpu_n[0] == p->GP) ? 1 : 0;
   if (sat::eval_smem_bytes(pb, p->NN, p->GP) > 227 * 1024)
     return fail(p, SATURN_ELIMIT, "evaluate tile exceeds shared memory");

@@ -32,6 +32,7 @@ struct Problem {
   int sumG;                // sum_n GPU_n
   int8_t gpu_n[MAX_NODES]; // GPU_n
   int full_nodes;          // 1: one node with exactly GP GPUs (decode reads the makespan off the state)
+  int one;                 // 1, opaque to ptxas (predicated FMA-pipe moves, decode.cuh pmov_fma)
 };
 
 __device__ __forceinline__ const uint32_t* tab_of(const uint8_t* blob) {

@@ -49,27 +49,56 @@ __device__ __forceinline__ int sel_fma(int p, int a, int b) {
   return r;
 }
 
+// Predicated move on the FMA pipe: if (p) d = s, as `@p IMAD d, s, one, RZ` with `one` a
+// run-time 1 (Problem::one) that ptxas cannot fold -- a predicated MOV would become an ALU
+// SEL.  One FMA-pipe instruction per element of an in-place barrel-shift stage.
+// `bit` is tested for != 0 (pass k & sh, not a 0/1 value: one LOP3 makes the predicate).
+__device__ __forceinline__ void pmov_fma(int& d, int s, int bit, int one) {
+  asm("{.reg .pred q; setp.ne.b32 q, %2, 0; @q mad.lo.s32 %0, %1, %3, 0;}" : "+r"(d) : "r"(s), "r"(bit), "r"(one));
+}
+// if (bit) d = +inf, in place: d * zero + inf with a run-time zero (a loop-invariant
+// `one * inf` would be hoisted and the predicated move turned back into an ALU SEL).
+__device__ __forceinline__ void pinf_fma(int& d, int bit, int zero) {
+  asm("{.reg .pred q; setp.ne.b32 q, %1, 0; @q mad.lo.s32 %0, %0, %2, 2147483647;}" : "+r"(d) : "r"(bit), "r"(zero));
+}
+
+#ifndef SAT_SHIFT_PMAD
+#define SAT_SHIFT_PMAD 1   // 0: every shift lane as a two-IMAD select (r1 design, A/B switch)
+#endif
+
 // In-place update of one node's sorted free-time vector after placing (g, R) at its
-// g-th smallest free time.  Returns s + R.
+// g-th smallest free time.  Returns s + R.  `one` = Problem::one.
 template <int GP>
-__device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R) {
+__device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R, int one) {
   const int k = g - 1;
   int b[GP];
 #pragma unroll
   for (int i = 0; i < GP; ++i) b[i] = x[i];
-  // Every stage on the FMA pipe (measured r1: +5 % TXT, +8 % MIX evaluate), except the lanes
-  // that shift in +inf: one ALU select beats two FMA-pipe ops there (pipe balance, +1.7 %).
   int stage = 0;
 #pragma unroll
   for (int sh = 1; sh < GP; sh <<= 1, ++stage) {
-    const bool on = (k & sh) != 0;
+    [[maybe_unused]] const bool on = (k & sh) != 0;
     const int p = (k >> stage) & 1;
 #pragma unroll
     for (int i = 0; i < GP; ++i) {
-      if (i + sh >= GP)
-        b[i] = on ? INF : b[i];
-      else
-        b[i] = sel_fma(p, b[i], b[i + sh]);
+      if constexpr (SAT_SHIFT_PMAD) {
+        // All on the FMA pipe (the decode's binding pipe is the ALU: VIMNMX / ISETP / SEL).
+        // b[i] <- b[i + sh] in place (ascending i reads lanes this stage has not written);
+        // lanes past the end shift in +inf.  The first stage's lanes still read x, so they
+        // are two-source selects (the IMAD pair).
+        if (stage == 0)
+          b[i] = sel_fma(p, b[i], (i + sh >= GP) ? INF : b[i + sh]);
+        else if (i + sh >= GP)
+          pinf_fma(b[i], k & sh, one - 1);
+        else
+          pmov_fma(b[i], b[i + sh], k & sh, one);
+      } else {
+        // r1: every stage on the FMA pipe as IMAD pairs, +inf lanes as ALU selects
+        if (i + sh >= GP)
+          b[i] = on ? INF : b[i];
+        else
+          b[i] = sel_fma(p, b[i], b[i + sh]);
+      }
     }
   }
   const int s = b[0];
@@ -208,7 +237,7 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
     const int R = (int)(w & R_MASK);
     int v;
     if constexpr (NN == 1) {
-      v = place_sorted<GP>(a[0], g, R);
+      v = place_sorted<GP>(a[0], g, R, pb.one);
     } else {
       // start of every node: its g-th smallest free time (+inf if it has fewer GPUs)
       int best = mux<GP>(a[0], g - 1);
@@ -228,7 +257,7 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
         for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
         x[i] = y;
       }
-      v = place_sorted<GP>(x, g, R);
+      v = place_sorted<GP>(x, g, R, pb.one);
 #pragma unroll
       for (int n = 0; n < NN; ++n)
 #pragma unroll
@@ -313,7 +342,7 @@ __device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ 
       for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
       x[i] = y;
     }
-    int v = place_sorted<GP>(x, max(g, 1), R);
+    int v = place_sorted<GP>(x, max(g, 1), R, pb.one);
     if (best == INF) v = 0;
 #pragma unroll
     for (int n = 0; n < NN; ++n)

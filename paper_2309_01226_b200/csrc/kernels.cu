@@ -522,9 +522,9 @@ __device__ __forceinline__ int start_of(const int (&a)[NN][GP], int g) {
 
 // place (g, R) on the cluster state a (greedy node, lowest id on ties); returns s + R
 template <int NN, int GP>
-__device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R) {
+__device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R, int one) {
   if constexpr (NN == 1) {
-    return place_sorted<GP>(a[0], g, R);
+    return place_sorted<GP>(a[0], g, R, one);
   } else {
     int best = mux<GP>(a[0], g - 1);
     int bn = 0;
@@ -543,7 +543,7 @@ __device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R) {
       for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
       x[i] = y;
     }
-    const int v = place_sorted<GP>(x, g, R);
+    const int v = place_sorted<GP>(x, g, R, one);
 #pragma unroll
     for (int n = 0; n < NN; ++n)
 #pragma unroll
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
       const int c = pi - ds.pre[t];
       if ((used & (1u << t)) || (used & ds.twin_prev[t]) != ds.twin_prev[t]) { ok = false; break; }
       const uint32_t w = tab[t * pb.stride + c];
-      ms = max(ms, place_T<NN, GP>(a, (int)(w >> 24), (int)(w & R_MASK)));
+      ms = max(ms, place_T<NN, GP>(a, (int)(w >> 24), (int)(w & R_MASK), pb.one));
       rperm += (uint64_t)__popc(~used & full & ((1u << t) - 1u)) * ds.es.fact[T - 1 - i];
       rcfg += (uint64_t)c * ds.es.radix[t];
       used |= 1u << t;
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(DFS_B) k_enumerate_dfs(Problem pb, DfsSpace ds
         for (int n = 0; n < NN; ++n)
 #pragma unroll
           for (int i = 0; i < GP; ++i) b[n][i] = a[n][i];
-        const int ms2 = max(ms, place_T<NN, GP>(b, (int)(w >> 24), (int)(w & R_MASK)));
+        const int ms2 = max(ms, place_T<NN, GP>(b, (int)(w >> 24), (int)(w & R_MASK), pb.one));
         if (ms2 > inc_ms) continue;  // strict cut: no leaf below can reach the incumbent
         // save this level and descend
 #pragma unroll

@@ -1,9 +1,9 @@
 # scratch GPU call used during round 2 (edited per call)
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-AB_WORKLOADS="SWEEP TXT MIX" timeout 900 bash tools/ab_run.sh gpurun_out/ab_bit.jsonl build_variants/base/libsaturn.so build_variants/bit/libsaturn.so build_variants/bitpf/libsaturn.so
-tail -3 gpurun_out/ab_bit.jsonl.err
+AB_WORKLOADS="TXT MIX SWEEP TINY" timeout 900 bash tools/ab_run.sh gpurun_out/ab_pmad.jsonl build_variants/prev/libsaturn.so build_variants/pmad/libsaturn.so
+tail -3 gpurun_out/ab_pmad.jsonl.err
 python - <<'PY'
 import json
-for l in open('gpurun_out/ab_bit.jsonl'):
+for l in open('gpurun_out/ab_pmad.jsonl'):
     d=json.loads(l); print(d['lib'][:22], d['workload'], 'eval %.4g' % d['evaluate_plans_per_s'], 'step %.4f' % d['step_ms'], 'kga %.4f' % d['ga_kernel_ms'], d['best'])
 PY
