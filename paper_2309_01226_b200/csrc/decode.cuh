@@ -62,6 +62,43 @@ __device__ __forceinline__ void pinf_fma(int& d, int bit, int zero) {
   asm("{.reg .pred q; setp.ne.b32 q, %1, 0; @q mad.lo.s32 %0, %0, %2, 2147483647;}" : "+r"(d) : "r"(bit), "r"(zero));
 }
 
+// if (sel == N) d = s, in place on the FMA pipe (the multi-node gather / scatter of the
+// chosen node's vector; ptxas shares the compare across the lanes).  Written as
+// d = d * zero + s so the product depends on d: with s * one, ptxas computes it once for
+// all nodes and turns every predicated move back into an ALU SEL.
+template <int N>
+__device__ __forceinline__ void pmov_eq(int& d, int s, int sel, int zero) {
+  asm("{.reg .pred q; setp.eq.s32 q, %2, %4; @q mad.lo.s32 %0, %0, %3, %1;}" : "+r"(d) : "r"(s), "r"(sel), "r"(zero), "n"(N));
+}
+
+// Chosen node's vector out of / back into the register states a[NN][GP] (multi-node T
+// design).  The first two gather steps are selects (ALU), the rest predicated moves (FMA
+// pipe): the 4-node decode was ALU-bound on these selects (r2: 103 ALU + 59 FMA per job
+// step; now 79 + 75).
+template <int NN, int GP, int N = 1>
+__device__ __forceinline__ void gather_node(int (&x)[GP], const int (&a)[NN][GP], int bn, int one) {
+  if constexpr (N < NN) {
+#pragma unroll
+    for (int i = 0; i < GP; ++i) {
+      if constexpr (N == 1) x[i] = (bn == 1) ? a[1][i] : a[0][i];
+      else if constexpr (N == 2) x[i] = (bn == 2) ? a[2][i] : x[i];   // (pipe balance, 4 nodes)
+      else pmov_eq<N>(x[i], a[N][i], bn, one - 1);
+    }
+    gather_node<NN, GP, N + 1>(x, a, bn, one);
+  } else if constexpr (NN == 1) {
+#pragma unroll
+    for (int i = 0; i < GP; ++i) x[i] = a[0][i];
+  }
+}
+template <int NN, int GP, int N = 0>
+__device__ __forceinline__ void scatter_node(int (&a)[NN][GP], const int (&x)[GP], int bn, int one) {
+  if constexpr (N < NN) {
+#pragma unroll
+    for (int i = 0; i < GP; ++i) pmov_eq<N>(a[N][i], x[i], bn, one - 1);
+    scatter_node<NN, GP, N + 1>(a, x, bn, one);
+  }
+}
+
 #ifndef SAT_SHIFT_PMAD
 #define SAT_SHIFT_PMAD 1   // 0: every shift lane as a two-IMAD select (r1 design, A/B switch)
 #endif
@@ -250,18 +287,9 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
         bn = lt ? n : bn;
       }
       int x[GP];
-#pragma unroll
-      for (int i = 0; i < GP; ++i) {
-        int y = a[0][i];
-#pragma unroll
-        for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
-        x[i] = y;
-      }
+      gather_node<NN, GP>(x, a, bn, pb.one);
       v = place_sorted<GP>(x, g, R, pb.one);
-#pragma unroll
-      for (int n = 0; n < NN; ++n)
-#pragma unroll
-        for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
+      scatter_node<NN, GP>(a, x, bn, pb.one);
     }
     if constexpr (TRACK_MS) ms = max(ms, v);
     if (AHEAD) w = wn;

@@ -536,18 +536,9 @@ __device__ __forceinline__ int place_T(int (&a)[NN][GP], int g, int R, int one) 
       bn = lt ? n : bn;
     }
     int x[GP];
-#pragma unroll
-    for (int i = 0; i < GP; ++i) {
-      int y = a[0][i];
-#pragma unroll
-      for (int n = 1; n < NN; ++n) y = (bn == n) ? a[n][i] : y;
-      x[i] = y;
-    }
+    gather_node<NN, GP>(x, a, bn, one);
     const int v = place_sorted<GP>(x, g, R, one);
-#pragma unroll
-    for (int n = 0; n < NN; ++n)
-#pragma unroll
-      for (int i = 0; i < GP; ++i) a[n][i] = (bn == n) ? x[i] : a[n][i];
+    scatter_node<NN, GP>(a, x, bn, one);
     return v;
   }
 }
