@@ -981,18 +981,37 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         uint8_t* wp = (a == 0) ? p0 + gap : p0;
         const uint8_t* Yq = Y + Tp;
         if (!LONGT) {
+          // Genes < 32: the slice is a bit set.  Four genes per shared-memory word, gene
+          // bits by wrapping funnel shifts (x & 31 for free), positions a..b as a bit mask.
+          const uint32_t* xq = reinterpret_cast<const uint32_t*>(p0);
+          const uint32_t* yq = reinterpret_cast<const uint32_t*>(Yq);
+          const uint32_t M = (0xffffffffu >> (31u - b)) & (0xffffffffu << a);   // b <= 31
           uint32_t kept = 0;
-          for (int k = 0; k < T; ++k) {
-            const uint32_t bit = 1u << ch.q(k);
-            kept |= ((uint32_t)k - a <= b - a) ? bit : 0u;
+          for (int w = 0; w < nw; ++w) {   // pad genes lie outside a..b
+            const uint32_t W = xq[w], Mw = M >> (4 * w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (Mw & (1u << e)) kept |= __funnelshift_l(0u, 1u, W >> (8 * e));
           }
           if (!(xo && child)) kept = 0xffffffffu;   // nothing is taken
-          for (int k = 0; k < T; ++k) {   // branch-free: predicated store, pointer arithmetic
-            const uint32_t x = Yq[k];
-            const uint32_t take = (~kept >> x) & 1u;
+          // branch-free fill: predicated byte store (of the low byte), pointer arithmetic
+          const auto fill = [&](uint32_t x) {
+            const uint32_t take = ~__funnelshift_r(kept, 0u, x) & 1u;
             if (take) *wp = (uint8_t)x;
             wp += take;
             wp = (wp == pa) ? wp + gap : wp;
+          };
+          const int nf = T >> 2;
+          for (int w = 0; w < nf; ++w) {
+            const uint32_t W = yq[w];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) fill(W >> (8 * e));
+          }
+          if (T & 3) {   // the last, partial word (its pad bytes are not genes)
+            const uint32_t W = yq[nf];
+#pragma unroll
+            for (int e = 0; e < 3; ++e)
+              if (e < (T & 3)) fill(W >> (8 * e));
           }
         } else {
           // Rows of lanes without a child hold stale bytes: the word index is clamped so
