@@ -387,12 +387,13 @@ __device__ __forceinline__ int decode_sorted_nodes(const uint32_t* __restrict__ 
 }
 
 // Column node states (decode_col): node n's sorted slot j of thread `tid` is the word
-// ns[(n * col_rows(GP) + j) * B + tid] of a block of B threads -- every thread's same slot in
+// ns[(n * col_rows(GP, rshift) + j) * B + tid] of a block of B threads -- every thread's same slot in
 // one row, so any per-thread slot index is bank-conflict free.  Rows GP .. 2GP-2 of every
 // node are +inf padding: slot j + g (g <= GP, j <= GP-2) reads +inf past the node's GPUs.
-__host__ __device__ __forceinline__ constexpr int col_rows(int GP) { return 2 * GP - 1; }
-__host__ __device__ __forceinline__ size_t col_state_bytes(int N, int GP, int B) {
-  return (size_t)4 * N * col_rows(GP) * B;
+// RSHIFT variant: no padding rows (the chosen node's vector is shifted in registers).
+__host__ __device__ __forceinline__ constexpr int col_rows(int GP, bool rshift) { return rshift ? GP : 2 * GP - 1; }
+__host__ __device__ __forceinline__ size_t col_state_bytes(int N, int GP, int B, bool rshift) {
+  return (size_t)4 * N * col_rows(GP, rshift) * B;
 }
 
 // T design for multi-node clusters with the node states in shared memory, column layout
@@ -402,11 +403,17 @@ __host__ __device__ __forceinline__ size_t col_state_bytes(int N, int GP, int B)
 // (the barrel shift of place_sorted done by the LSU's addressing instead of select stages)
 // -- and the update x'[i] = (b[i+1] <= s) ? x[i] : min(b[i+1], max(x[i], s+R)) is stored
 // back.  No gather/scatter selects, no shift stages, 8-slot register footprint.
-template <int NN, int GP, int B, int CHECK, class G>
+// RSHIFT: the chosen node's vector is read (GP loads), shifted and updated in registers
+// (place_sorted: predicated FMA-pipe moves) and stored back -- 7 fewer shared-memory loads
+// per step than the shifted reads and no padding rows: the multi-node evaluate is bound by
+// shared-memory wavefronts, and there this measured SWEEP 1.83e9 -> 2.23e9, MIX 1.08e10 ->
+// 1.20e10 plans/s (r2); a single node (TXT -4 %) and the MIX GA (+11 % time, the GA's own
+// shared traffic no longer dominates) keep the shifted reads.
+template <int NN, int GP, int B, bool RSHIFT, int CHECK, class G>
 __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, const uint8_t* __restrict__ S,
                                           int stride, const G& gen, int T, const Problem& pb, int* ns,
                                           uint32_t* mask = nullptr, int mstride = 0) {
-  constexpr int RW = col_rows(GP);
+  constexpr int RW = col_rows(GP, RSHIFT);
   const int N = NN ? NN : pb.N;
   bool bad = false;
   int maxt = 0;
@@ -489,6 +496,14 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
     const int s = start_min(g, bn);
     const int v = s + R;
     int* row = ns + bn * RW * B;
+    if constexpr (RSHIFT) {   // the shift in registers (predicated FMA-pipe moves)
+      int x[GP];
+#pragma unroll
+      for (int i = 0; i < GP; ++i) x[i] = row[i * B];
+      place_sorted<GP>(x, g, R, pb.one);
+#pragma unroll
+      for (int i = 0; i < GP; ++i) row[i * B] = x[i];
+    } else {
     const int* sh = row + g * B;   // sh[i * B] = slot i + g = b[i + 1]
     int x[GP], y[GP];
 #pragma unroll
@@ -503,6 +518,7 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
       } else {
         row[i * B] = max(x[i], v);
       }
+    }
     }
     ms = max(ms, v);
     w = wn;

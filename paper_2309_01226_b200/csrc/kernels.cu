@@ -47,7 +47,11 @@ constexpr int WARP_B = 128;
 // -4 %) but lose on one node (TXT +5.5 %) and on 32-slot states (SWEEP +37 %: 30 KB more
 // shared memory per CTA, 3 instead of 4 CTAs per SM).  NN == 0 (run-time node count) is
 // columns only.
-__host__ __device__ __forceinline__ constexpr bool eval_col(int NN, int GP) { return NN != 1 || GP >= 8; }
+// Modes: 0 registers, 1 columns with shifted reads, 2 columns with the shift in registers.
+enum { ST_REG = 0, ST_COL = 1, ST_COLR = 2 };
+__host__ __device__ __forceinline__ constexpr int eval_mode(int NN, int GP) {
+  return NN == 1 ? (GP >= 8 ? ST_COL : ST_REG) : ST_COLR;
+}
 #ifndef SAT_GA_COL_MAX
 #define SAT_GA_COL_MAX 16   // largest NN * GP the GA kernel decodes with column states
 #endif
@@ -55,19 +59,20 @@ __host__ __device__ __forceinline__ constexpr bool ga_col(int NN, int GP) {
   return NN == 0 || (NN >= 2 && NN * GP <= SAT_GA_COL_MAX);
 }
 // Shared-memory bytes of the column node states for a block of B threads (0: registers).
-__host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, bool col, int NN, int GP, int B) {
-  return col ? col_state_bytes(NN ? NN : pb.N, GP, B) : 0;
+__host__ __device__ __forceinline__ constexpr int ga_mode(int NN, int GP) { return ga_col(NN, GP) ? ST_COL : ST_REG; }
+__host__ __device__ __forceinline__ size_t ns_bytes(const Problem& pb, int mode, int NN, int GP, int B) {
+  return mode != ST_REG ? col_state_bytes(NN ? NN : pb.N, GP, B, mode == ST_COLR) : 0;
 }
 
 // Decode one genome with the (NN, GP) design; `ns` = this thread's node-state slice (NN == 0).
 // STATE_MS: allow reading the makespan off the final state for one full node (decode_sorted);
 // only the evaluate kernel uses it -- in k_ga the extra loop copy measured 3 % slower.
 // COL: column states, `ns` = &state[threadIdx.x] of a block of B threads; else registers.
-template <int NN, int GP, int B, bool COL, int CHECK, bool STATE_MS = false, class G>
+template <int NN, int GP, int B, int MODE, int CHECK, bool STATE_MS = false, class G>
 __device__ __forceinline__ int decode_T(const uint32_t* tab, const uint8_t* S, int stride, const G& gen, int T,
                                         const Problem& pb, int* ns, uint32_t* mask = nullptr, int mstride = 0) {
-  static_assert(COL || NN >= 1, "a run-time node count needs the column states");
-  if constexpr (COL) return decode_col<NN, GP, B, CHECK>(tab, S, stride, gen, T, pb, ns, mask, mstride);
+  static_assert(MODE != ST_REG || NN >= 1, "a run-time node count needs the column states");
+  if constexpr (MODE != ST_REG) return decode_col<NN, GP, B, MODE == ST_COLR, CHECK>(tab, S, stride, gen, T, pb, ns, mask, mstride);
   else if constexpr (STATE_MS) return decode_sorted<NN, GP, CHECK>(tab, S, stride, gen, T, pb, mask, mstride);
   else return decode_sorted_impl<NN, GP, CHECK, true>(tab, S, stride, gen, T, pb, mask, mstride);
 }
@@ -120,7 +125,7 @@ __device__ __forceinline__ void topE_insert(uint64_t& lst, uint64_t key, int E, 
 #endif
 __host__ __device__ __forceinline__ int eval_nbuf(int T) { return 4 * EVAL_TILE * T <= SAT_EVAL_DB_LIMIT ? 2 : 1; }
 size_t eval_smem_bytes(const Problem& pb, int NN, int GP) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, EVAL_B) + 2u * eval_nbuf(pb.T) * EVAL_TILE * pb.T +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_mode(NN, GP), NN, GP, EVAL_B) + 2u * eval_nbuf(pb.T) * EVAL_TILE * pb.T +
          4u * EVAL_B * ((pb.T + 31) / 32) + 3 * 8;
 }
 
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
   const int nbuf = eval_nbuf(T);
-  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, EVAL_B);   // [nbuf buffers][cfg | perm]
+  uint8_t* s_g = sm + pb.blob_bytes + ns_bytes(pb, eval_mode(NN, GP), NN, GP, EVAL_B);   // [nbuf buffers][cfg | perm]
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_g + 2 * nbuf * tileB);
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_mask + EVAL_B * ((T + 31) / 32));
   const int64_t ntiles = (n + EVAL_TILE - 1) / EVAL_TILE;
@@ -189,8 +194,8 @@ __global__ void __launch_bounds__(EVAL_B) k_evaluate(Problem pb, const uint8_t* 
     if (first + tid < n) {
       RowGenome gen{bc + tid * T, bp + tid * T};
       int* ns = s_ns + tid;
-      out[first + tid] = (T <= 32) ? decode_T<NN, GP, EVAL_B, eval_col(NN, GP), 1, true>(tab, S, pb.stride, gen, T, pb, ns)
-                                   : decode_T<NN, GP, EVAL_B, eval_col(NN, GP), 2, true>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
+      out[first + tid] = (T <= 32) ? decode_T<NN, GP, EVAL_B, eval_mode(NN, GP), 1, true>(tab, S, pb.stride, gen, T, pb, ns)
+                                   : decode_T<NN, GP, EVAL_B, eval_mode(NN, GP), 2, true>(tab, S, pb.stride, gen, T, pb, ns, s_mask + tid, EVAL_B);
     }
     __syncthreads();
     if (nbuf == 1 && tid == 0) {  // one buffer: the next tile's copy starts once it is free
@@ -397,7 +402,7 @@ cudaError_t launch_evaluate_nodes(const Problem& pb, int NN, int GP, const uint8
 // Consecutive indices advance cfg like an odometer (job 0 fastest), then perm by
 // next_permutation, so only the first index of a chunk is unranked.
 static size_t enum_smem_bytes(const Problem& pb, int NN, int GP) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, ENUM_B) + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_mode(NN, GP), NN, GP, ENUM_B) + (size_t)ENUM_B * odd_row_stride(perm_offset(pb.T) + pb.T) +
          32 * 8 + 8;
 }
 
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
   extern __shared__ __align__(16) uint8_t sm[];
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_gen = sm + pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, ENUM_B);
+  uint8_t* s_gen = sm + pb.blob_bytes + ns_bytes(pb, eval_mode(NN, GP), NN, GP, ENUM_B);
   const int T = pb.T;
   const int RS = odd_row_stride(perm_offset(T) + T);
   uint64_t* s_red = reinterpret_cast<uint64_t*>(s_gen + ((ENUM_B * RS + 7) & ~7));
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(ENUM_B) k_enumerate(Problem pb, EnumSpace es, 
       gen.q(p) = (uint8_t)x;
     }
     for (uint64_t idx = i0; idx < i1; ++idx) {
-      const int ms = decode_T<NN, GP, ENUM_B, eval_col(NN, GP), 0>(tab, S, pb.stride, gen, T, pb,
+      const int ms = decode_T<NN, GP, ENUM_B, eval_mode(NN, GP), 0>(tab, S, pb.stride, gen, T, pb,
                                          s_ns + threadIdx.x);
       const uint64_t key = ((uint64_t)ms << 38) | idx;
       best = key < best ? key : best;
@@ -730,9 +735,23 @@ __host__ __device__ __forceinline__ int ga_rows(int T, bool init) { return (init
 __host__ __device__ __forceinline__ size_t lox_bits_bytes(const Problem& pb, bool init) {
   return (init || pb.T <= 32) ? 0 : (size_t)4 * ((pb.T + 31) / 32) * GA_B;
 }
+// Long genomes on column states stage each child's parents in shared memory (cp.async, one
+// round trip): X into the child row, Y into the idle node-state region, GS / 4 rows.
+__host__ __device__ __forceinline__ size_t ga_ns_bytes(const Problem& pb, int NN, int GP, int GS) {
+  const size_t col = ns_bytes(pb, ga_mode(NN, GP), NN, GP, GA_B);
+  return (ga_col(NN, GP) && pb.T > 32 && (size_t)GS * GA_B > col) ? (size_t)GS * GA_B : col;
+}
 static size_t ga_smem_bytes(const Problem& pb, int NN, int GP, int GS, bool init) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B) +
+  return (size_t)pb.blob_bytes + ga_ns_bytes(pb, NN, GP, GS) +
          (size_t)ga_rows(pb.T, init) * GA_B * odd_row_stride(GS) + lox_bits_bytes(pb, init) + 8 * GA_B + 8;
+}
+
+// 4-byte asynchronous global -> shared copies (LDGSTS), completed by cp_async_wait_all.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
 // Copy a GS-byte global record into a smem row (4-byte stores) and back.
@@ -820,7 +839,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   const int T = pb.T, GS = gp.GS, RS = odd_row_stride(GS), Tp = perm_offset(T);
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B);
+  uint8_t* s_rows = sm + pb.blob_bytes + ga_ns_bytes(pb, NN, GP, GS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(s_rows + GA_B * RS);
   uint64_t* bar = s_lists + GA_B;
   stage_problem(s_blob, pb, bar);
@@ -850,7 +869,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           ch.q(j) = a;
         }
       }
-      msv = decode_T<NN, GP, GA_B, ga_col(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
+      msv = decode_T<NN, GP, GA_B, ga_mode(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
       store_row(pop + slot * GS, ch.base, GS);
       ms_out[slot] = msv;
     }
@@ -871,7 +890,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
   constexpr int ROWS = LONGT ? 1 : 3;
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_rows = sm + pb.blob_bytes + ns_bytes(pb, ga_col(NN, GP), NN, GP, GA_B);
+  uint8_t* s_rows = sm + pb.blob_bytes + ga_ns_bytes(pb, NN, GP, GS);
   uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_rows + ROWS * GA_B * RS);
   uint64_t* s_lists = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s_bits) + lox_bits_bytes(pb, false));
   uint64_t* bar = s_lists + GA_B;
@@ -946,7 +965,37 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         load_row(ch.base, rec_gen + (size_t)slot * GS, GS);
         msv = rec_ms[slot];
       }
-      if (child) {
+      // Long genomes on column states: X's record is copied into the child row and Y's into
+      // the idle node-state region (word w at ns[w * GA_B]) with cp.async, one round trip,
+      // instead of the loops below waiting on global loads (12 warps per SM leave too few to
+      // hide them).  The child then starts as X: crossover and LOX work in place.
+      constexpr bool STAGE = LONGT && ga_col(NN, GP);
+      if (STAGE && child) {
+        const uint32_t* gx = reinterpret_cast<const uint32_t*>(X);
+        const uint32_t* gy = reinterpret_cast<const uint32_t*>(Y);
+        uint32_t* cw = reinterpret_cast<uint32_t*>(ch.base);
+        for (int w = 0; w < GS / 4; ++w) {
+          cp_async4(cw + w, gx + w);
+          cp_async4(ns + w * GA_B, gy + w);
+        }
+        cp_async_wait_all();
+        uint32_t* cwv = cw;
+        const auto ys = [&](int w) -> uint32_t { return (uint32_t)ns[w * GA_B]; };
+        const auto mixs = [&](int t, uint32_t bits) {
+          const uint32_t nib = xo ? (~(bits >> (t & 31)) & 0xfu) : 0u;
+          const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
+          cwv[t >> 2] = (cwv[t >> 2] & ~m) | (ys(t >> 2) & m);
+        };
+        for (int t0 = 0; t0 < T; t0 += 32) {
+          const int k = t0 >> 5;
+          const uint32_t bits =
+              k == 0 ? w1.z : (k == 1 ? w1.w : philox_word(k0, k1, (uint32_t)q, gp.gen, c2, 16u + (k - 2)));
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (t0 + 4 * j < T) mixs(t0 + 4 * j, bits);
+        }
+      }
+      if (!STAGE && child) {
         // 3. uniform crossover of the config genes, 4 genes per step (bit 1 -> X's gene);
         //    the permutation starts as a copy of X's
         const uint32_t* cx = reinterpret_cast<const uint32_t*>(X);
@@ -1022,12 +1071,21 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
             inA[min(x >> 5, nb - 1) * GA_B] |= 1u << (x & 31);
           }
           const uint32_t xm = (xo && child) ? 1u : 0u;
-          for (int k = 0; k < T; ++k) {
-            const int x = child ? Yq[k] : 0;
+          const auto fill = [&](int x) {
             const uint32_t take = (~inA[min(x >> 5, nb - 1) * GA_B] >> (x & 31)) & xm;
             if (take) *wp = (uint8_t)x;
             wp += take;
             wp = (wp == pa) ? wp + gap : wp;
+          };
+          if constexpr (STAGE) {   // Y's permutation from the staged words
+            for (int k = 0; k < T; k += 4) {
+              const uint32_t y4 = child ? (uint32_t)ns[((Tp + k) >> 2) * GA_B] : 0u;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (k + e < T) fill((int)((y4 >> (8 * e)) & 0xffu));
+            }
+          } else {
+            for (int k = 0; k < T; ++k) fill(child ? Yq[k] : 0);
           }
         }
       }
@@ -1063,7 +1121,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
           ch.q(mj) = xi;
         }
       }
-      if (child) msv = decode_T<NN, GP, GA_B, ga_col(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
+      if (child) msv = decode_T<NN, GP, GA_B, ga_mode(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
       if (in) {
         store_row(pop + (size_t)slot * GS, ch.base, GS);
         ms_out[slot] = msv;
@@ -1162,7 +1220,7 @@ cudaError_t launch_ga_generation(const Problem& pb, int NN, int GP, const GaPara
 // strict improvement, up to `iters` times.  Records are updated in place.
 constexpr int LS_B = 128;
 static size_t ls_smem_bytes(const Problem& pb, int NN, int GP, int GS) {
-  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, LS_B) + (size_t)(LS_B + 1) * odd_row_stride(GS) +
+  return (size_t)pb.blob_bytes + ns_bytes(pb, eval_mode(NN, GP), NN, GP, LS_B) + (size_t)(LS_B + 1) * odd_row_stride(GS) +
          (size_t)4 * (pb.T + 1) + 8 * (LS_B / 32) + 16 + 8;
 }
 
@@ -1173,7 +1231,7 @@ __global__ void __launch_bounds__(LS_B) k_local_search(Problem pb, uint8_t* __re
   const int T = pb.T, Tp = perm_offset(T), RS = odd_row_stride(GS);
   uint8_t* s_blob = sm;
   int* s_ns = reinterpret_cast<int*>(sm + pb.blob_bytes);
-  uint8_t* s_base = sm + pb.blob_bytes + ns_bytes(pb, eval_col(NN, GP), NN, GP, LS_B);
+  uint8_t* s_base = sm + pb.blob_bytes + ns_bytes(pb, eval_mode(NN, GP), NN, GP, LS_B);
   uint8_t* s_rows = s_base + RS;
   int* s_pre = reinterpret_cast<int*>(s_rows + LS_B * RS);       // prefix of (S_t - 1), T + 1 entries
   uint64_t* s_red = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(s_pre + T + 1) + 7) & ~uintptr_t(7));
@@ -1217,7 +1275,7 @@ __global__ void __launch_bounds__(LS_B) k_local_search(Problem pb, uint8_t* __re
         row.c(t) = (uint8_t)(r < base.c(t) ? r : r + 1);
         for (int k = 0; k < T; ++k) row.q(k) = base.q(k);
       }
-      const int msn = decode_T<NN, GP, LS_B, eval_col(NN, GP), 0>(tab, S, pb.stride, row, T, pb, ns);
+      const int msn = decode_T<NN, GP, LS_B, eval_mode(NN, GP), 0>(tab, S, pb.stride, row, T, pb, ns);
       const uint64_t key = ((uint64_t)(uint32_t)msn << 32) | (uint32_t)m;
       best = key < best ? key : best;
     }

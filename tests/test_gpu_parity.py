@@ -341,6 +341,29 @@ def test_multinode_shared_memory_decoder(sat, torch):
     assert np.array_equal(gc, rc) and np.array_equal(gq, rq) and np.array_equal(gm, oracle.decode_batch(c, rc, rq))
 
 
+def test_long_genome_ga_on_column_states_replays_oracle(sat, torch):
+    """Long genomes (T > 32) on column node states: each child's parents are staged in
+    shared memory with cp.async (X into the child row, Y into the idle state region) before
+    crossover and LOX -- SWEEP (4x8, T = 100) and a 3-node T = 40 instance on the run-time
+    node-count shape, two generations replayed by oracle/ga.py bit for bit."""
+    for inst in (synth.sweep(3), synth.sweep(7, n_jobs=40, nodes=[8, 4, 2])):
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        P, E, seed = 256, 8, 4242
+        px, pc, pm = oga.q32(0.9), oga.q32(0.3), oga.q32(0.6)
+        cfg, perm = oga.initial_population(c.S, P, seed)
+        rm = oracle.decode_batch(c, cfg, perm)
+        rc, rq = cfg, perm
+        for gen in (1, 2):
+            rc, rq, _ = oga.next_generation(c.S, rc, rq, rm, gen, seed, 0, E, px, pc, pm)
+            rm = oracle.decode_batch(c, rc, rq)
+        plan = _plan(sat, inst)
+        plan.set_decoder(sat.DECODER_NODE_SMEM)
+        plan.search(sat.SearchConfig(seed=seed, population=P, max_generations=2, elites=E, generations_per_epoch=1,
+                                     p_xover=0.9, p_cfg_mut=0.3, p_perm_mut=0.6))
+        gc, gq, gm = plan.search_population(P)
+        assert np.array_equal(gc, rc) and np.array_equal(gq, rq) and np.array_equal(gm, rm)
+
+
 # ------------------------------------------------------------------ f4: local search
 @pytest.mark.parametrize("name,n,iters", [("TXT", 24, 6), ("MIX", 8, 3), ("TINY", 16, 4)])
 def test_improve_matches_oracle_local_search(sat, torch, name, n, iters):
