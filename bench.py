@@ -395,7 +395,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="saturn", choices=["saturn", "reference"])
     ap.add_argument("--workload", default="TXT", choices=sorted(WORKLOADS))
-    ap.add_argument("--population", type=int, default=1 << 22)
+    # 2^23 genomes per GPU: the per-launch fixed cost (prologue, the last chunk's tail) is
+    # 3 % of a k_ga launch at 2^22 and 1 % here (tools/pop_scaling.py)
+    ap.add_argument("--population", type=int, default=1 << 23)
     ap.add_argument("--generations", type=int, default=16)
     ap.add_argument("--elites", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")

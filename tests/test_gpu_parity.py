@@ -627,7 +627,7 @@ def test_dfs_symmetry_reduction_matches_oracle(sat, torch, n_lrs, nodes):
 # ------------------------------------------------------------------ bench scale
 @pytest.mark.parametrize("name", ["TXT", "MIX", "SWEEP"])
 def test_bench_scale_search_sampled_replay(sat, torch, name):
-    """The launch configuration bench.py times (P = 2^22 genomes, E = 16, epochs of 8,
+    """The launch configuration bench.py times (P = 2^23 genomes, E = 16, epochs of 8,
     seed 2309) at BASELINE.json's full sizes: generation 16 is checked against the oracle on
     sampled slots -- every sampled child is rebuilt from generation 15 by oga.make_child and
     decoded by the C oracle; the 16 elites are generation 15's best (ms, slot); every genome
@@ -637,7 +637,7 @@ def test_bench_scale_search_sampled_replay(sat, torch, name):
     c = oracle.compact(inst.node_gpus, inst.runtime)
     # SWEEP (T = 100: parent B read from global memory, the LOX bit set in shared memory) at
     # 2^20 genomes to bound the host copies (2 x 200 MB) and the Python replay
-    P, E, seed = (1 << 22) if name != "SWEEP" else (1 << 20), 16, 2309
+    P, E, seed = (1 << 23) if name != "SWEEP" else (1 << 20), 16, 2309
     base = dict(seed=seed, population=P, elites=E, generations_per_epoch=8)
     px, pc, pm = oga.q32(0.9), oga.q32(0.5), oga.q32(0.5)
     plan = _plan(sat, inst)
