@@ -99,12 +99,13 @@ __device__ __forceinline__ void scatter_node(int (&a)[NN][GP], const int (&x)[GP
   }
 }
 
-#ifndef SAT_SHIFT_PMAD
-#define SAT_SHIFT_PMAD 1   // 0: every shift lane as a two-IMAD select (r1 design, A/B switch)
-#endif
-
 // In-place update of one node's sorted free-time vector after placing (g, R) at its
 // g-th smallest free time.  Returns s + R.  `one` = Problem::one.
+// The barrel shift is all on the FMA pipe (the decode's binding pipe is the ALU: VIMNMX /
+// ISETP / SEL): b[i] <- b[i + sh] in place (ascending i reads lanes this stage has not
+// written), lanes past the end shift in +inf; the first stage's lanes still read x, so they
+// are two-source selects (the IMAD pair).  r1 ran every lane as an IMAD pair and the +inf
+// lanes as ALU selects: 84 instead of 72 SASS per one-node step.
 template <int GP>
 __device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R, int one) {
   const int k = g - 1;
@@ -114,28 +115,15 @@ __device__ __forceinline__ int place_sorted(int (&x)[GP], int g, int R, int one)
   int stage = 0;
 #pragma unroll
   for (int sh = 1; sh < GP; sh <<= 1, ++stage) {
-    [[maybe_unused]] const bool on = (k & sh) != 0;
     const int p = (k >> stage) & 1;
 #pragma unroll
     for (int i = 0; i < GP; ++i) {
-      if constexpr (SAT_SHIFT_PMAD) {
-        // All on the FMA pipe (the decode's binding pipe is the ALU: VIMNMX / ISETP / SEL).
-        // b[i] <- b[i + sh] in place (ascending i reads lanes this stage has not written);
-        // lanes past the end shift in +inf.  The first stage's lanes still read x, so they
-        // are two-source selects (the IMAD pair).
-        if (stage == 0)
-          b[i] = sel_fma(p, b[i], (i + sh >= GP) ? INF : b[i + sh]);
-        else if (i + sh >= GP)
-          pinf_fma(b[i], k & sh, one - 1);
-        else
-          pmov_fma(b[i], b[i + sh], k & sh, one);
-      } else {
-        // r1: every stage on the FMA pipe as IMAD pairs, +inf lanes as ALU selects
-        if (i + sh >= GP)
-          b[i] = on ? INF : b[i];
-        else
-          b[i] = sel_fma(p, b[i], b[i + sh]);
-      }
+      if (stage == 0)
+        b[i] = sel_fma(p, b[i], (i + sh >= GP) ? INF : b[i + sh]);
+      else if (i + sh >= GP)
+        pinf_fma(b[i], k & sh, one - 1);
+      else
+        pmov_fma(b[i], b[i + sh], k & sh, one);
     }
   }
   const int s = b[0];
