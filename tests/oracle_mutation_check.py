@@ -3,7 +3,10 @@
 Each mutation plants one plausible mistake in an oracle source (a wrong GPU rule, a wrong
 tie-break, an off-by-one, a dropped max, a transposed radix in oracle/saturn_oracle.c; a
 non-strict acceptance, a wrong tie-break or a dropped move family in oracle/local_search.py;
-Sattolo's shuffle, a skipped swap or a short config range in oracle/ga.py:initial_genome)
+Sattolo's shuffle, a skipped swap or a short config range in oracle/ga.py:initial_genome;
+a reversed tournament or tie-break, a flipped crossover bit, unswapped child roles, a
+reversed LOX fill or unordered cuts, a wrong insertion target or shared child fields in
+oracle/ga.py:make_child)
 and confirms that the `-m "not gpu"` pins of that source fail.  The original source is
 restored afterwards.  Result for this round is recorded in DESIGN.md ("Oracle pins").
 """
@@ -20,6 +23,7 @@ GA_SRC = "oracle/ga.py"
 LB_SRC = "oracle/bounds.py"
 PINS = "tests/test_oracle_pins.py"
 SEARCH_PINS = "tests/test_oracle_search_pins.py"
+GA_PINS = "tests/test_oracle_ga_pins.py"
 
 MUTATIONS = [
     (C_SRC, PINS, "gpu rule smallest-free", "f > free_t[first[best_n] + pick]", "f < free_t[first[best_n] + pick]"),
@@ -42,6 +46,19 @@ MUTATIONS = [
     (GA_SRC, SEARCH_PINS, "last swap skipped", "for i in range(T - 1, 0, -1):", "for i in range(T - 1, 1, -1):"),
     (GA_SRC, SEARCH_PINS, "config range short by one", "cfg = [st.below(int(S[t])) for t in range(T)]",
      "cfg = [st.below(max(int(S[t]) - 1, 1)) for t in range(T)]"),
+    (GA_SRC, GA_PINS, "tournament picks the larger key", "return i if (int(ms[i]), i) < (int(ms[j]), j) else j",
+     "return i if (int(ms[i]), i) > (int(ms[j]), j) else j"),
+    (GA_SRC, GA_PINS, "tournament tie -> larger slot", "return i if (int(ms[i]), i) < (int(ms[j]), j) else j",
+     "return i if (int(ms[i]), -i) < (int(ms[j]), -j) else j"),
+    (GA_SRC, GA_PINS, "crossover bit sense flipped", "if not (w[xbit_word(t // 32)] >> (t % 32)) & 1:",
+     "if (w[xbit_word(t // 32)] >> (t % 32)) & 1:"),
+    (GA_SRC, GA_PINS, "second child not role-swapped", "(a_idx, b_idx) if r == 0 else (b_idx, a_idx)",
+     "(a_idx, b_idx)"),
+    (GA_SRC, GA_PINS, "LOX fills in reverse order", "fill = [x for x in B_perm if x not in kept]",
+     "fill = [x for x in reversed(B_perm) if x not in kept]"),
+    (GA_SRC, GA_PINS, "LOX cuts not ordered", "if a > b:\n            a, b = b, a", "if a < b:\n            a, b = b, a"),
+    (GA_SRC, GA_PINS, "insertion back at its own position", "child_perm.insert(j, x)", "child_perm.insert(i, x)"),
+    (GA_SRC, GA_PINS, "both children use child 0's fields", "c = 8 + 4 * r", "c = 8"),
     (LB_SRC, PINS, "knapsack capacity one too many", "best = [0.0] * (cap + 1)\n    choice = [[] for _ in range(cap + 1)]",
      "cap = cap + 1\n    best = [0.0] * (cap + 1)\n    choice = [[] for _ in range(cap + 1)]"),
     (LB_SRC, PINS, "job progress counted twice", "A[nK + t, j] = -1.0 / jobs[t][s][1]",
