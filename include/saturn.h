@@ -266,6 +266,35 @@ saturn_status saturn_improve(saturn_plan *p, uint8_t *h_cfg, uint8_t *h_perm, in
 saturn_status saturn_search_population(const saturn_plan *p, int64_t capacity, uint8_t *h_cfg, uint8_t *h_perm,
                                        int32_t *h_makespan, int64_t *n_out);
 
+/* Search-state checkpoint / resume (SURVEY.md §5 "Checkpoint / resume": a search is
+ * deterministic and restartable from (seed, generation, population); the paper checkpoints
+ * jobs at plan switches).  The state of the last search (or resume) on
+ * this handle is a flat host byte buffer: a header (magic "SATSRCH1", T, record stride,
+ * population P, elites E, island rank / world, seed, generation reached, an FNV-1a hash of
+ * the cluster and runtime table, an FNV-1a hash of the payload), then the population
+ * records [P][stride], their makespans int32 [P], the elite makespans int32 [E] and the
+ * elite records [E][stride].
+ *
+ * saturn_search_save: with h_state NULL only *bytes_out is set; otherwise the state is
+ * written to h_state (caller-owned host memory of `capacity` bytes; EINVAL if too small).
+ * ESTATE before a search.  Synchronous.
+ *
+ * saturn_search_resume: continue a saved search on a handle with the same cluster and
+ * runtime table (any handle on any device; EINVAL otherwise): sp->seed, population and
+ * elites must equal the saved ones, the state's island / world must equal this handle's
+ * rank / world, and every saved genome must be valid (EINVAL otherwise; also for a bad
+ * magic, size or checksum).  sp->max_generations MORE generations are run, numbered from
+ * the saved generation + 1 (their Philox streams and epoch boundaries are those the saved
+ * search would have used next); sp->seed_cfg / n_seed are ignored.  For one island without
+ * the memetic step, search(G1) + save + resume(G2) returns exactly what search(G1 + G2)
+ * returns (final population, elites, best plan).  (With several islands or a memetic step
+ * the saved state is taken after the search's final exchange, which the continuous search
+ * does not run at generation G1.)  out->generations = generations run by this call.
+ * Synchronous. */
+saturn_status saturn_search_save(const saturn_plan *p, void *h_state, uint64_t capacity, uint64_t *bytes_out);
+saturn_status saturn_search_resume(saturn_plan *p, const void *h_state, uint64_t bytes,
+                                   const saturn_search_params *sp, void *stream, saturn_result *out);
+
 /* The best plan of the last enumerate/search (row a8): placements host [T] (job-id order),
  * genome_out host [2T] (cfg then perm) or NULL, makespan.  ESTATE before any search. */
 saturn_status saturn_best_plan(saturn_plan *p, saturn_placement *out, uint8_t *genome_out, int64_t *makespan);

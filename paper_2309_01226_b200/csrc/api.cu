@@ -168,6 +168,11 @@ struct saturn_plan {
   int last_pop = 0;
   int64_t pop_P = 0;
   int pop_GS = 0;
+  // the last search's position (saturn_search_save / saturn_search_resume)
+  int64_t last_gen = 0;
+  uint64_t last_seed = 0;
+  int last_E = 0, last_world = 1;
+  uint32_t last_island = 0;
   std::vector<double> hist_t;
   std::vector<int64_t> hist_ms;
   // best-so-far records in flight: async D2H copies into pinned slots + an event each, read
@@ -983,6 +988,8 @@ struct Island {
   int cur = 0;
   int64_t n_prof = 0, n_timed = 0;
   double t0 = 0;
+  const uint8_t* resume = nullptr;   // saved state payload (saturn_search_resume), or none
+  int64_t gen0 = 0;                  // generation the state was saved at
 
   saturn_status validate() {
     if (!p->loaded) return fail(p, SATURN_ESTATE, "search before load_runtime_table");
@@ -1037,7 +1044,7 @@ struct Island {
     CU(p, p->rec_gen.ensure((size_t)E * GS));
     CU(p, p->all_ms.ensure((size_t)E * world));
     CU(p, p->all_gen.ensure((size_t)E * GS * world));
-    const int64_t n_seed = std::min<int64_t>(sp->n_seed, P);
+    const int64_t n_seed = resume ? 0 : std::min<int64_t>(sp->n_seed, P);
     if (n_seed > 0) {
       std::vector<uint8_t> packed((size_t)n_seed * GS, 0);
       for (int64_t i = 0; i < n_seed; ++i) {
@@ -1058,12 +1065,26 @@ struct Island {
     gp.px = sp->p_xover_q32;
     gp.pc = sp->p_cfg_mut_q32;
     gp.pm = sp->p_perm_mut_q32;
-    evaluated = (uint64_t)P;
     cur = 0;
-    CU(p, sat::launch_ga_init(p->pb, NN, GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p,
-                              p->pms[0].p, p->cand.p, p->n_cand.p, p->sms, st));
-    CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
-    p->stats.kernel_launches += 2;
+    if (resume) {   // population, makespans and elite records as saved (payload order)
+      gp.gen = (uint32_t)gen0;
+      evaluated = 0;
+      const uint8_t* q = resume;
+      CU(p, cudaMemcpyAsync(p->pop[0].p, q, (size_t)P * GS, cudaMemcpyHostToDevice, st));
+      q += (size_t)P * GS;
+      CU(p, cudaMemcpyAsync(p->pms[0].p, q, (size_t)P * 4, cudaMemcpyHostToDevice, st));
+      q += (size_t)P * 4;
+      CU(p, cudaMemcpyAsync(p->rec_ms.p, q, (size_t)E * 4, cudaMemcpyHostToDevice, st));
+      q += (size_t)E * 4;
+      CU(p, cudaMemcpyAsync(p->rec_gen.p, q, (size_t)E * GS, cudaMemcpyHostToDevice, st));
+      p->stats.h2d_bytes += (int64_t)((size_t)P * (GS + 4) + (size_t)E * (GS + 4));
+    } else {
+      evaluated = (uint64_t)P;
+      CU(p, sat::launch_ga_init(p->pb, NN, GP, gp, n_seed ? p->seeds.p : nullptr, n_seed, p->pop[0].p,
+                                p->pms[0].p, p->cand.p, p->n_cand.p, p->sms, st));
+      CU(p, sat::launch_select(p->cand.p, p->n_cand.p, E, GS, p->pop[0].p, p->rec_ms.p, p->rec_gen.p, st));
+      p->stats.kernel_launches += 2;
+    }
     // profiling: event triples around every `profiling`-th GA generation kernel (at most 512
     // per search).  An event record between kernels costs a few microseconds of drain, so
     // sampling keeps the instrumented step within ~1 % of the uninstrumented one.
@@ -1177,6 +1198,11 @@ struct Island {
     p->last_pop = cur;
     p->pop_P = P;
     p->pop_GS = GS;
+    p->last_gen = gen0 + gens_run;
+    p->last_seed = sp->seed;
+    p->last_E = E;
+    p->last_island = island;
+    p->last_world = world;
     if (out) {
       memset(out, 0, sizeof *out);
       out->makespan = best;
@@ -1191,15 +1217,22 @@ struct Island {
 
 }  // namespace
 
-saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out) {
-  if (p && host_only(p)) return SATURN_ESTATE;
-  if (!p) return SATURN_EINVAL;
+namespace {
+
+// The search loop of saturn_search; with `resume` the island starts from a saved state at
+// generation gen0 (population, makespans, elites) instead of generation 0, and runs
+// generations gen0+1 .. gen0+max_generations -- the Philox streams, epoch boundaries and
+// exchanges of those generations are the ones the saved search would have run next.
+saturn_status search_run(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out,
+                         const uint8_t* resume, int64_t gen0) {
   Island is;
   is.p = p;
   is.sp = sp;
   is.st = static_cast<cudaStream_t>(stream);
   is.island = (uint32_t)p->rank;
   is.world = distributed(p) ? p->world : 1;
+  is.resume = resume;
+  is.gen0 = gen0;
   saturn_status s;
   if ((s = is.validate()) != SATURN_OK) return s;
   if ((s = is.begin()) != SATURN_OK) return s;
@@ -1240,12 +1273,12 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
   };
   {
     Nvtx r("saturn_search: initial population + exchange");
-    if ((s = exchange()) != SATURN_OK) return s;
+    if (!resume && (s = exchange()) != SATURN_OK) return s;   // a saved state is post-exchange
     if ((s = is.record()) != SATURN_OK) return s;
   }
-  int64_t gen = 1;
+  int64_t gen = gen0 + 1;
   std::unique_ptr<Nvtx> epoch;
-  for (; gen <= sp->max_generations; ++gen) {
+  for (; gen <= gen0 + sp->max_generations; ++gen) {
     if (!epoch) epoch.reset(new Nvtx("saturn_search: epoch"));
     if ((s = is.generation(gen)) != SATURN_OK) return s;
     if (gen % sp->generations_per_epoch == 0) {
@@ -1284,11 +1317,134 @@ saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void
     }
   }
   epoch.reset();
-  const int64_t gens_run = gen - 1;
+  const int64_t gens_run = gen - 1 - gen0;
   Nvtx r("saturn_search: final exchange");
   if ((s = exchange()) != SATURN_OK) return s;
   if ((s = is.record()) != SATURN_OK) return s;
   return is.finish(gens_run, is.evaluated * (uint64_t)is.world, out);
+}
+
+// Saved search state: this header, then the payload -- population [P][GS] (genome records),
+// makespans int32 [P], elite makespans int32 [E], elite records [E][GS].
+struct SearchStateHeader {
+  char magic[8];          // "SATSRCH1"
+  int32_t T, GS;
+  int64_t P;
+  int32_t E, world;
+  uint32_t island, reserved;
+  uint64_t seed;
+  int64_t generation;
+  uint64_t table_hash;    // FNV-1a of the cluster and the loaded runtime table
+  uint64_t payload_hash;  // FNV-1a of the payload
+  uint64_t payload_bytes;
+};
+static_assert(sizeof(SearchStateHeader) == 80, "state header layout is part of the ABI");
+constexpr char kStateMagic[8] = {'S', 'A', 'T', 'S', 'R', 'C', 'H', '1'};
+
+uint64_t fnv1a(const void* d, size_t n, uint64_t h = 1469598103934665603ull) {
+  const uint8_t* b = static_cast<const uint8_t*>(d);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+uint64_t table_hash(const saturn_plan* p) {
+  const int32_t dims[4] = {p->T, p->U, p->Gmax, (int32_t)p->gpu_n.size()};
+  uint64_t h = fnv1a(dims, sizeof dims);
+  h = fnv1a(p->gpu_n.data(), p->gpu_n.size() * sizeof(int), h);
+  return fnv1a(p->dense.data(), p->dense.size() * sizeof(int32_t), h);
+}
+uint64_t state_payload_bytes(int64_t P, int E, int GS) {
+  return (uint64_t)P * (uint64_t)(GS + 4) + (uint64_t)E * (uint64_t)(GS + 4);
+}
+
+}  // namespace
+
+saturn_status saturn_search(saturn_plan* p, const saturn_search_params* sp, void* stream, saturn_result* out) {
+  if (p && host_only(p)) return SATURN_ESTATE;
+  if (!p) return SATURN_EINVAL;
+  return search_run(p, sp, stream, out, nullptr, 0);
+}
+
+saturn_status saturn_search_save(const saturn_plan* pc, void* h_state, uint64_t capacity, uint64_t* bytes_out) {
+  saturn_plan* p = const_cast<saturn_plan*>(pc);
+  if (!p) return SATURN_EINVAL;
+  if (!p->have_pop) return fail(p, SATURN_ESTATE, "no search state on this handle");
+  const int64_t P = p->pop_P;
+  const int E = p->last_E, GS = p->pop_GS;
+  const uint64_t payload = state_payload_bytes(P, E, GS), total = sizeof(SearchStateHeader) + payload;
+  if (bytes_out) *bytes_out = total;
+  if (!h_state) return SATURN_OK;
+  if (capacity < total)
+    return fail(p, SATURN_EINVAL, "capacity %llu < state size %llu", (unsigned long long)capacity,
+                (unsigned long long)total);
+  DeviceGuard dg(p->device);
+  SearchStateHeader h{};
+  memcpy(h.magic, kStateMagic, 8);
+  h.T = p->T;
+  h.GS = GS;
+  h.P = P;
+  h.E = E;
+  h.world = p->last_world;
+  h.island = p->last_island;
+  h.seed = p->last_seed;
+  h.generation = p->last_gen;
+  h.table_hash = table_hash(p);
+  h.payload_bytes = payload;
+  uint8_t* q = static_cast<uint8_t*>(h_state) + sizeof h;
+  const int b = p->last_pop;
+  CU(p, cudaMemcpy(q, p->pop[b].p, (size_t)P * GS, cudaMemcpyDeviceToHost));
+  CU(p, cudaMemcpy(q + (size_t)P * GS, p->pms[b].p, (size_t)P * 4, cudaMemcpyDeviceToHost));
+  CU(p, cudaMemcpy(q + (size_t)P * (GS + 4), p->rec_ms.p, (size_t)E * 4, cudaMemcpyDeviceToHost));
+  CU(p, cudaMemcpy(q + (size_t)P * (GS + 4) + (size_t)E * 4, p->rec_gen.p, (size_t)E * GS, cudaMemcpyDeviceToHost));
+  p->stats.d2h_bytes += (int64_t)payload;
+  h.payload_hash = fnv1a(q, payload);
+  memcpy(h_state, &h, sizeof h);
+  return SATURN_OK;
+}
+
+saturn_status saturn_search_resume(saturn_plan* p, const void* h_state, uint64_t bytes,
+                                   const saturn_search_params* sp, void* stream, saturn_result* out) {
+  if (p && host_only(p)) return SATURN_ESTATE;
+  if (!p || !sp) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "resume before load_runtime_table");
+  if (!h_state || bytes < sizeof(SearchStateHeader)) return fail(p, SATURN_EINVAL, "state buffer too small");
+  SearchStateHeader h;
+  memcpy(&h, h_state, sizeof h);
+  if (memcmp(h.magic, kStateMagic, 8) != 0) return fail(p, SATURN_EINVAL, "not a saturn search state");
+  const int T = p->T, GS = gs_of(T);
+  if (h.T != T || h.GS != GS) return fail(p, SATURN_EINVAL, "state has T=%d, the table has T=%d", h.T, T);
+  if (h.table_hash != table_hash(p)) return fail(p, SATURN_EINVAL, "state was saved with another cluster or table");
+  if (h.P < 1 || h.E < 1 || h.payload_bytes != state_payload_bytes(h.P, h.E, GS) ||
+      bytes != sizeof h + h.payload_bytes)
+    return fail(p, SATURN_EINVAL, "state size mismatch");
+  const uint8_t* q = static_cast<const uint8_t*>(h_state) + sizeof h;
+  if (fnv1a(q, h.payload_bytes) != h.payload_hash) return fail(p, SATURN_EINVAL, "state payload checksum mismatch");
+  if (sp->population != h.P || sp->elites != h.E || sp->seed != h.seed)
+    return fail(p, SATURN_EINVAL, "params (seed, population, elites) differ from the saved search's");
+  const int world = distributed(p) ? p->world : 1;
+  if (h.world != world || h.island != (uint32_t)p->rank)
+    return fail(p, SATURN_EINVAL, "state is island %u of %d; this handle is rank %d of %d", h.island, h.world,
+                p->rank, world);
+  if (h.generation < 0 || h.generation + sp->max_generations >= (int64_t(1) << 32))
+    return fail(p, SATURN_EINVAL, "generation counter out of range");
+  // every genome of the population and of the elite records must be valid (the decoder
+  // indexes the staged table with them)
+  const int Tp = sat::perm_offset(T);
+  auto valid = [&](const uint8_t* g) {
+    uint32_t seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < T; ++k) {
+      const int t = g[Tp + k];
+      if (t >= T || (seen[t >> 5] >> (t & 31)) & 1u) return false;
+      seen[t >> 5] |= 1u << (t & 31);
+      if (g[t] >= p->S[t]) return false;
+    }
+    return true;
+  };
+  for (int64_t i = 0; i < h.P; ++i)
+    if (!valid(q + (size_t)i * GS)) return fail(p, SATURN_EINVAL, "state genome %lld is invalid", (long long)i);
+  const uint8_t* rec = q + (size_t)h.P * (GS + 4) + (size_t)h.E * 4;
+  for (int i = 0; i < h.E; ++i)
+    if (!valid(rec + (size_t)i * GS)) return fail(p, SATURN_EINVAL, "state elite %d is invalid", i);
+  return search_run(p, sp, stream, out, q, h.generation);
 }
 
 saturn_status saturn_search_group(saturn_plan** plans, int32_t k, const saturn_search_params* sp, void** streams,

@@ -775,6 +775,12 @@ __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t
 #ifndef SAT_GA_L2PF
 #define SAT_GA_L2PF 1   // long genomes: L2 prefetch of the next pair's parent records
 #endif
+#ifndef SAT_GA_L2PF_SHORT
+#define SAT_GA_L2PF_SHORT 0   // the same for short genomes (A/B)
+#endif
+#ifndef SAT_GA_VEC
+#define SAT_GA_VEC 1   // long genomes on register states: parents read by 16-byte loads
+#endif
 
 template <int NN, int GP>
 struct GaMinBlocks {
@@ -1008,18 +1014,46 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         };
         if (!LONGT) {
           for (int t = 0; t < T; t += 4) mix(t, w1.z);
-        } else {   // 32 genes per crossover word; the parents' 8 words of a block loaded together
+        } else {   // 32 genes per crossover word; the parents' 8 words of a block as two
+                   // 16-byte loads each (records are 16-byte aligned; ceil(T/32)*32 <= GS)
           for (int t0 = 0; t0 < T; t0 += 32) {
             const int k = t0 >> 5;
             const uint32_t bits =
                 k == 0 ? w1.z : (k == 1 ? w1.w : philox_word(k0, k1, (uint32_t)q, gp.gen, c2, 16u + (k - 2)));
+#if SAT_GA_VEC
+            const uint4* x4 = reinterpret_cast<const uint4*>(X) + 2 * k;
+            const uint4* y4 = reinterpret_cast<const uint4*>(Y) + 2 * k;
+            const uint4 xa = x4[0], xb = x4[1], ya = y4[0], yb = y4[1];
+            const uint32_t xw[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+            const uint32_t yw[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (t0 + 4 * j < T) {
+                const uint32_t nib = xo ? (~(bits >> (4 * j)) & 0xfu) : 0u;
+                const uint32_t m = ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
+                cw[(t0 >> 2) + j] = (xw[j] & ~m) | (yw[j] & m);
+              }
+#else
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               if (t0 + 4 * j < T) mix(t0 + 4 * j, bits);
+#endif
           }
         }
+        if (!LONGT || !SAT_GA_VEC) {
 #pragma unroll 4
-        for (int w = 0; w < nw; ++w) cw[(Tp >> 2) + w] = cx[(Tp >> 2) + w];
+          for (int w = 0; w < nw; ++w) cw[(Tp >> 2) + w] = cx[(Tp >> 2) + w];
+        } else {   // X's permutation words by 16-byte loads from the aligned word below Tp
+          const uint4* x4 = reinterpret_cast<const uint4*>(X);
+          const int w0 = Tp >> 2, w1e = w0 + nw;
+          for (int u = w0 >> 2; 4 * u < w1e; ++u) {
+            const uint4 v = x4[u];
+            const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (4 * u + e >= w0 && 4 * u + e < w1e) cw[4 * u + e] = vw[e];
+          }
+        }
       }
       // 4. LOX: keep X.perm[a..b] in place; fill positions 0..a-1, then b+1..T-1, with Y's
       //    genes in Y's order from position 0, skipping the slice's genes.
@@ -1084,6 +1118,18 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
               for (int e = 0; e < 4; ++e)
                 if (k + e < T) fill((int)((y4 >> (8 * e)) & 0xffu));
             }
+          } else if (SAT_GA_VEC) {   // Y's permutation 16 genes per load (aligned below Tp)
+            const uint4* y4 = reinterpret_cast<const uint4*>(Y);
+            const int g0 = Tp & ~15;
+            for (int u = g0 >> 4; 16 * u < Tp + T; ++u) {
+              const uint4 v = child ? y4[u] : make_uint4(0u, 0u, 0u, 0u);
+              const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const int k = 16 * u + e - Tp;
+                if (k >= 0 && k < T) fill((int)((vw[e >> 2] >> (8 * (e & 3))) & 0xffu));
+              }
+            }
           } else {
             for (int k = 0; k < T; ++k) fill(child ? Yq[k] : 0);
           }
@@ -1128,7 +1174,7 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       }
       topE_insert(lst, in ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull, gp.E, cap);
     }
-    if constexpr (LONGT && SAT_GA_L2PF) {
+    if constexpr ((LONGT && SAT_GA_L2PF) || (!LONGT && SAT_GA_L2PF_SHORT)) {
       // The next pair's tournaments are decided now (their makespans arrived during this
       // pair's decodes) and both winners' records are pulled into L2: long genomes read
       // their parents straight from the population (an HBM-sized array), and the

@@ -28,7 +28,7 @@ EXPORTS = (
     "saturn_plan_create", "saturn_workspace_bytes", "saturn_bind_workspace", "saturn_load_runtime_table", "saturn_num_configs", "saturn_config",
     "saturn_set_decoder", "saturn_evaluate", "saturn_evaluate_nodes", "saturn_evaluate_host", "saturn_trace", "saturn_space_size",
     "saturn_enumerate", "saturn_enumerate_range", "saturn_set_enumeration_options", "saturn_search", "saturn_search_group", "saturn_search_history",
-    "saturn_search_population", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
+    "saturn_search_population", "saturn_search_save", "saturn_search_resume", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_plan_attach_peers", "saturn_plan_barrier",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
     "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_improve", "saturn_last_error",
@@ -136,6 +136,8 @@ def load_library(path: str = LIB_PATH):
         "saturn_search_group": [P(vp), i32, P(SearchParams), P(vp), P(Result)],
         "saturn_search_history": [h, i64, P(ctypes.c_double), P(i64), P(i64)],
         "saturn_search_population": [h, i64, P(u8), P(u8), P(i32), P(i64)],
+        "saturn_search_save": [h, vp, u64, P(u64)],
+        "saturn_search_resume": [h, vp, u64, P(SearchParams), vp, P(Result)],
         "saturn_workspace_bytes": [h, vp, P(u64)],
         "saturn_bind_workspace": [h, vp, u64],
         "saturn_best_plan": [h, P(Placement), P(u8), P(i64)],
@@ -424,6 +426,26 @@ class Plan:
         self._check(self._lib.saturn_search(self._h, ctypes.byref(sp), self._stream(stream), ctypes.byref(r)),
                     "saturn_search")
         del keep
+        return r.as_dict()
+
+    def search_save(self) -> np.ndarray:
+        """saturn_search_save: the last search's state as a host uint8 buffer."""
+        n = ctypes.c_uint64()
+        self._check(self._lib.saturn_search_save(self._h, None, 0, ctypes.byref(n)), "saturn_search_save")
+        buf = np.zeros(n.value, np.uint8)
+        self._check(self._lib.saturn_search_save(self._h, buf.ctypes.data_as(ctypes.c_void_p), buf.nbytes,
+                                                 ctypes.byref(n)), "saturn_search_save")
+        return buf
+
+    def search_resume(self, state, cfg: SearchConfig, stream=None) -> dict:
+        """saturn_search_resume: run cfg.max_generations more generations from a saved state
+        (cfg.seed / population / elites must be the saved search's)."""
+        st = np.ascontiguousarray(state, dtype=np.uint8)
+        sp = self._search_params(cfg)
+        r = Result()
+        self._check(self._lib.saturn_search_resume(self._h, st.ctypes.data_as(ctypes.c_void_p), st.nbytes,
+                                                   ctypes.byref(sp), self._stream(stream), ctypes.byref(r)),
+                    "saturn_search_resume")
         return r.as_dict()
 
     def improve(self, cfg, perm, iters: int = 8, stream=None):

@@ -74,6 +74,8 @@ def test_null_and_bad_arguments_never_crash(lib):
     assert lib.saturn_evaluate(None, None, None, 1, None, None) == sat.EINVAL
     assert lib.saturn_search(None, None, None, None) == sat.EINVAL
     assert lib.saturn_best_plan(None, None, None, None) == sat.EINVAL
+    assert lib.saturn_search_save(None, None, 0, None) == sat.EINVAL
+    assert lib.saturn_search_resume(None, None, 0, None, None, None) == sat.EINVAL
     assert lib.saturn_last_error(None) == b"NULL handle"
     lib.saturn_plan_destroy(None)
 
@@ -169,3 +171,16 @@ def test_c_example_compiles_and_links(lib, tmp_path):
     import torch
     if not torch.cuda.is_available():
         assert r.returncode == 2 and "saturn_plan_create" in r.stderr
+
+
+def test_search_state_calls_on_a_host_only_handle(lib):
+    """saturn_search_save before any search -> ESTATE; saturn_search_resume on a host-only
+    handle (no device) -> ESTATE, whatever the buffer holds."""
+    p = _host([8])
+    p.load_runtime_table(np.ones((3, 1, 8), np.int32) * 7)
+    with pytest.raises(sat.SaturnError) as e:
+        p.search_save()
+    assert e.value.status == sat.ESTATE
+    with pytest.raises(sat.SaturnError) as e:
+        p.search_resume(np.zeros(128, np.uint8), sat.SearchConfig(seed=1, population=64, elites=4))
+    assert e.value.status == sat.ESTATE
