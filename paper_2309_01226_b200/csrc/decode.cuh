@@ -26,6 +26,10 @@
 
 namespace sat {
 
+#ifndef SAT_NODE_KEYS
+#define SAT_NODE_KEYS 1   // multi-node register states hold (t << 2 | node) keys
+#endif
+
 // a[k] for a runtime k in [0, GP): binary mux tree on the bits of k (GP-1 selects).
 template <int GP>
 __device__ __forceinline__ int mux(const int (&a)[GP], int k) {
@@ -227,6 +231,11 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
   // Position 0 in closed form: every GPU is free at 0, so the first job starts at 0 on the
   // lowest node with >= g GPUs and (latest-free-first = all equal, lower ids first ... in the
   // multiset view: the g top slots of that node's GPU_n free ones) ends at R.
+  // Several nodes: every free time is held as a node KEY (t << 2 | n).  Keys of one node
+  // order like their times, so the sorted update runs on keys unchanged (with R << 2), and
+  // the earliest start over the nodes with ties to the lowest node id is a plain min of the
+  // nodes' g-th keys -- its low bits are the node (no compare / select chain).
+  constexpr int KS = (NN >= 2 && SAT_NODE_KEYS) ? 2 : 0;
   int a[NN][GP];
   int ms;
   {
@@ -244,10 +253,11 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
       for (int n = 0; n < NN; ++n) {
         const int gn = n < pb.N ? pb.gpu_n[n] : 0;
 #pragma unroll
-        for (int i = 0; i < GP; ++i) a[n][i] = (i < gn) ? ((n == bn && i >= gn - g) ? R : 0) : INF;
+        for (int i = 0; i < GP; ++i)
+          a[n][i] = (i < gn) ? ((((n == bn && i >= gn - g) ? R : 0) << KS) | (KS ? n : 0)) : INF;
       }
     }
-    ms = R;
+    ms = R << KS;
   }
   // Positions 1 .. T-2: the full update.  The next position's config word is fetched one
   // step ahead (its three dependent shared-memory loads -- perm byte, cfg byte, table word
@@ -271,16 +281,22 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
       // start of every node: its g-th smallest free time (+inf if it has fewer GPUs)
       int best = mux<GP>(a[0], g - 1);
       int bn = 0;
+      if constexpr (KS) {
 #pragma unroll
-      for (int n = 1; n < NN; ++n) {
-        const int st = mux<GP>(a[n], g - 1);
-        const bool lt = st < best;   // strict: ties keep the lowest node id
-        best = lt ? st : best;
-        bn = lt ? n : bn;
+        for (int n = 1; n < NN; ++n) best = min(best, mux<GP>(a[n], g - 1));
+        bn = best & 3;
+      } else {
+#pragma unroll
+        for (int n = 1; n < NN; ++n) {
+          const int st = mux<GP>(a[n], g - 1);
+          const bool lt = st < best;   // strict: ties keep the lowest node id
+          best = lt ? st : best;
+          bn = lt ? n : bn;
+        }
       }
       int x[GP];
       gather_node<NN, GP>(x, a, bn, pb.one);
-      v = place_sorted<GP>(x, g, R, pb.one);
+      v = place_sorted<GP>(x, g, R << KS, pb.one);
       scatter_node<NN, GP>(a, x, bn, pb.one);
     }
     if constexpr (TRACK_MS) ms = max(ms, v);
@@ -292,6 +308,7 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
 #pragma unroll
     for (int n = 0; n < NN; ++n) ms = max(ms, a[n][GP - 1]);
   }
+  ms >>= KS;
   // Position T-1 (its word is in w): only its end matters (no later job reads the state):
   // earliest start + R.
   if (T > 1) {
@@ -300,7 +317,7 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
     int best = mux<GP>(a[0], g - 1);
 #pragma unroll
     for (int n = 1; n < NN; ++n) best = min(best, mux<GP>(a[n], g - 1));
-    ms = max(ms, best + R);
+    ms = max(ms, (best >> KS) + R);
   }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;
   if constexpr (CHECK != 0) {

@@ -754,29 +754,37 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-// Copy a GS-byte global record into a smem row (4-byte stores) and back.
+#ifndef SAT_GA_CACHE_HINTS
+#define SAT_GA_CACHE_HINTS 1   // r2: TXT k_ga -1.8 %, MIX -1.9 %, DRAM reads -14 % per launch
+#endif
+// Copy a GS-byte global record into a smem row (4-byte stores) and back.  STREAM: the
+// record is read / written with the evict-first hint (ld/st .cs), so the population records
+// (2 x P x GS bytes per generation, > L2) do not push the makespan array out of L2.
+template <bool STREAM = false>
 __device__ __forceinline__ void load_row(uint8_t* row, const uint8_t* __restrict__ g, int GS) {
   const uint4* src = reinterpret_cast<const uint4*>(g);
   uint32_t* d = reinterpret_cast<uint32_t*>(row);
   for (int k = 0; k < GS / 16; ++k) {
-    const uint4 v = src[k];
+    const uint4 v = STREAM ? __ldcs(src + k) : src[k];
     d[4 * k] = v.x;
     d[4 * k + 1] = v.y;
     d[4 * k + 2] = v.z;
     d[4 * k + 3] = v.w;
   }
 }
+template <bool STREAM = false>
 __device__ __forceinline__ void store_row(uint8_t* __restrict__ g, const uint8_t* row, int GS) {
   uint4* dst = reinterpret_cast<uint4*>(g);
   const uint32_t* s = reinterpret_cast<const uint32_t*>(row);
-  for (int k = 0; k < GS / 16; ++k) dst[k] = make_uint4(s[4 * k], s[4 * k + 1], s[4 * k + 2], s[4 * k + 3]);
+  for (int k = 0; k < GS / 16; ++k) {
+    const uint4 v = make_uint4(s[4 * k], s[4 * k + 1], s[4 * k + 2], s[4 * k + 3]);
+    if (STREAM) __stcs(dst + k, v);
+    else dst[k] = v;
+  }
 }
 
 #ifndef SAT_GA_L2PF
 #define SAT_GA_L2PF 1   // long genomes: L2 prefetch of the next pair's parent records
-#endif
-#ifndef SAT_GA_L2PF_SHORT
-#define SAT_GA_L2PF_SHORT 0   // the same for short genomes (A/B)
 #endif
 #ifndef SAT_GA_VEC
 #define SAT_GA_VEC 1   // long genomes on register states: parents read by 16-byte loads
@@ -950,8 +958,8 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
     const uint8_t* gA = prev_pop + (uint64_t)A * GS;
     const uint8_t* gB = prev_pop + (uint64_t)B * GS;
     if (!LONGT && any) {
-      load_row(rowA, gA, GS);
-      load_row(rowB, gB, GS);
+      load_row<SAT_GA_CACHE_HINTS>(rowA, gA, GS);
+      load_row<SAT_GA_CACHE_HINTS>(rowB, gB, GS);
     }
     const bool xo = any && (w1.x & 0xffffu) < px16;
     uint32_t a = v16(w1.x >> 16, T), b = v16(w1.y & 0xffffu, T);
@@ -1169,12 +1177,12 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
       }
       if (child) msv = decode_T<NN, GP, GA_B, ga_mode(NN, GP), 0>(tab, S, pb.stride, ch, T, pb, ns);
       if (in) {
-        store_row(pop + (size_t)slot * GS, ch.base, GS);
+        store_row<SAT_GA_CACHE_HINTS>(pop + (size_t)slot * GS, ch.base, GS);
         ms_out[slot] = msv;
       }
       topE_insert(lst, in ? (((uint64_t)(uint32_t)msv << 32) | (uint64_t)slot) : ~0ull, gp.E, cap);
     }
-    if constexpr ((LONGT && SAT_GA_L2PF) || (!LONGT && SAT_GA_L2PF_SHORT)) {
+    if constexpr (LONGT && SAT_GA_L2PF) {   // (short genomes: measured +2.5 % TXT k_ga, r2)
       // The next pair's tournaments are decided now (their makespans arrived during this
       // pair's decodes) and both winners' records are pulled into L2: long genomes read
       // their parents straight from the population (an HBM-sized array), and the

@@ -1,16 +1,12 @@
 # scratch GPU call used during round 2 (edited per call)
 set -x
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_r2f.txt 2>&1; echo pytest=$?
-tail -3 gpurun_out/gputest_r2f.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_r2g.txt 2>&1; echo pytest=$?
+tail -3 gpurun_out/gputest_r2g.txt
 sed -i 's/population=1 << 22/population=1 << 23/' tools/variant_bench.py
-AB_WORKLOADS="TXT MIX SWEEP" timeout 1500 bash tools/ab_run.sh gpurun_out/ab_vec.jsonl build_variants/cur/libsaturn.so build_variants/novec/libsaturn.so build_variants/pfs/libsaturn.so
-tail -3 gpurun_out/ab_vec.jsonl.err
+AB_WORKLOADS="SWEEP" timeout 1500 bash tools/ab_run.sh gpurun_out/ab_keys.jsonl build_variants/cur/libsaturn.so build_variants/nokeys/libsaturn.so
+tail -3 gpurun_out/ab_keys.jsonl.err
 python - <<'PY'
 import json
-for l in open('gpurun_out/ab_vec.jsonl'):
+for l in open('gpurun_out/ab_keys.jsonl'):
     d=json.loads(l); print(d['lib'][-22:], d['workload'], 'eval %.4g' % d['evaluate_plans_per_s'], 'step %.4f' % d['step_ms'], 'kga %.4f' % d['ga_kernel_ms'], d['best'])
 PY
-for v in cur novec; do
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_ga --launch-skip 6 --launch-count 1 -o gpurun_out/prof_ga_sweep_$v python tools/variant_bench.py build_variants/$v/libsaturn.so SWEEP > /dev/null 2>&1
-done
-ls gpurun_out
