@@ -419,6 +419,10 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
                                           int stride, const G& gen, int T, const Problem& pb, int* ns,
                                           uint32_t* mask = nullptr, int mstride = 0) {
   constexpr int RW = col_rows(GP, RSHIFT);
+  // node keys (t << KS | n) as in decode_sorted: the argmin over the nodes is a min
+  // (a run-time node count needs 5 bits: times < 2^26 keep keys below 2^31 - 32 < INF).
+  // Measured r2: SWEEP 4x8 evaluate +1.7 %; two nodes -2.8 % (MIX) -- they keep times.
+  constexpr int KS = (NN == 1 || NN == 2 || !SAT_NODE_KEYS) ? 0 : (NN == 0 ? 5 : (NN <= 4 ? 2 : 3));
   const int N = NN ? NN : pb.N;
   bool bad = false;
   int maxt = 0;
@@ -454,7 +458,15 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
     const int* cg = ns + (g - 1) * B;
     int best = cg[0];
     bn = 0;
-    if constexpr (NN > 0) {
+    if constexpr (KS > 0) {
+      if constexpr (NN > 0) {
+#pragma unroll
+        for (int n = 1; n < NN; ++n) best = min(best, cg[n * RW * B]);
+      } else {
+        for (int n = 1; n < N; ++n) best = min(best, cg[n * RW * B]);
+      }
+      bn = best & ((1 << KS) - 1);
+    } else if constexpr (NN > 0) {
 #pragma unroll
       for (int n = 1; n < NN; ++n) {
         const int st = cg[n * RW * B];
@@ -488,9 +500,9 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
       const int lo = (n == bn) ? gn - g : gn;
       int* row = ns + n * RW * B;
 #pragma unroll
-      for (int j = 0; j < RW; ++j) row[j * B] = (j < gn) ? ((j >= lo) ? R : 0) : INF;
+      for (int j = 0; j < RW; ++j) row[j * B] = (j < gn) ? ((((j >= lo) ? R : 0) << KS) | (KS ? n : 0)) : INF;
     }
-    ms = R;
+    ms = R << KS;
   }
   uint32_t w = T > 1 ? fetch(1) : 0u;
   for (int p = 1; p < T - 1; ++p) {
@@ -499,13 +511,13 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
     const int R = (int)(w & R_MASK);
     int bn;
     const int s = start_min(g, bn);
-    const int v = s + R;
+    const int v = s + (R << KS);
     int* row = ns + bn * RW * B;
     if constexpr (RSHIFT) {   // the shift in registers (predicated FMA-pipe moves)
       int x[GP];
 #pragma unroll
       for (int i = 0; i < GP; ++i) x[i] = row[i * B];
-      place_sorted<GP>(x, g, R, pb.one);
+      place_sorted<GP>(x, g, R << KS, pb.one);
 #pragma unroll
       for (int i = 0; i < GP; ++i) row[i * B] = x[i];
     } else {
@@ -529,9 +541,10 @@ __device__ __forceinline__ int decode_col(const uint32_t* __restrict__ tab, cons
     w = wn;
   }
   // Position T-1 (its word is in w): earliest start + R, no state update.
+  ms >>= KS;
   if (T > 1) {
     int bn;
-    ms = max(ms, start_min((int)(w >> 24), bn) + (int)(w & R_MASK));
+    ms = max(ms, (start_min((int)(w >> 24), bn) >> KS) + (int)(w & R_MASK));
   }
   if constexpr (CHECK == 1) bad = __popc(seen) != T;
   if constexpr (CHECK != 0) {
