@@ -804,22 +804,27 @@ struct GaMinBlocks {
 // stride, later ones are claimed from a counter (n_cand[1], zeroed by the previous elite
 // selection) one iteration before they are needed, so warps that finish early take more
 // (the static stride left SMs idle in the tail -- measured r1: MIX k_ga -11 %, SWEEP -10 %).
+// Only lane 0's `pending` is meaningful (read by the shuffle); the atomic's result is first
+// consumed by the next advance(), not by a select right after it.
 struct WarpChunks {
   unsigned int* work;
   int64_t nthr, next;
-  unsigned int pending;
+  unsigned int pending = 0u;
   int lane;
-  __device__ __forceinline__ unsigned int claim() const { return lane == 0 ? atomicAdd(work, 32u) : 0u; }
+  __device__ __forceinline__ void claim() {
+    if (lane == 0) pending = atomicAdd(work, 32u);
+  }
   __device__ __forceinline__ WarpChunks(int* n_cand, int64_t nthr_, int lane_)
       : work(reinterpret_cast<unsigned int*>(n_cand + 1)), nthr(nthr_), lane(lane_) {
-    next = nthr + (int64_t)__shfl_sync(0xffffffffu, claim(), 0);
-    pending = claim();
+    claim();
+    next = nthr + (int64_t)__shfl_sync(0xffffffffu, pending, 0);
+    claim();
   }
   // the next chunk's base; the one after it is claimed now
   __device__ __forceinline__ int64_t advance() {
     const int64_t b = next;
     next = nthr + (int64_t)__shfl_sync(0xffffffffu, pending, 0);
-    pending = claim();
+    claim();
     return b;
   }
 };
