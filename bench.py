@@ -357,12 +357,16 @@ def quality_leg(sat, torch, local, budget_s, runs):
     for name, s in runs:
         inst = synth.by_name(name, s)
         plan = sat.Plan(inst.node_gpus, local).load_runtime_table(inst.runtime)
-        sc, sq, base = [], [], {}
+        sc, sq, base, per_node = [], [], {}, {}
         for kind in ("max", "min", "optimus", "random"):
             gc, gq = plan.baseline_genome(kind, s)
             sc.append(gc)
             sq.append(gq)
             base[kind] = int(plan.evaluate_host(gc[None], gq[None])[0])
+            if len(inst.node_gpus) > 1:   # the heuristics' own per-node plan (node genes, reading A16)
+                gn = torch.from_numpy(plan.baseline_nodes(kind, s)[None]).cuda()
+                per_node[kind] = int(plan.evaluate_nodes(torch.from_numpy(gc[None]).cuda(),
+                                                         torch.from_numpy(gq[None]).cuda(), gn).cpu()[0])
         cfg = sat.SearchConfig(seed=100 + s, population=1 << 20, max_generations=1 << 30, time_budget_s=budget_s,
                                elites=16, generations_per_epoch=32)
         t0 = time.perf_counter()
@@ -383,7 +387,8 @@ def quality_leg(sat, torch, local, budget_s, runs):
                     "lower_bound": lb, "best_over_lb": (r["makespan"] / lb) if lb else None,
                     "best_lower_bound": b.get("bar_best_lower_bound"),
                     "gap_to_best_lower_bound": ((r["makespan"] - b["bar_best_lower_bound"]) / b["bar_best_lower_bound"])
-                    if b.get("bar_best_lower_bound") else None, "baselines": base})
+                    if b.get("bar_best_lower_bound") else None, "baselines": base,
+                    **({"baselines_per_node": per_node} if per_node else {})})
         del plan
     return out
 

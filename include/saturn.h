@@ -305,11 +305,19 @@ saturn_status saturn_best_plan(saturn_plan *p, saturn_placement *out, uint8_t *g
  * uniform random genome.  Configs: best runtime at the chosen width (ties to the lower UPP
  * index); order: LPT.  Multi-node job groups are drawn with probability GPU_n / sum GPU
  * (PAPER.md:1002).  Exact rules: DESIGN.md "Baselines" / oracle/baselines.py.  On multi-node
- * clusters the per-node job groups fix each job's WIDTH only; the genome carries no node, so
- * the decoder re-picks the node greedily (reading A16).
+ * clusters the genome alone fixes each job's WIDTH; decoded without node genes the decoder
+ * re-picks every node greedily.  The per-node plan the paper's heuristics run is the genome
+ * decoded with saturn_baseline_nodes' node genes (saturn_evaluate_nodes; reading A16).
  * cfg, perm: host uint8 [T].  Host-only (works on host-only handles).  ESTATE without a table. */
 enum { SATURN_BASELINE_MAX = 1, SATURN_BASELINE_MIN = 2, SATURN_BASELINE_OPTIMUS = 3, SATURN_BASELINE_RANDOM = 4 };
 saturn_status saturn_baseline_genome(const saturn_plan *p, int32_t kind, uint64_t seed, uint8_t *cfg, uint8_t *perm);
+
+/* Node genes of a baseline's per-node plan (row f2; "one node at a time", PAPER.md:962,
+ * 1002): node host uint8 [T] (job-id order) -- job t's distributed node when the config
+ * saturn_baseline_genome(kind, seed) chose for it fits that node, else 0xFF (greedy; only
+ * when even its narrowest width exceeds the node); RANDOM: all 0xFF.  Pass with that genome
+ * to saturn_evaluate_nodes.  Host-only.  EINVAL for a bad kind, ESTATE without a table. */
+saturn_status saturn_baseline_nodes(const saturn_plan *p, int32_t kind, uint64_t seed, uint8_t *node);
 
 /* Round introspection (row f1; PAPER.md:241-262 App. algorithm, §4.4) on
  * the loaded workload W:  S = solve(W), M = makespan(S), time = 0; while M > I: W = W after I

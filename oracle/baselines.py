@@ -25,6 +25,12 @@ task; the plan is then built by list scheduling.  Here each baseline yields a GE
       no config at L_t + 1); increment the first argmax; stop early if every gain is -inf;
   RANDOM: the GA's initial genome of slot k (oracle/ga.py) -- uniform config
       per job, uniform order.
+
+baseline_nodes: the baselines decide each job's node ("one node at a time": the per-node
+  allocations of MAX / MIN / OPTIMUS).  As node genes (reading A16) job t
+  runs on its distributed node when its chosen config fits there, else it is placed greedily
+  (0xFF, only when even the job's narrowest width exceeds that node); RANDOM is all greedy.
+  The decoder with these genes yields the per-node plan; without them it re-picks nodes.
 """
 from __future__ import annotations
 
@@ -162,6 +168,18 @@ def optimus_greedy(c, seed: int = 0):
 
 def randomized(c, seed: int = 0, k: int = 0):
     return ga.initial_genome(c.S, seed, 0, k)
+
+
+GREEDY = 0xFF
+
+
+def baseline_nodes(c, kind: str, seed: int = 0):
+    """Node genes (job-id order) of a baseline's per-node plan; see the module docstring."""
+    if kind == "random":
+        return [GREEDY] * c.n_jobs
+    cfg, _ = KINDS[kind](c, seed)
+    node = distribute(c, seed)
+    return [node[t] if c.config(t, cfg[t])[1] <= int(c.node_gpus[node[t]]) else GREEDY for t in range(c.n_jobs)]
 
 
 KINDS = {"max": max_heuristic, "min": min_heuristic, "optimus": optimus_greedy, "random": randomized}

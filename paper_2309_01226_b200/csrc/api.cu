@@ -1800,6 +1800,24 @@ saturn_status saturn_baseline_genome(const saturn_plan* cp, int32_t kind, uint64
   return SATURN_OK;
 }
 
+saturn_status saturn_baseline_nodes(const saturn_plan* cp, int32_t kind, uint64_t seed, uint8_t* node) {
+  saturn_plan* p = const_cast<saturn_plan*>(cp);
+  if (!p || !node) return SATURN_EINVAL;
+  if (!p->loaded) return fail(p, SATURN_ESTATE, "baseline before load_runtime_table");
+  const int T = p->T;
+  if (kind == SATURN_BASELINE_RANDOM) {
+    memset(node, 0xFF, T);
+    return SATURN_OK;
+  }
+  std::vector<uint8_t> cfg(T), perm(T);
+  saturn_status s = saturn_baseline_genome(p, kind, seed, cfg.data(), perm.data());
+  if (s != SATURN_OK) return s;
+  const std::vector<int> nd = distribute_jobs(p, seed);
+  for (int t = 0; t < T; ++t)
+    node[t] = p->cfg_g[t * p->stride + cfg[t]] <= p->gpu_n[nd[t]] ? (uint8_t)nd[t] : (uint8_t)0xFF;
+  return SATURN_OK;
+}
+
 saturn_status saturn_introspect(saturn_plan* p, const saturn_introspect_params* ip, void* stream,
                                 saturn_introspect_result* out, int64_t* round_log) {
   if (!p) return SATURN_EINVAL;

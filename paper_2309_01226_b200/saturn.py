@@ -31,7 +31,7 @@ EXPORTS = (
     "saturn_search_population", "saturn_search_save", "saturn_search_resume", "saturn_best_plan", "saturn_get_unique_id", "saturn_plan_attach_comm",
     "saturn_plan_attach_peers", "saturn_plan_barrier",
     "saturn_partition", "saturn_probe_int_peak", "saturn_set_profiling", "saturn_get_stats",
-    "saturn_reset_stats", "saturn_baseline_genome", "saturn_introspect", "saturn_improve", "saturn_last_error",
+    "saturn_reset_stats", "saturn_baseline_genome", "saturn_baseline_nodes", "saturn_introspect", "saturn_improve", "saturn_last_error",
     "saturn_plan_destroy",
 )
 BASELINES = {"max": 1, "min": 2, "optimus": 3, "random": 4}
@@ -151,6 +151,7 @@ def load_library(path: str = LIB_PATH):
         "saturn_get_stats": [h, P(Stats)],
         "saturn_reset_stats": [h],
         "saturn_baseline_genome": [h, i32, u64, P(u8), P(u8)],
+        "saturn_baseline_nodes": [h, i32, u64, P(u8)],
         "saturn_introspect": [h, P(IntrospectParams), vp, P(IntrospectResult), P(i64)],
         "saturn_improve": [h, P(u8), P(u8), i64, i32, P(i32), vp],
     }
@@ -547,6 +548,14 @@ class Plan:
         self._check(self._lib.saturn_baseline_genome(self._h, BASELINES[kind], int(seed), _np_ptr(c, ctypes.c_uint8),
                                                      _np_ptr(q, ctypes.c_uint8)), "saturn_baseline_genome")
         return c, q
+
+    def baseline_nodes(self, kind: str, seed: int = 0):
+        """Node genes of the baseline's per-node plan (0xFF = greedy); use with
+        baseline_genome(kind, seed) in evaluate_nodes."""
+        n = np.zeros(self.n_jobs, np.uint8)
+        self._check(self._lib.saturn_baseline_nodes(self._h, BASELINES[kind], int(seed), _np_ptr(n, ctypes.c_uint8)),
+                    "saturn_baseline_nodes")
+        return n
 
     def set_profiling(self, on=True):
         """False/0: off; True/1: time every GA generation; n >= 2: every n-th."""

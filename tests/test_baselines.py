@@ -123,3 +123,56 @@ def test_host_only_handle_refuses_device_work():
     assert e.value.status == sat.ESTATE
     with pytest.raises(sat.SaturnError):
         plan.enumerate()
+
+
+# ---------------------------------------------------------------- per-node plans (node genes)
+def test_baseline_nodes_single_node_and_greedy_fallback():
+    """One node: every baseline job is on node 0 and the node-gene decode is the greedy one.
+    Two nodes {4, 2} with a job whose narrowest width is 4: wherever distribute() sends it to
+    the 2-GPU node its gene is 0xFF (greedy), every other gene is the distributed node."""
+    c = _c([8], [[(0, 1, 90), (0, 2, 50), (1, 4, 30)]] * 3)
+    for kind in ("max", "min", "optimus"):
+        cfg, perm = ob.KINDS[kind](c, 0)
+        assert ob.baseline_nodes(c, kind, 0) == [0, 0, 0]
+        assert oracle.decode(c, cfg, perm, node_gene=[0, 0, 0])[0] == oracle.decode(c, cfg, perm)[0]
+    assert ob.baseline_nodes(c, "random", 0) == [0xFF] * 3
+    wide = [(0, 4, 40), (1, 4, 35)]
+    small = [(0, 1, 60), (0, 2, 35)]
+    c = _c([4, 2], [wide, small, wide, small, wide, small])
+    hits = 0
+    for seed in range(20):
+        d = ob.distribute(c, seed)
+        for kind in ("max", "min", "optimus"):
+            nodes = ob.baseline_nodes(c, kind, seed)
+            for t in range(6):
+                if t % 2 == 0 and d[t] == 1:
+                    assert nodes[t] == 0xFF
+                    hits += 1
+                else:
+                    assert nodes[t] == d[t]
+    assert hits > 0
+
+
+@pytest.mark.parametrize("name", ["MIX", "SWEEP"])
+def test_baseline_node_genes_give_per_node_schedules(name):
+    """Decoded with its node genes, every baseline plan is valid (O3) and runs each job on
+    its gene's node: the per-node plan of the paper's heuristics."""
+    inst = synth.by_name(name, 0)
+    c = oracle.compact(inst.node_gpus, inst.runtime)
+    for kind in ("max", "min", "optimus"):
+        cfg, perm = ob.KINDS[kind](c, 2)
+        nodes = ob.baseline_nodes(c, kind, 2)
+        ms, pl = oracle.decode(c, cfg, perm, node_gene=nodes)
+        assert ms > 0 and oracle.validate(c, pl, ms) == []
+        assert all(pl[t]["node"] == nodes[t] for t in range(c.n_jobs) if nodes[t] != 0xFF)
+
+
+def test_library_baseline_nodes_match_oracle():
+    cases = [synth.by_name(n, s) for n in ("TXT", "MIX", "SWEEP") for s in (0, 3)]
+    cases += [synth.sweep(3, n_jobs=30, nodes=nodes) for nodes in ([2, 2, 4, 8], [8, 4], [3, 5], [1, 1, 1])]
+    for inst in cases:
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        plan = _host_plan(inst)
+        for kind in ob.KINDS:
+            for seed in (0, 9):
+                assert list(plan.baseline_nodes(kind, seed)) == ob.baseline_nodes(c, kind, seed), (inst.node_gpus, kind)

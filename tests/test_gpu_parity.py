@@ -492,6 +492,23 @@ def test_node_genes_match_oracle(sat, torch):
         assert np.array_equal(got, oracle.decode_batch(c, cfg, perm))
 
 
+def test_baseline_per_node_plans_match_oracle(sat, torch):
+    """Row f2 with node genes (reading A16): every baseline genome decoded on the device with
+    saturn_baseline_nodes' genes equals the oracle's node-gene decode of the oracle's genome."""
+    from oracle import baselines as ob
+    for inst in (synth.mix(0), synth.sweep(0), synth.sweep(4, n_jobs=30, nodes=[2, 2, 4, 8])):
+        c = oracle.compact(inst.node_gpus, inst.runtime)
+        plan = _plan(sat, inst)
+        for kind in ob.KINDS:
+            for seed in (0, 5):
+                gc, gq = plan.baseline_genome(kind, seed)
+                gn = plan.baseline_nodes(kind, seed)
+                got = plan.evaluate_nodes(torch.from_numpy(gc[None]).cuda(), torch.from_numpy(gq[None]).cuda(),
+                                          torch.from_numpy(gn[None]).cuda()).cpu().numpy()[0]
+                rc, rq = ob.KINDS[kind](c, seed)
+                assert got == oracle.decode(c, rc, rq, node_gene=ob.baseline_nodes(c, kind, seed))[0], (kind, seed)
+
+
 def test_node_gene_space_reaches_the_exact_optimum(sat, torch):
     """Completeness: min over all (cfg, node, perm) genomes, decoded on the
     GPU, equals the independent time-indexed exact optimum (O4a)."""
