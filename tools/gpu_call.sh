@@ -1,5 +1,10 @@
 # scratch GPU call used during round 2 (edited per call)
 set -x
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_r2k.txt 2>&1; echo pytest=$?
-tail -3 gpurun_out/gputest_r2k.txt
-timeout 900 python bench.py > gpurun_out/bench_r2k.json 2> gpurun_out/bench_r2k.err; echo bench=$?
+sed -i 's/population=1 << 22/population=1 << 23/' tools/variant_bench.py
+AB_WORKLOADS="TXT MIX TINY" timeout 1500 bash tools/ab_run.sh gpurun_out/ab_fma.jsonl build_variants/cur/libsaturn.so build_variants/nofma/libsaturn.so build_variants/cur/libsaturn.so build_variants/nofma/libsaturn.so
+python - <<'PY'
+import json
+for f in ['gpurun_out/ab_fma.jsonl']:
+  for l in open(f):
+    d=json.loads(l); print(d['lib'][-22:], d['workload'], 'eval %.4g' % d['evaluate_plans_per_s'], 'step %.4f' % d['step_ms'], 'kga %.4f' % d['ga_kernel_ms'], d['best'])
+PY
