@@ -279,13 +279,22 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
       v = place_sorted<GP>(a[0], g, R, pb.one);
     } else {
       // start of every node: its g-th smallest free time (+inf if it has fewer GPUs)
-      int best = mux<GP>(a[0], g - 1);
+      int best;
       int bn = 0;
       if constexpr (KS) {
+        // min over the nodes slot by slot (3-input VIMNMX3), then one mux: the g-th key of
+        // the min vector is the min over the nodes of their g-th keys
+        int m[GP];
 #pragma unroll
-        for (int n = 1; n < NN; ++n) best = min(best, mux<GP>(a[n], g - 1));
+        for (int i = 0; i < GP; ++i) {
+          m[i] = a[0][i];
+#pragma unroll
+          for (int n = 1; n < NN; ++n) m[i] = min(m[i], a[n][i]);
+        }
+        best = mux<GP>(m, g - 1);
         bn = best & 3;
       } else {
+        best = mux<GP>(a[0], g - 1);
 #pragma unroll
         for (int n = 1; n < NN; ++n) {
           const int st = mux<GP>(a[n], g - 1);
