@@ -68,11 +68,14 @@ def main():
     ap.add_argument('--eval')
     ap.add_argument('--launches')
     ap.add_argument('--enum')
+    ap.add_argument('--sweep', help='k_ga capture at the SWEEP workload (tools/variant_bench.py)')
     ap.add_argument('--workload', default='TXT')
+    ap.add_argument('--merge', action='store_true', help='update the existing summary instead of replacing it')
     args = ap.parse_args()
     outdir = os.path.join(ROOT, 'profiles', args.round)
     os.makedirs(outdir, exist_ok=True)
-    summ = {}
+    path = os.path.join(outdir, 'ncu_summary.json')
+    summ = json.load(open(path)) if args.merge and os.path.exists(path) else {}
     if args.ga:
         summ['k_ga (bench config)'] = summarise(args.ga)
         with open(os.path.join(ROOT, 'profiles', 'roofline_traffic.json'), 'w') as f:
@@ -84,9 +87,11 @@ def main():
         summ['k_evaluate (2^24 genomes)'] = summarise(args.eval)
     if args.enum:
         summ['k_enumerate (TINY-shaped 7 jobs, 1.41e9 genomes)'] = summarise(args.enum)
+    if args.sweep:
+        summ['k_ga (SWEEP 4x8, 2^22 genomes, tools/variant_bench.py)'] = summarise(args.sweep)
     if args.launches:
         summ['launch_list_shares'] = launches(args.launches)
-    with open(os.path.join(outdir, 'ncu_summary.json'), 'w') as f:
+    with open(path, 'w') as f:
         json.dump(summ, f, indent=1)
     print(json.dumps(summ, indent=1))
 
