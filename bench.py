@@ -502,13 +502,14 @@ def main():
         er = ep.enumerate()                      # DFS, prefix sharing + branch and bound
         t_dfs = time.perf_counter() - t0
         t0 = time.perf_counter()
-        fr = ep.enumerate_range(0, er["evaluated"])   # index order, one full decode per genome
+        space = ep.space_size()
+        fr = ep.enumerate_range(0, space)   # index order, one full decode per genome
         t_full = time.perf_counter() - t0
         kernel_only["enumerate"] = {
-            "instance": "TINY-shaped 7 jobs on 1x4 (seed 7)", "genomes": er["evaluated"], "optimum": er["makespan"],
+            "instance": "TINY-shaped 7 jobs on 1x4 (seed 7)", "genomes": space, "optimum": er["makespan"],
             "full_decode_plans_per_s": fr["evaluated"] / t_full,
             "dfs_seconds": t_dfs, "dfs_leaves": er["leaves"], "dfs_leaves_per_s": er["leaves"] / t_dfs,
-            "dfs_genomes_covered_per_s": er["evaluated"] / t_dfs,
+            "dfs_genomes_covered_per_s": space / t_dfs,
             "same_result": (er["makespan"], er["genome_index"]) == (fr["makespan"], fr["genome_index"])}
         # the decode kernel alone against the same ALU roofline (algorithmic ops per plan)
         kernel_only["roofline_thread"] = {"bound": "alu", "achieved": ops * kernel_only["thread"] / 1e12,

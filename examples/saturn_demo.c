@@ -65,8 +65,11 @@ int main(int argc, char **argv) {
   saturn_result r;
   CHECK(saturn_enumerate(plan, (uint64_t)1 << 34, NULL, &r));
   int64_t ms = 0;
+  uint64_t space = 0;
   CHECK(saturn_best_plan(plan, pl, NULL, &ms));
-  printf("exhaustive optimum over %llu genomes (%.3f s):\n", (unsigned long long)r.evaluated, r.seconds);
+  CHECK(saturn_space_size(plan, &space));
+  printf("exhaustive optimum over %llu genomes (%llu leaves visited, %.3f s):\n", (unsigned long long)space,
+         (unsigned long long)r.leaves, r.seconds);
   print_plan(pl, ms);
 
   saturn_search_params sp = {0};

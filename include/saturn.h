@@ -202,9 +202,12 @@ saturn_status saturn_enumerate(saturn_plan *p, uint64_t max_genomes, void *strea
 
 /* saturn_enumerate runs a depth-first enumeration with prefix sharing and a strict
  * branch-and-bound cut (incumbent = the best paper-baseline genome) when T >= 3 and the
- * cluster has a register decoder shape (flags |= SATURN_PREFIX_SHARED; `evaluated` = the
- * genomes accounted for, `leaves` = leaves actually visited); the result is identical to
- * the index-order brute force.  SATURN_ENUM_ODOMETER=1 forces full decodes in index order.
+ * cluster has a register decoder shape (flags |= SATURN_PREFIX_SHARED; `evaluated` = 0: it
+ * performs no full T-step decode (SURVEY.md §8d counting rule: prefix-shared leaves are
+ * reported separately, pruned plans never); `leaves` = leaves actually visited, each a
+ * makespan completed from a shared prefix state; the space covered is saturn_space_size);
+ * the result is identical to the index-order brute force (saturn_enumerate_range(0, space)
+ * does the full decodes in index order).
  *
  * Symmetry reduction (row f4; reading A14): with
  * SATURN_ENUM_SYMMETRY set, jobs whose compacted config lists are the same (g, R) sequence

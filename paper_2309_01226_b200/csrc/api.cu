@@ -917,7 +917,7 @@ static saturn_status enumerate_dfs_impl(saturn_plan* p, uint64_t total, cudaStre
     memset(out, 0, sizeof *out);
     out->makespan = ms;
     out->genome_index = idx;
-    out->evaluated = total;
+    out->evaluated = 0;   // no full T-step decode: leaves are prefix-shared, pruned plans not counted (§8d)
     out->leaves = kl[1];
     out->seconds = now_s() - t0;
     out->flags = SATURN_PROVEN_OPTIMAL | SATURN_PREFIX_SHARED | (reduced ? SATURN_SYMMETRY_REDUCED : 0);
