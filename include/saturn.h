@@ -286,7 +286,8 @@ saturn_status saturn_search_population(const saturn_plan *p, int64_t capacity, u
  * runtime table (any handle on any device; EINVAL otherwise): sp->seed, population and
  * elites must equal the saved ones, the state's island / world must equal this handle's
  * rank / world, and every saved genome must be valid (EINVAL otherwise; also for a bad
- * magic, size or checksum).  sp->max_generations MORE generations are run, numbered from
+ * magic, size or checksum; the saved makespans are trusted, not re-decoded).
+ * sp->max_generations MORE generations are run, numbered from
  * the saved generation + 1 (their Philox streams and epoch boundaries are those the saved
  * search would have used next); sp->seed_cfg / n_seed are ignored.  For one island without
  * the memetic step, search(G1) + save + resume(G2) returns exactly what search(G1 + G2)

@@ -19,3 +19,4 @@ def test_readme_usage_block_runs():
     exec(compile(block, "README.md", "exec"), env)
     assert env["makespan"] > 0 and len(env["placements"]) == 12
     assert env["result"]["e2e_makespan"] <= env["result"]["one_shot_makespan"]
+    assert int(env["ms_optimus"].cpu()[0]) > 0
