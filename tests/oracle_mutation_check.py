@@ -6,7 +6,8 @@ non-strict acceptance, a wrong tie-break or a dropped move family in oracle/loca
 Sattolo's shuffle, a skipped swap or a short config range in oracle/ga.py:initial_genome;
 a reversed tournament or tie-break, a flipped crossover bit, unswapped child roles, a
 reversed LOX fill or unordered cuts, a wrong insertion target or shared child fields in
-oracle/ga.py:make_child)
+oracle/ga.py:make_child; a dropped greedy fallback, a strict fit test or a fixed node
+in oracle/baselines.py:baseline_nodes)
 and confirms that the `-m "not gpu"` pins of that source fail.  The original source is
 restored afterwards.  Result for this round is recorded in DESIGN.md ("Oracle pins").
 """
@@ -24,6 +25,8 @@ LB_SRC = "oracle/bounds.py"
 PINS = "tests/test_oracle_pins.py"
 SEARCH_PINS = "tests/test_oracle_search_pins.py"
 GA_PINS = "tests/test_oracle_ga_pins.py"
+BL_SRC = "oracle/baselines.py"
+BL_PINS = "tests/test_baselines.py::test_baseline_nodes_single_node_and_greedy_fallback"
 
 MUTATIONS = [
     (C_SRC, PINS, "gpu rule smallest-free", "f > free_t[first[best_n] + pick]", "f < free_t[first[best_n] + pick]"),
@@ -64,6 +67,11 @@ MUTATIONS = [
     (LB_SRC, PINS, "job progress counted twice", "A[nK + t, j] = -1.0 / jobs[t][s][1]",
      "A[nK + t, j] = -2.0 / jobs[t][s][1]"),
     (LB_SRC, PINS, "longest-job row dropped", "[(longest, None)]", "[(0, None)]"),
+    (BL_SRC, BL_PINS, "baseline node genes: greedy fallback never applied", "else GREEDY for t in",
+     "else node[t] for t in"),
+    (BL_SRC, BL_PINS, "baseline node genes: fit test strict", "<= int(c.node_gpus[node[t]])",
+     "< int(c.node_gpus[node[t]])"),
+    (BL_SRC, BL_PINS, "random baseline pinned to node 0", "return [GREEDY] * c.n_jobs", "return [0] * c.n_jobs"),
 ]
 
 
