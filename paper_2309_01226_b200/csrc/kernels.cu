@@ -1115,17 +1115,20 @@ __global__ void __launch_bounds__(GA_B, GaMinBlocks<NN, GP>::value)
         } else {
           // Rows of lanes without a child hold stale bytes: the word index is clamped so
           // those lanes stay inside this thread's ceil(T/32) words.
-          for (int w = 0; w < nb; ++w) inA[w * GA_B] = 0u;
+          // the complemented set (bit x set <=> gene x is taken), all clear when nothing
+          // is taken: the fill's test is one rotate + one AND-to-predicate
+          const uint32_t init = (xo && child) ? 0xffffffffu : 0u;
+          for (int w = 0; w < nb; ++w) inA[w * GA_B] = init;
           for (int k = (int)a; k <= (int)b; ++k) {
             const int x = ch.q(k);
-            inA[min(x >> 5, nb - 1) * GA_B] |= 1u << (x & 31);
+            inA[min(x >> 5, nb - 1) * GA_B] &= ~(1u << (x & 31));
           }
-          const uint32_t xm = (xo && child) ? 1u : 0u;
           const auto fill = [&](int x) {
-            const uint32_t take = (~inA[min(x >> 5, nb - 1) * GA_B] >> (x & 31)) & xm;
+            const uint32_t w = inA[min(x >> 5, nb - 1) * GA_B];
+            const uint32_t take = __funnelshift_r(w, w, x) & 1u;
             if (take) *wp = (uint8_t)x;
             wp += take;
-            wp = (wp == pa) ? wp + gap : wp;
+            if (wp == pa) wp += gap;
           };
           if constexpr (STAGE) {   // Y's permutation from the staged words
             for (int k = 0; k < T; k += 4) {
