@@ -262,8 +262,9 @@ __device__ __forceinline__ int decode_sorted_impl(const uint32_t* __restrict__ t
   // Positions 1 .. T-2: the full update.  The next position's config word is fetched one
   // step ahead (its three dependent shared-memory loads -- perm byte, cfg byte, table word
   // -- overlap this step's arithmetic instead of stalling the next one).
-  // (Not for 4-node states: their 128 registers leave no room -- measured SWEEP k_ga +1.6 %.)
-  constexpr bool AHEAD = NN <= 2;
+  // (4-node states: +1.6 % SWEEP k_ga in r1 at 128 registers; -0.6 % since the node keys and
+  // the min-then-mux node choice freed registers, r2.)
+  constexpr bool AHEAD = NN <= 4;
   uint32_t w = (AHEAD && T > 1) ? fetch(1) : 0u;
   // Unrolled by two (the loop counter and its compare once per two steps): SWEEP k_ga -2.8 %,
   // TXT / MIX equal (r2).  First-stage shift lanes as ALU selects instead of IMAD pairs:
